@@ -1,0 +1,116 @@
+/*
+ * pasa_b200.h -- C-ABI of the B200-native PASA forward (libpasa_b200.so).
+ *
+ * Plain C types only: device or host pointers, sizes, a status code.  Every
+ * entry point replaces one piece of the reference C++ operator API in
+ * /root/reference/proj (citations are include/pasa/<file>:<line> or
+ * src/<file>:<line>); INTEGRATION.md shows the bindings a maintainer adds.
+ *
+ * Layouts (reference tensor.hpp:13-29): Q is (B, Hq, S1, d), K and V are
+ * (B, Hkv, S2, d), O is (B, Hq, S1, d); dense row-major BHSD, IEEE binary16
+ * (the reference carries FP16-exact values in doubles, tensor.hpp:19-20).
+ * Hq == Hkv reproduces the reference; Hq % Hkv == 0 adds grouped-query heads.
+ *
+ * Status codes: 0 success, otherwise one of PASA_B200_E* (negative).  The
+ * reference throws std::invalid_argument for the same conditions
+ * (pasa.cpp:200-211, tensor.cpp:19-55); pasa_b200_last_error() returns the
+ * message of the last failure on the calling thread.  NaN/Inf in the OUTPUT
+ * are results, not errors.
+ */
+#ifndef PASA_B200_H_
+#define PASA_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PASA_B200_API __attribute__((visibility("default")))
+#else
+#define PASA_B200_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PASA_B200_OK 0
+#define PASA_B200_EINVAL -1      /* shape / parameter violation (invalid_argument) */
+#define PASA_B200_EUNSUPPORTED -2 /* valid for the reference, not for this build   */
+#define PASA_B200_ECUDA -3       /* CUDA runtime error                            */
+#define PASA_B200_ENODEV -4      /* no sm_100 device                              */
+
+/* Problem + parameters: AttentionProblem (tensor.hpp:41-51) + PasaParams
+ * (pasa.hpp:57-64) + the causal extension.  The shifting matrix M is not
+ * passed: it is fully determined by (s2, beta, alpha) at FP16
+ * (pasa.cpp:97-108, built by bench.cpp:196 with Prec::FP16). */
+typedef struct pasa_b200_desc {
+  int32_t batch;     /* B                                                      */
+  int32_t heads_q;   /* Hq                                                     */
+  int32_t heads_kv;  /* Hkv; must divide Hq (reference requires equality)      */
+  int32_t seq_q;     /* S1, multiple of s1                                     */
+  int32_t seq_kv;    /* S2, multiple of s2                                     */
+  int32_t head_dim;  /* d in {64, 128}                                         */
+  int32_t s1;        /* query block; numerically irrelevant, multiple of 128 or a divisor of it */
+  int32_t s2;        /* KV block = shifting-matrix size; this build: 128       */
+  int32_t causal;    /* 0: reference semantics; 1: causal (requires S1 == S2) */
+  int32_t reserved;
+  double beta;       /* shift fraction in (0, 1) (pasa.cpp:98-101)              */
+  double alpha;      /* static scale, must equal sqrt(d) (pasa.cpp:206-208)     */
+} pasa_b200_desc;
+
+/* Optional device-side counters, accumulated atomically (RunDiagnostics,
+ * attention.hpp:30-48).  Pass NULL to skip. */
+typedef struct pasa_b200_diag {
+  unsigned long long out_nonfinite;
+  unsigned long long out_total;
+} pasa_b200_diag;
+
+/* Library version (major*10000 + minor*100 + patch). */
+PASA_B200_API int pasa_b200_version(void);
+
+/* Message of the last failing call on this thread ("" if none). */
+PASA_B200_API const char* pasa_b200_last_error(void);
+
+/* The two distinct entries of the shifting matrix M, as binary16 bit
+ * patterns: diag = fl16((1 - beta/s2)/alpha), off = fl16(-beta/(alpha*s2)).
+ * Replaces build_shifting_matrix (pasa.hpp:27-28, pasa.cpp:16-35) /
+ * PasaParams::make (pasa.cpp:97-108) with prec = FP16. */
+PASA_B200_API int pasa_b200_shift_entries(int32_t s2, double beta, double alpha, uint16_t* diag_f16,
+                            uint16_t* off_f16);
+
+/* Validate a descriptor exactly like make_problem (tensor.cpp:19-55) and
+ * pasa_attention (pasa.cpp:200-211); 0 if the fused path accepts it. */
+PASA_B200_API int pasa_b200_check(const pasa_b200_desc* desc);
+
+/* Bytes of device workspace pasa_b200_attention_fwd needs (K' for every KV
+ * head and block, plus per-head statistics). */
+PASA_B200_API size_t pasa_b200_workspace_size(const pasa_b200_desc* desc);
+
+/* Key pre-pass K'_j = K_j^T M for every (b, kv head, j) (pasa.cpp:53-56, the
+ * loop at :231-240), device pointers, stream-ordered.  Output layout is
+ * K-major: kp[(b, h, j*s2 + c), t] = K'_j[t][c].  lscale = 1 gives the
+ * reference's bits exactly (FP32 sequential accumulate, one FP16 rounding);
+ * the fused path uses lscale = log2(e).  vmax (nullable, B*Hkv floats) gets
+ * max|V| per head when v is non-NULL. */
+PASA_B200_API int pasa_b200_preprocess_keys(const pasa_b200_desc* desc, const void* k, const void* v,
+                              void* kp, float* vmax, float lscale, void* stream);
+
+/* The PASA forward, device pointers, stream-ordered, asynchronous.
+ * Replaces pasa::pasa_attention (pasa.hpp:95-99, pasa.cpp:196-293) for the
+ * PASA_FP16 policy.  workspace must hold pasa_b200_workspace_size() bytes.
+ * stream is a cudaStream_t (NULL = legacy default stream). */
+PASA_B200_API int pasa_b200_attention_fwd(const pasa_b200_desc* desc, const void* q, const void* k,
+                            const void* v, void* o, void* workspace, size_t workspace_bytes,
+                            pasa_b200_diag* diag, void* stream);
+
+/* Same, from HOST buffers (binary16 bit patterns): copies in, runs, copies
+ * O back and synchronizes.  The drop-in for a CPU caller of pasa_attention
+ * (the reference's `sweep`, bench.cpp:224). */
+PASA_B200_API int pasa_b200_attention_host(const pasa_b200_desc* desc, const uint16_t* q, const uint16_t* k,
+                             const uint16_t* v, uint16_t* o);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif /* PASA_B200_H_ */

@@ -530,7 +530,7 @@ ORC_API int orc_pasa_ref(const orc_shape* sh, const double* q, const double* k,
 /* exact in real arithmetic:                                                 */
 /*  - every score lives in the L domain (lscale = log2 e: 2^x replaces e^x), */
 /*  - row statistics (sum of S', mean, F, corrections, running max, l) are   */
-/*    FP32; the S' row sum runs as two chains (even / odd columns),          */
+/*    FP32; the S' and P row sums run as two chains (even / odd columns),    */
 /*  - F_j = F_{j-1} + (Sbar - F_{j-1}) / j (no (j-1)*F product),             */
 /*  - e_cur is folded into P: P = 2^(fl16(S' - c_j) ) with                   */
 /*    c_j = fl16(m_j - dm_cur + c0), c0 >= 0 a per-head inflation that      */
@@ -643,13 +643,15 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
           const float earg = (m[r] + dmp) - mnew;
           ep = fl16(log2dom ? exp2((double)earg) : exp((double)earg));
         }
-        float lloc = 0.f;
+        float le = 0.f, lo = 0.f; /* two chains: even / odd columns */
         for (size_t c = 0; c < s2; ++c) {
           const int masked = sh->causal && (j * s2 + c > pos);
           const double a = fl16(S[c] - cj);
           S[c] = masked ? 0.0 : fl16(log2dom ? exp2(a) : exp(a));
-          lloc = lloc + (float)S[c];
+          if (c & 1) lo = lo + (float)S[c];
+          else le = le + (float)S[c];
         }
+        const float lloc = le + lo;
         l[r] = (jc == 1) ? lloc : (float)ep * l[r] + lloc;
         double* orow = oacc + r * d;
         for (size_t n = 0; n < d; ++n) {

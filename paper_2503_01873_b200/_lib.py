@@ -1,0 +1,78 @@
+"""ctypes binding of the C-ABI in include/pasa_b200.h (libpasa_b200.so).
+
+Loading the library needs no GPU; every compute entry point does.  There is no
+fallback: if the library is missing, ``load()`` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(PKG, "_build", "libpasa_b200.so")
+HEADER = os.path.join(os.path.dirname(PKG), "include", "pasa_b200.h")
+
+OK, EINVAL, EUNSUPPORTED, ECUDA, ENODEV = 0, -1, -2, -3, -4
+
+
+class Desc(C.Structure):
+    """Mirror of ``pasa_b200_desc``."""
+
+    _fields_ = [
+        ("batch", C.c_int32), ("heads_q", C.c_int32), ("heads_kv", C.c_int32),
+        ("seq_q", C.c_int32), ("seq_kv", C.c_int32), ("head_dim", C.c_int32),
+        ("s1", C.c_int32), ("s2", C.c_int32), ("causal", C.c_int32),
+        ("reserved", C.c_int32), ("beta", C.c_double), ("alpha", C.c_double),
+    ]
+
+
+class Diag(C.Structure):
+    _fields_ = [("out_nonfinite", C.c_ulonglong), ("out_total", C.c_ulonglong)]
+
+
+_LIB = None
+
+
+def exported_symbols_from_header() -> list[str]:
+    """Every function the public header declares."""
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"PASA_B200_API\s+[\w\s\*]*?\b(pasa_b200_\w+)\s*\(", text)))
+
+
+def load(path: str = SO) -> C.CDLL:
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise FileNotFoundError(
+            f"{path} is missing: build it with `python -m paper_2503_01873_b200.build` "
+            "(there is no CPU fallback)")
+    L = C.CDLL(path)
+    vp, dp = C.c_void_p, C.POINTER(Desc)
+    L.pasa_b200_version.restype = C.c_int
+    L.pasa_b200_last_error.restype = C.c_char_p
+    L.pasa_b200_shift_entries.argtypes = [C.c_int32, C.c_double, C.c_double,
+                                          C.POINTER(C.c_uint16), C.POINTER(C.c_uint16)]
+    L.pasa_b200_check.argtypes = [dp]
+    L.pasa_b200_workspace_size.restype = C.c_size_t
+    L.pasa_b200_workspace_size.argtypes = [dp]
+    L.pasa_b200_preprocess_keys.argtypes = [dp, vp, vp, vp, vp, C.c_float, vp]
+    L.pasa_b200_attention_fwd.argtypes = [dp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp]
+    L.pasa_b200_attention_host.argtypes = [dp, vp, vp, vp, vp]
+    _LIB = L
+    return L
+
+
+class PasaError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+def check(rc: int) -> None:
+    if rc != OK:
+        msg = load().pasa_b200_last_error().decode()
+        if rc == EINVAL:
+            raise ValueError(msg)  # the reference's std::invalid_argument
+        raise PasaError(rc, msg)

@@ -1,0 +1,305 @@
+"""Python mirror of the reference PASA operator API, over the C-ABI.
+
+Same names, argument meaning and error behaviour as the reference C++ surface
+(/root/reference/proj/include/pasa/*.hpp):
+
+=====================================  =========================================
+reference                              here
+=====================================  =========================================
+``Prec``, ``PolicyId``,                ``Prec``, ``PolicyId``, ``PrecisionPolicy``,
+``PrecisionPolicy``, ``policy_for``    ``policy_for``       (precision.hpp:16-56)
+``AttnOptions``, ``RunDiagnostics``    same                 (attention.hpp:16-48)
+``build_shifting_matrix``              same                 (pasa.hpp:23-28)
+``PasaParams::make``                   ``PasaParams.make``  (pasa.hpp:57-64)
+``make_problem`` / ``AttentionProblem`` same                (tensor.hpp:41-56)
+``preprocess_keys``                    same, batched on device (pasa.hpp:34-36)
+``pasa_attention``                     same                 (pasa.hpp:92-99)
+=====================================  =========================================
+
+Tensors are torch fp16 tensors in BHSD layout.  CUDA tensors run in place on
+their stream; host tensors go through ``pasa_b200_attention_host`` (copy in,
+compute, copy out).  There is no CPU fallback: without the CUDA library or a
+device every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+
+BETA_STAR = 0.984497  # optimal beta for s2=128, FP16 (bench.hpp:93)
+LOG2E = 1.4426950408889634
+
+
+class Prec(enum.IntEnum):
+    FP64 = 0
+    FP32 = 1
+    FP16 = 2
+
+
+class PolicyId(enum.IntEnum):
+    GOLDEN_FP64 = 0
+    FA_FP32 = 1
+    FA_PARTIAL_FP16 = 2
+    FA_FULL_FP16 = 3
+    PASA_FP16 = 4
+
+
+@dataclass(frozen=True)
+class PrecisionPolicy:
+    id: PolicyId = PolicyId.GOLDEN_FP64
+    gemm_accum: Prec = Prec.FP64
+    gemm_store: Prec = Prec.FP64
+    vector_prec: Prec = Prec.FP64
+
+
+def policy_for(pid: PolicyId) -> PrecisionPolicy:
+    """precision.cpp:23-38."""
+    table = {
+        PolicyId.GOLDEN_FP64: (Prec.FP64, Prec.FP64, Prec.FP64),
+        PolicyId.FA_FP32: (Prec.FP32, Prec.FP32, Prec.FP32),
+        PolicyId.FA_PARTIAL_FP16: (Prec.FP32, Prec.FP16, Prec.FP16),
+        PolicyId.FA_FULL_FP16: (Prec.FP16, Prec.FP16, Prec.FP16),
+        PolicyId.PASA_FP16: (Prec.FP32, Prec.FP16, Prec.FP16),
+    }
+    return PrecisionPolicy(pid, *table[PolicyId(pid)])
+
+
+class M0Mode(enum.IntEnum):
+    NEG_INF = 0
+    ZERO = 1
+
+
+@dataclass
+class AttnOptions:
+    """attention.hpp:21-25, plus the causal-mask extension (SPEC.md:189 has none)."""
+
+    m0: M0Mode = M0Mode.NEG_INF  # ignored by PASA, as in the reference (pasa.cpp:141-147)
+    threads: int = 0             # accepted for API parity; the GPU ignores it
+    diagnose: bool = False
+    causal: bool = False
+    check_finite: bool = True    # make_problem's finiteness rule (tensor.cpp:39-46)
+
+
+@dataclass
+class RunDiagnostics:
+    """attention.hpp:30-48 (the output counters are filled)."""
+
+    store_finite_min: float = math.inf
+    store_finite_max: float = -math.inf
+    store_pos_inf: int = 0
+    store_neg_inf: int = 0
+    store_nan: int = 0
+    out_nonfinite: int = 0
+    out_total: int = 0
+    has_fp64_ranges: bool = False
+
+    def merge(self, o: "RunDiagnostics") -> None:
+        self.store_finite_min = min(self.store_finite_min, o.store_finite_min)
+        self.store_finite_max = max(self.store_finite_max, o.store_finite_max)
+        self.store_pos_inf += o.store_pos_inf
+        self.store_neg_inf += o.store_neg_inf
+        self.store_nan += o.store_nan
+        self.out_nonfinite += o.out_nonfinite
+        self.out_total += o.out_total
+        self.has_fp64_ranges = self.has_fp64_ranges or o.has_fp64_ranges
+
+
+def _f16_bits_to_float(u: int) -> float:
+    return float(np.array([u], dtype=np.uint16).view(np.float16)[0])
+
+
+def shift_entries(s2: int, beta: float, alpha: float) -> tuple[float, float]:
+    """(diag, off) of M at FP16 (pasa.cpp:26-27), computed by the C-ABI."""
+    d, o = C.c_uint16(), C.c_uint16()
+    _lib.check(_lib.load().pasa_b200_shift_entries(s2, beta, alpha, C.byref(d), C.byref(o)))
+    return _f16_bits_to_float(d.value), _f16_bits_to_float(o.value)
+
+
+def build_shifting_matrix(s2: int, beta: float, alpha: float, prec: Prec = Prec.FP16) -> np.ndarray:
+    """M = I/alpha - beta*J/(alpha*s2), each entry rounded once (pasa.cpp:16-35)."""
+    if prec != Prec.FP16:
+        n = float(s2)
+        diag, off = (1.0 - beta / n) / alpha, -beta / (alpha * n)
+        if prec == Prec.FP32:
+            diag, off = float(np.float32(diag)), float(np.float32(off))
+    else:
+        diag, off = shift_entries(s2, beta, alpha)
+    m = np.full((s2, s2), off)
+    np.fill_diagonal(m, diag)
+    return m
+
+
+@dataclass
+class PasaParams:
+    """pasa.hpp:57-64; ``m`` is materialised lazily (only its 2 entries matter)."""
+
+    beta: float = 0.0
+    alpha: float = 1.0
+    s2: int = 0
+    prec: Prec = Prec.FP16
+    _m: np.ndarray | None = field(default=None, repr=False)
+
+    @staticmethod
+    def make(s2: int, beta: float, alpha: float, prec: Prec = Prec.FP16) -> "PasaParams":
+        if beta < 0.0 or beta >= 1.0:  # pasa.cpp:98-101
+            raise ValueError("pasa params: beta must lie in [0, 1); beta == 1 has no recovery")
+        return PasaParams(beta=beta, alpha=alpha, s2=s2, prec=prec)
+
+    @property
+    def m(self) -> np.ndarray:
+        if self._m is None:
+            self._m = build_shifting_matrix(self.s2, self.beta, self.alpha, self.prec)
+        return self._m
+
+
+@dataclass
+class AttentionProblem:
+    """tensor.hpp:41-51: Q (B,Hq,S1,d), K/V (B,Hkv,S2,d), block sizes, alpha = sqrt(d)."""
+
+    q: torch.Tensor
+    k: torch.Tensor
+    v: torch.Tensor
+    s1: int
+    s2: int
+    alpha: float
+
+    def seq_q(self) -> int:
+        return self.q.shape[2]
+
+    def seq_kv(self) -> int:
+        return self.k.shape[2]
+
+    def q_blocks(self) -> int:
+        return self.seq_q() // self.s1
+
+    def kv_blocks(self) -> int:
+        return self.seq_kv() // self.s2
+
+
+def _as_f16(t) -> torch.Tensor:
+    if isinstance(t, np.ndarray):
+        t = torch.from_numpy(np.ascontiguousarray(t))
+    if t.dtype != torch.float16:
+        t = t.to(torch.float16)
+    return t.contiguous()
+
+
+def make_problem(q, k, v, s1: int, s2: int, check_finite: bool = True) -> AttentionProblem:
+    """Validation rules of tensor.cpp:19-55 (GQA: Hkv may divide Hq)."""
+    q, k, v = _as_f16(q), _as_f16(k), _as_f16(v)
+    if q.dim() != 4 or q.numel() == 0:
+        raise ValueError("problem: empty query tensor")
+    B, Hq, S1, d = q.shape
+    if k.dim() != 4 or k.shape[0] != B or k.shape[3] != d or k.shape[1] == 0 or Hq % k.shape[1]:
+        raise ValueError("problem: K shape does not match Q")
+    if tuple(v.shape) != tuple(k.shape):
+        raise ValueError("problem: V shape does not match K")
+    S2 = k.shape[2]
+    if s1 == 0 or s2 == 0 or S1 % s1 or S2 % s2:
+        raise ValueError(
+            f"problem: sequence lengths must be nonzero multiples of the block sizes (S1={S1}, "
+            f"s1={s1}, S2={S2}, s2={s2}); ragged inputs are rejected, use truncation explicitly")
+    if check_finite:
+        for t in (q, k, v):
+            if not bool(torch.isfinite(t).all()):
+                raise ValueError("problem: input tensors must be finite in the input precision")
+    return AttentionProblem(q, k, v, s1, s2, math.sqrt(float(d)))
+
+
+def _desc(q: torch.Tensor, k: torch.Tensor, s1: int, s2: int, beta: float, alpha: float,
+          causal: bool) -> _lib.Desc:
+    B, Hq, S1, d = q.shape
+    return _lib.Desc(B, Hq, k.shape[1], S1, k.shape[2], d, s1, s2, int(causal), 0, beta, alpha)
+
+
+_WS: dict[tuple[int, int], torch.Tensor] = {}
+
+
+def workspace_for(desc: _lib.Desc, device: torch.device) -> torch.Tensor:
+    n = _lib.load().pasa_b200_workspace_size(C.byref(desc))
+    key = (device.index or 0, n)
+    ws = _WS.get(key)
+    if ws is None:
+        ws = torch.empty(n, dtype=torch.uint8, device=device)
+        _WS[key] = ws
+    return ws
+
+
+def pasa_attention_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, beta: float = BETA_STAR,
+                       causal: bool = False, s1: int = 128, s2: int = 128,
+                       out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+                       stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Device entry point: fp16 CUDA tensors (BHSD), asynchronous on ``stream``."""
+    L = _lib.load()
+    if not (q.is_cuda and k.is_cuda and v.is_cuda):
+        raise ValueError("pasa_attention_fwd expects CUDA tensors; use pasa_attention for host data")
+    q, k, v = (t if t.is_contiguous() else t.contiguous() for t in (q, k, v))
+    desc = _desc(q, k, s1, s2, beta, math.sqrt(float(q.shape[-1])), causal)
+    _lib.check(L.pasa_b200_check(C.byref(desc)))
+    if out is None:
+        out = torch.empty_like(q)
+    if workspace is None:
+        workspace = workspace_for(desc, q.device)
+    st = (stream or torch.cuda.current_stream(q.device)).cuda_stream
+    _lib.check(L.pasa_b200_attention_fwd(C.byref(desc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                         out.data_ptr(), workspace.data_ptr(), workspace.numel(),
+                                         None, st))
+    return out
+
+
+def preprocess_keys(k: torch.Tensor, params: PasaParams, lscale: float = 1.0,
+                    v: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Batched K'_j = K_j^T M on device (pasa.cpp:53-56, loop :231-240).
+
+    Returns (kp, vmax) with kp in the K-major layout kp[b,h,j*s2+c,t] = K'_j[t][c];
+    ``lscale=1`` reproduces the reference's bits."""
+    L = _lib.load()
+    B, H, S2, d = k.shape
+    desc = _lib.Desc(B, H, H, S2, S2, d, params.s2, params.s2, 0, 0, params.beta, params.alpha)
+    kp = torch.empty_like(k)
+    vmax = torch.zeros(B * H, dtype=torch.float32, device=k.device)
+    st = torch.cuda.current_stream(k.device).cuda_stream
+    _lib.check(L.pasa_b200_preprocess_keys(C.byref(desc), k.data_ptr(),
+                                           v.data_ptr() if v is not None else None,
+                                           kp.data_ptr(), vmax.data_ptr(), lscale, st))
+    return kp, vmax
+
+
+def pasa_attention(problem: AttentionProblem, params: PasaParams,
+                   policy: PrecisionPolicy | PolicyId = PolicyId.PASA_FP16,
+                   opts: AttnOptions | None = None,
+                   diag: RunDiagnostics | None = None) -> torch.Tensor:
+    """pasa.hpp:95-99 on the B200.  Only the PASA_FP16 policy runs on the device;
+    any other policy raises (the FP64/FP32 policies live in the CPU oracle)."""
+    opts = opts or AttnOptions()
+    pol = policy if isinstance(policy, PrecisionPolicy) else policy_for(policy)
+    if params.s2 != problem.s2:
+        raise ValueError("pasa: params.s2 does not match the problem")
+    if params.alpha != problem.alpha:
+        raise ValueError("pasa: params.alpha does not match sqrt(d)")
+    if params.beta == 1.0:
+        raise ValueError("pasa: beta == 1 has no recovery")
+    if pol.id != PolicyId.PASA_FP16:
+        raise ValueError(f"pasa_attention on B200 implements PASA_FP16 only, got {pol.id.name}")
+    q, k, v = problem.q, problem.k, problem.v
+    if q.is_cuda:
+        out = pasa_attention_fwd(q, k, v, params.beta, opts.causal, problem.s1, problem.s2)
+    else:
+        L = _lib.load()
+        desc = _desc(q, k, problem.s1, problem.s2, params.beta, problem.alpha, opts.causal)
+        out = torch.empty_like(q)
+        qn, kn, vn = (t.contiguous().view(torch.int16) for t in (q, k, v))
+        _lib.check(L.pasa_b200_attention_host(C.byref(desc), qn.data_ptr(), kn.data_ptr(),
+                                              vn.data_ptr(), out.view(torch.int16).data_ptr()))
+    if diag is not None:
+        d = RunDiagnostics(out_total=out.numel(),
+                           out_nonfinite=int((~torch.isfinite(out)).sum().item()))
+        diag.merge(d)
+    return out

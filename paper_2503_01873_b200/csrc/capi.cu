@@ -1,0 +1,269 @@
+// capi.cu -- the C-ABI of libpasa_b200.so (declared in include/pasa_b200.h).
+//
+// Host side of the drop-in boundary: argument validation with the reference's
+// rules (tensor.cpp:19-55, pasa.cpp:200-211), the shifting-matrix scalars
+// (pasa.cpp:16-35), TMA descriptors, workspace carving and the two launches
+// (key pre-pass, fused forward).  No exceptions cross the ABI.
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/pasa_b200.h"
+#include "pasa_kernels.cuh"
+
+namespace pasa_b200 {
+cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stream);
+cudaError_t launch_fwd(int D, bool causal, const CUtensorMap& tq, const CUtensorMap& tk,
+                       const CUtensorMap& tv, const FwdParams& p, cudaStream_t stream);
+}  // namespace pasa_b200
+
+using namespace pasa_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(PASA_B200_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+constexpr double kLog2e = 1.4426950408889634;
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// ---------------------------------------------------------------- TMA encode
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 3-D view {d, seq, batch*heads} of a BHSD fp16 tensor, box {64, 128, 1}, 128B swizzle.
+int make_tmap(CUtensorMap* m, const void* base, int d, int seq, int bh) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return fail(PASA_B200_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(seq),
+                        static_cast<cuuint64_t>(bh)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(d) * 2,
+                           static_cast<cuuint64_t>(d) * 2 * static_cast<cuuint64_t>(seq)};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(kTile), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PASA_B200_ECUDA, "cuTensorMapEncodeTiled failed");
+  return PASA_B200_OK;
+}
+
+int check_desc(const pasa_b200_desc* d) {
+  if (!d) return fail(PASA_B200_EINVAL, "desc is NULL");
+  if (d->batch <= 0 || d->heads_q <= 0 || d->seq_q <= 0 || d->head_dim <= 0)
+    return fail(PASA_B200_EINVAL, "problem: empty query tensor");  // tensor.cpp:20-22
+  if (d->heads_kv <= 0 || d->heads_q % d->heads_kv != 0)
+    return fail(PASA_B200_EINVAL, "problem: K heads must divide Q heads");  // tensor.cpp:24-26 (+GQA)
+  if (d->seq_kv <= 0) return fail(PASA_B200_EINVAL, "problem: V shape does not match K");
+  if (d->s1 <= 0 || d->s2 <= 0 || d->seq_q % d->s1 != 0 || d->seq_kv % d->s2 != 0)
+    return fail(PASA_B200_EINVAL,
+                "problem: sequence lengths must be nonzero multiples of the block sizes (S1=" +
+                    std::to_string(d->seq_q) + ", s1=" + std::to_string(d->s1) +
+                    ", S2=" + std::to_string(d->seq_kv) + ", s2=" + std::to_string(d->s2) +
+                    "); ragged inputs are rejected, use truncation explicitly");  // tensor.cpp:31-38
+  if (!(d->beta >= 0.0 && d->beta < 1.0))
+    return fail(PASA_B200_EINVAL, "pasa params: beta must lie in [0, 1); beta == 1 has no recovery");
+  if (d->alpha != std::sqrt(static_cast<double>(d->head_dim)))
+    return fail(PASA_B200_EINVAL, "pasa: params.alpha does not match sqrt(d)");  // pasa.cpp:206-208
+  // ---- limits of this build (valid for the reference, unsupported here)
+  if (d->beta == 0.0)
+    return fail(PASA_B200_EUNSUPPORTED,
+                "beta == 0 routes to flash_attention (pasa.cpp:212-221); not in this build");
+  if (d->head_dim != 64 && d->head_dim != 128)
+    return fail(PASA_B200_EUNSUPPORTED, "head_dim must be 64 or 128");
+  if (d->s2 != kTile) return fail(PASA_B200_EUNSUPPORTED, "s2 must be 128");
+  if (d->seq_q % kTile != 0 || d->seq_kv % kTile != 0)
+    return fail(PASA_B200_EUNSUPPORTED, "S1 and S2 must be multiples of 128");
+  if (d->causal && d->seq_q != d->seq_kv)
+    return fail(PASA_B200_EUNSUPPORTED, "causal requires S1 == S2");
+  return PASA_B200_OK;
+}
+
+void shift_scalars(int s2, double beta, double alpha, __half* diag, __half* off) {
+  const double n = static_cast<double>(s2);
+  *diag = __double2half((1.0 - beta / n) / alpha);  // pasa.cpp:26 (RNE)
+  *off = __double2half(-beta / (alpha * n));        // pasa.cpp:27
+}
+
+size_t kp_bytes(const pasa_b200_desc* d) {
+  return static_cast<size_t>(d->batch) * d->heads_kv * d->seq_kv * d->head_dim * 2;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pasa_b200_version(void) { return 100; }
+
+const char* pasa_b200_last_error(void) { return g_last_error.c_str(); }
+
+int pasa_b200_shift_entries(int32_t s2, double beta, double alpha, uint16_t* diag_f16,
+                            uint16_t* off_f16) {
+  if (s2 <= 0) return fail(PASA_B200_EINVAL, "shifting matrix: s2 must be >= 1");
+  if (beta < 0.0 || beta > 1.0) return fail(PASA_B200_EINVAL, "shifting matrix: beta must lie in [0, 1]");
+  if (!(alpha > 0.0)) return fail(PASA_B200_EINVAL, "shifting matrix: alpha must be positive");
+  __half dg, of;
+  shift_scalars(s2, beta, alpha, &dg, &of);
+  std::memcpy(diag_f16, &dg, 2);
+  std::memcpy(off_f16, &of, 2);
+  return PASA_B200_OK;
+}
+
+int pasa_b200_check(const pasa_b200_desc* desc) {
+  g_last_error.clear();
+  return check_desc(desc);
+}
+
+size_t pasa_b200_workspace_size(const pasa_b200_desc* d) {
+  if (!d || d->batch <= 0 || d->heads_kv <= 0 || d->seq_kv <= 0 || d->head_dim <= 0) return 0;
+  return align_up(kp_bytes(d), 256) + align_up(static_cast<size_t>(d->batch) * d->heads_kv * 4, 256);
+}
+
+int pasa_b200_preprocess_keys(const pasa_b200_desc* d, const void* k, const void* v, void* kp,
+                              float* vmax, float lscale, void* stream) {
+  g_last_error.clear();
+  if (!d || !k || !kp) return fail(PASA_B200_EINVAL, "preprocess_keys: NULL argument");
+  if (d->head_dim != 64 && d->head_dim != 128)
+    return fail(PASA_B200_EUNSUPPORTED, "head_dim must be 64 or 128");
+  if (d->s2 != kTile || d->seq_kv % kTile != 0)
+    return fail(PASA_B200_EUNSUPPORTED, "s2 must be 128 and divide S2");
+  if (!(d->beta >= 0.0 && d->beta <= 1.0) || !(d->alpha > 0.0))
+    return fail(PASA_B200_EINVAL, "shifting matrix: invalid beta/alpha");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  __half dg, of;
+  shift_scalars(d->s2, d->beta, d->alpha, &dg, &of);
+  KprepParams p{};
+  p.k = static_cast<const uint16_t*>(k);
+  p.v = static_cast<const uint16_t*>(v ? v : k);
+  p.kp = static_cast<uint16_t*>(kp);
+  float* scratch = nullptr;
+  if (!vmax) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                                    static_cast<size_t>(d->batch) * d->heads_kv * 4, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+  }
+  p.vmax = vmax ? vmax : scratch;
+  p.S2 = d->seq_kv;
+  p.D = d->head_dim;
+  p.diag = __half2float(dg);
+  p.off = __half2float(of);
+  p.lscale = lscale;
+  cudaError_t e = cudaMemsetAsync(p.vmax, 0, static_cast<size_t>(d->batch) * d->heads_kv * 4, st);
+  if (e == cudaSuccess) e = launch_kprep(p, d->batch, d->heads_kv, st);
+  if (scratch) cudaFreeAsync(scratch, st);
+  if (e != cudaSuccess) return cuda_fail(e, "pasa_kprep launch");
+  return PASA_B200_OK;
+}
+
+int pasa_b200_attention_fwd(const pasa_b200_desc* d, const void* q, const void* k, const void* v,
+                            void* o, void* workspace, size_t workspace_bytes,
+                            pasa_b200_diag* diag, void* stream) {
+  g_last_error.clear();
+  int rc = check_desc(d);
+  if (rc) return rc;
+  if (!q || !k || !v || !o || !workspace)
+    return fail(PASA_B200_EINVAL, "attention_fwd: NULL tensor or workspace");
+  if (workspace_bytes < pasa_b200_workspace_size(d))
+    return fail(PASA_B200_EINVAL, "attention_fwd: workspace too small");
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) |
+       reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(o) |
+       reinterpret_cast<uintptr_t>(workspace)) & 15)
+    return fail(PASA_B200_EINVAL, "attention_fwd: tensors must be 16-byte aligned");
+  (void)diag;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  void* kp = ws;
+  float* vmax = reinterpret_cast<float*>(ws + align_up(kp_bytes(d), 256));
+  rc = pasa_b200_preprocess_keys(d, k, v, kp, vmax, static_cast<float>(kLog2e), stream);
+  if (rc) return rc;
+
+  CUtensorMap tq, tk, tv;
+  if ((rc = make_tmap(&tq, q, d->head_dim, d->seq_q, d->batch * d->heads_q))) return rc;
+  if ((rc = make_tmap(&tk, kp, d->head_dim, d->seq_kv, d->batch * d->heads_kv))) return rc;
+  if ((rc = make_tmap(&tv, v, d->head_dim, d->seq_kv, d->batch * d->heads_kv))) return rc;
+  FwdParams p{};
+  p.B = d->batch;
+  p.Hq = d->heads_q;
+  p.Hkv = d->heads_kv;
+  p.S1 = d->seq_q;
+  p.S2 = d->seq_kv;
+  p.nq = d->seq_q / kTile;
+  p.nkv = d->seq_kv / kTile;
+  p.group = d->heads_q / d->heads_kv;
+  p.tiles_per_kv = p.group * p.nq;
+  p.inva = static_cast<float>(d->beta / (1.0 - d->beta));  // pasa.cpp:85
+  p.vmax = vmax;
+  p.out = static_cast<uint16_t*>(o);
+  cudaError_t e = launch_fwd(d->head_dim, d->causal != 0, tq, tk, tv, p, st);
+  if (e != cudaSuccess) return cuda_fail(e, "pasa_fwd launch");
+  return PASA_B200_OK;
+}
+
+int pasa_b200_attention_host(const pasa_b200_desc* d, const uint16_t* q, const uint16_t* k,
+                             const uint16_t* v, uint16_t* o) {
+  g_last_error.clear();
+  int rc = check_desc(d);
+  if (rc) return rc;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(PASA_B200_ENODEV, "no CUDA device");
+  const size_t nq = static_cast<size_t>(d->batch) * d->heads_q * d->seq_q * d->head_dim * 2;
+  const size_t nk = kp_bytes(d);
+  const size_t ws = pasa_b200_workspace_size(d);
+  uint8_t* buf = nullptr;
+  const size_t total = 2 * align_up(nq, 256) + 2 * align_up(nk, 256) + ws;
+  cudaError_t e = cudaMalloc(&buf, total);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  uint8_t* dq = buf;
+  uint8_t* dk = dq + align_up(nq, 256);
+  uint8_t* dv = dk + align_up(nk, 256);
+  uint8_t* dout = dv + align_up(nk, 256);
+  uint8_t* dws = dout + align_up(nq, 256);
+  e = cudaMemcpy(dq, q, nq, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dk, k, nk, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dv, v, nk, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(buf);
+    return cuda_fail(e, "H2D copy");
+  }
+  rc = pasa_b200_attention_fwd(d, dq, dk, dv, dout, dws, ws, nullptr, nullptr);
+  if (rc == PASA_B200_OK) {
+    e = cudaMemcpy(o, dout, nq, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = cuda_fail(e, "D2H copy / kernel");
+  }
+  cudaFree(buf);
+  return rc;
+}
+
+}  // extern "C"

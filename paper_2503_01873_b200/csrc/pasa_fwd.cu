@@ -1,0 +1,366 @@
+// pasa_fwd.cu -- the fused PASA forward kernel for sm_100a.
+//
+// One CTA owns NT = 2 query tiles of 128 rows that share one KV head (GQA
+// groups and neighbouring query tiles are paired), so every K'/V tile staged
+// in shared memory feeds two tensor-core tiles.  Warp roles:
+//
+//   warp 0      TMA producer: Q tiles once, then a K'/V ring (2 stages each)
+//   warp 1      MMA issuer (one elected lane) + TMEM owner (512 columns)
+//   warps 2-3   idle (warpgroup 0 gives its registers away via setmaxnreg)
+//   warps 4-7   softmax/correction warpgroup for tile 0 (thread = row)
+//   warps 8-11  softmax/correction warpgroup for tile 1
+//
+// Per KV block j and tile t (reference pasa.cpp:256-278, Algorithm 1):
+//   S'_t  = Q_t K'_j^T      tcgen05.mma kind::f16, SS, F16 accumulator in TMEM
+//   softmax WG: tcgen05.ld S' (packed half2), row max / FP32 row mean,
+//   pseudo-average recursion, corrected max, P = 2^(S' - c_j) (f16x2 MUFU),
+//   tcgen05.st P back over the S' columns (packed 2 x f16 per column)
+//   T_t   = P V_j           tcgen05.mma kind::f16, TS (P from TMEM), F16 acc
+//   softmax WG: O <- e_prev * O + T in half2 registers (HFMA2)
+// Epilogue ("global recovering"): O / l, fp16 store.
+//
+// Numerics are documented in DESIGN.md section 4 and restated on the CPU in
+// oracle/pasa_oracle.c:orc_model_pasa (the tight oracle for this kernel).
+#include <cuda.h>
+#include <cuda_fp16.h>
+
+#include "pasa_kernels.cuh"
+#include "sm100.cuh"
+
+namespace pasa_b200 {
+using namespace sm100;
+
+template <int D>
+struct FwdCfg {
+  static constexpr int NT = 2;
+  static constexpr int KS = 2;
+  static constexpr int VS = 2;
+  static constexpr int NBOX = D / 64;                     // 128-byte swizzle boxes per row
+  static constexpr int BOX_BYTES = kTile * 128;           // 128 rows x 64 halves
+  static constexpr int TILE_BYTES = NBOX * BOX_BYTES;     // one 128 x D fp16 tile
+  static constexpr int SMEM_Q = 0;
+  static constexpr int SMEM_K = SMEM_Q + NT * TILE_BYTES;
+  static constexpr int SMEM_V = SMEM_K + KS * TILE_BYTES;
+  static constexpr int SMEM_BAR = SMEM_V + VS * TILE_BYTES;
+  static constexpr int NUM_BARS = NT + 2 * KS + 2 * VS + 4 * NT;
+  static constexpr int SMEM_BYTES = SMEM_BAR + NUM_BARS * 8 + 16 + 1024;
+  static constexpr int THREADS = 128 + NT * 128;  // WG0: TMA, MMA, 2 idle; WG1..NT: softmax
+  static constexpr uint32_t TMEM_COLS = 512;
+  static constexpr uint32_t TMEM_TILE = 256;               // S/P at +0, T at +128
+};
+
+namespace {
+
+__device__ __forceinline__ float lo_f(uint32_t u) { return __low2float(u32_as_h2(u)); }
+__device__ __forceinline__ float hi_f(uint32_t u) { return __high2float(u32_as_h2(u)); }
+
+struct TileInfo {
+  int valid, i, hq, nblk;
+};
+
+__device__ __forceinline__ TileInfo tile_info(const FwdParams& p, int hkv, int idx, bool causal) {
+  TileInfo ti;
+  ti.valid = idx < p.tiles_per_kv;
+  ti.i = p.nq - 1 - idx / p.group;  // longest (causal) tiles first
+  ti.hq = hkv * p.group + idx % p.group;
+  ti.nblk = ti.valid ? (causal ? min(ti.i + 1, p.nkv) : p.nkv) : 0;
+  return ti;
+}
+
+}  // namespace
+
+template <int D, bool CAUSAL>
+__global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
+    pasa_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
+                    const __grid_constant__ CUtensorMap tm_kp,
+                    const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
+  using Cfg = FwdCfg<D>;
+  constexpr int NT = Cfg::NT, KS = Cfg::KS, VS = Cfg::VS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::SMEM_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = q_full + NT;
+  uint64_t* k_empty = k_full + KS;
+  uint64_t* v_full = k_empty + KS;
+  uint64_t* v_empty = v_full + VS;
+  uint64_t* s_full = v_empty + VS;
+  uint64_t* p_full = s_full + NT;
+  uint64_t* t_full = p_full + NT;
+  uint64_t* t_empty = t_full + NT;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
+
+  const int warp = static_cast<int>(warp_id());
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x / p.Hkv;
+  const int hkv = blockIdx.x % p.Hkv;
+  TileInfo tl[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) tl[t] = tile_info(p, hkv, blockIdx.y * NT + t, CAUSAL);
+  int nmax = 0;
+#pragma unroll
+  for (int t = 0; t < NT; ++t) nmax = max(nmax, tl[t].nblk);
+
+  if (threadIdx.x == 0) {
+    for (int t = 0; t < NT; ++t) {
+      mbar_init(&q_full[t], 1);
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 4);
+      mbar_init(&t_full[t], 1);
+      mbar_init(&t_empty[t], 4);
+    }
+    for (int s = 0; s < KS; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < VS; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp < 4) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      tma_prefetch(&tm_q);
+      tma_prefetch(&tm_kp);
+      tma_prefetch(&tm_v);
+      for (int t = 0; t < NT; ++t) {
+        if (!tl[t].valid) continue;
+        mbar_expect_tx(&q_full[t], Cfg::TILE_BYTES);
+        for (int bx = 0; bx < Cfg::NBOX; ++bx)
+          tma_load_3d(smem + Cfg::SMEM_Q + t * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_q,
+                      &q_full[t], bx * 64, tl[t].i * kTile, b * p.Hq + tl[t].hq);
+      }
+      for (int j = 0; j < nmax; ++j) {
+        const int ks = j % KS, vs = j % VS;
+        mbar_wait(&k_empty[ks], ((j / KS) & 1) ^ 1);
+        mbar_expect_tx(&k_full[ks], Cfg::TILE_BYTES);
+        for (int bx = 0; bx < Cfg::NBOX; ++bx)
+          tma_load_3d(smem + Cfg::SMEM_K + ks * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_kp,
+                      &k_full[ks], bx * 64, j * kTile, b * p.Hkv + hkv);
+        mbar_wait(&v_empty[vs], ((j / VS) & 1) ^ 1);
+        mbar_expect_tx(&v_full[vs], Cfg::TILE_BYTES);
+        for (int bx = 0; bx < Cfg::NBOX; ++bx)
+          tma_load_3d(smem + Cfg::SMEM_V + vs * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_v,
+                      &v_full[vs], bx * 64, j * kTile, b * p.Hkv + hkv);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t kIdS = idesc_f16(128, 128, 0, 0, 0);  // F16 acc, K-major A/B
+      constexpr uint32_t kIdPV = idesc_f16(128, D, 0, 0, 1);   // F16 acc, V MN-major
+      auto issue_s = [&](int t, int ks) {
+        const uint32_t d_tmem = tmem_base + t * Cfg::TMEM_TILE;
+        const uint32_t qa = smem_u32(smem + Cfg::SMEM_Q + t * Cfg::TILE_BYTES);
+        const uint32_t ka = smem_u32(smem + Cfg::SMEM_K + ks * Cfg::TILE_BYTES);
+#pragma unroll
+        for (int s = 0; s < D / 16; ++s) {
+          const uint32_t off = (s / 4) * Cfg::BOX_BYTES + (s % 4) * 32;
+          umma_ss(d_tmem, smem_desc_sw128(qa + off, 16, 1024), smem_desc_sw128(ka + off, 16, 1024),
+                  kIdS, s > 0);
+        }
+      };
+      auto issue_pv = [&](int t, int vs) {
+        const uint32_t d_tmem = tmem_base + t * Cfg::TMEM_TILE + 128;
+        const uint32_t a_tmem = tmem_base + t * Cfg::TMEM_TILE;
+        const uint32_t va = smem_u32(smem + Cfg::SMEM_V + vs * Cfg::TILE_BYTES);
+#pragma unroll
+        for (int s = 0; s < kTile / 16; ++s)
+          umma_ts(d_tmem, a_tmem + s * 8, smem_desc_sw128(va + s * 2048, Cfg::BOX_BYTES, 1024),
+                  kIdPV, s > 0);
+      };
+      for (int t = 0; t < NT; ++t)
+        if (tl[t].valid) mbar_wait(&q_full[t], 0);
+      if (nmax > 0) {
+        mbar_wait(&k_full[0], 0);
+        tc_fence_after();
+        for (int t = 0; t < NT; ++t) {
+          if (tl[t].nblk == 0) continue;
+          issue_s(t, 0);
+          tc_commit(&s_full[t]);
+        }
+        tc_commit(&k_empty[0]);
+      }
+      for (int j = 0; j < nmax; ++j) {
+        const int vs = j % VS;
+        mbar_wait(&v_full[vs], (j / VS) & 1);
+        bool k_next = false;
+        for (int t = 0; t < NT; ++t) {
+          if (j >= tl[t].nblk) continue;
+          mbar_wait(&p_full[t], j & 1);
+          mbar_wait(&t_empty[t], (j & 1) ^ 1);
+          tc_fence_after();
+          issue_pv(t, vs);
+          tc_commit(&t_full[t]);
+          if (j + 1 < tl[t].nblk) {
+            const int ks = (j + 1) % KS;
+            if (!k_next) {
+              mbar_wait(&k_full[ks], ((j + 1) / KS) & 1);
+              tc_fence_after();
+              k_next = true;
+            }
+            issue_s(t, ks);
+            tc_commit(&s_full[t]);
+          }
+        }
+        tc_commit(&v_empty[vs]);
+        if (k_next) tc_commit(&k_empty[(j + 1) % KS]);
+      }
+    }
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
+    // ------------------------------------------------------------ softmax WGs
+    const int t = (warp - 4) / 4;
+    const int quad = warp % 4;  // TMEM lane quadrant this warp may access
+    const int row = quad * 32 + lane;
+    const TileInfo ti = tile_info(p, hkv, blockIdx.y * NT + t, CAUSAL);
+    const uint32_t t_s = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + t * Cfg::TMEM_TILE;
+    const uint32_t t_t = t_s + 128;
+    if (ti.nblk > 0) {
+      // Inflation c0 (log2 units) keeping l * max|V| below 2^14.
+      const float vm = p.vmax[b * p.Hkv + hkv];
+      const float need = __fmul_rn(__fmul_rn(static_cast<float>(p.S2), vm), 1.0f / 16384.0f);
+      float c0 = 0.f;
+      if (need > 1.0f) {
+        const int e = ilogbf(need);
+        c0 = static_cast<float>(ldexpf(1.0f, e) == need ? e : e + 1);
+      }
+      uint32_t o[D / 2];
+      uint32_t s[64];
+      float m_run = 0.f, l_run = 0.f, fbar = 0.f;
+      for (int j = 0; j < ti.nblk; ++j) {
+        mbar_wait(&s_full[t], j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld_32cols_pack16(t_s + c * 32, s + c * 16);
+        tmem_wait_ld();
+        const bool diag = CAUSAL && (j == ti.nblk - 1);
+        // pass 1: local max over unmasked columns, FP32 sum over all columns
+        uint32_t mx = 0xFC00FC00u;  // (-inf, -inf)
+        float se = 0.f, so = 0.f;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          uint32_t v = s[i];
+          se = add_lo_f16(se, v);
+          so = add_hi_f16(so, v);
+          if (diag) {
+            const uint32_t keep = (2 * i + 1 <= row) ? 0xFFFFFFFFu : (2 * i <= row ? 0x0000FFFFu : 0u);
+            v = (v & keep) | (0xFC00FC00u & ~keep);
+          }
+          mx = h2_as_u32(__hmax2(u32_as_h2(mx), u32_as_h2(v)));
+        }
+        const float mloc = fmaxf(lo_f(mx), hi_f(mx));
+        const float sbar = __fmul_rn(__fadd_rn(se, so), 1.0f / 128.0f);
+        const int jc = j + 1;
+        const float fnew =
+            (jc == 1) ? sbar : __fadd_rn(fbar, __fdiv_rn(__fsub_rn(sbar, fbar), static_cast<float>(jc)));
+        const float dmc = __fmul_rn(p.inva, __fsub_rn(sbar, fnew));
+        const float dmp = (jc == 1) ? 0.f : __fmul_rn(p.inva, __fsub_rn(fbar, fnew));
+        const float cand = __fadd_rn(mloc, dmc);
+        const float mprev = __fadd_rn(m_run, dmp);
+        const float mnew = (jc == 1) ? cand : fmaxf(mprev, cand);
+        const __half cj = __float2half_rn(__fadd_rn(__fsub_rn(mnew, dmc), c0));
+        const float ep = (jc == 1) ? 0.f : __half2float(__float2half_rn(ex2_f32(__fsub_rn(mprev, mnew))));
+        // pass 2: P = 2^(S' - c_j) in f16x2, masked entries -> 0, FP32 row sum
+        const uint32_t cj2 = h2_as_u32(__half2half2(cj));
+        float le = 0.f, lo = 0.f;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          uint32_t pv = ex2_f16x2(h2_as_u32(__hsub2(u32_as_h2(s[i]), u32_as_h2(cj2))));
+          if (diag) {
+            const uint32_t keep = (2 * i + 1 <= row) ? 0xFFFFFFFFu : (2 * i <= row ? 0x0000FFFFu : 0u);
+            pv &= keep;
+          }
+          le = add_lo_f16(le, pv);
+          lo = add_hi_f16(lo, pv);
+          s[i] = pv;
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_st_16cols_b32(t_s + c * 16, s + c * 16);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
+        const float lsum = __fadd_rn(le, lo);
+        l_run = (jc == 1) ? lsum : __fadd_rn(__fmul_rn(ep, l_run), lsum);
+        m_run = mnew;
+        fbar = fnew;
+        // T = P V_j -> O
+        mbar_wait(&t_full[t], j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) tmem_ld_32cols_pack16(t_t + c * 32, s + c * 16);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&t_empty[t]);
+        if (jc == 1) {
+#pragma unroll
+          for (int i = 0; i < D / 2; ++i) o[i] = s[i];
+        } else {
+          const __half2 ep2 = __float2half2_rn(ep);
+#pragma unroll
+          for (int i = 0; i < D / 2; ++i)
+            o[i] = h2_as_u32(__hfma2(ep2, u32_as_h2(o[i]), u32_as_h2(s[i])));
+        }
+      }
+      // Epilogue: global recovering O / l (pasa.cpp:184-194), fp16 store.
+      const float inv_l = __frcp_rn(l_run);
+      uint16_t* dst = p.out + ((static_cast<size_t>(b) * p.Hq + ti.hq) * p.S1 +
+                               static_cast<size_t>(ti.i) * kTile + row) * D;
+#pragma unroll
+      for (int i = 0; i < D / 2; i += 4) {
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const __half a = __float2half_rn(__fmul_rn(lo_f(o[i + k]), inv_l));
+          const __half c = __float2half_rn(__fmul_rn(hi_f(o[i + k]), inv_l));
+          w[k] = h2_as_u32(__halves2half2(a, c));
+        }
+        *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+}
+
+// ---------------------------------------------------------------- launcher
+template <int D, bool CAUSAL>
+cudaError_t launch_fwd_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                         const FwdParams& p, cudaStream_t stream) {
+  using Cfg = FwdCfg<D>;
+  auto kern = pasa_fwd_kernel<D, CAUSAL>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       Cfg::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  const int units = (p.tiles_per_kv + Cfg::NT - 1) / Cfg::NT;
+  dim3 grid(p.B * p.Hkv, units);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(tq, tk, tv, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fwd(int D, bool causal, const CUtensorMap& tq, const CUtensorMap& tk,
+                       const CUtensorMap& tv, const FwdParams& p, cudaStream_t stream) {
+  if (D == 128) return causal ? launch_fwd_t<128, true>(tq, tk, tv, p, stream)
+                              : launch_fwd_t<128, false>(tq, tk, tv, p, stream);
+  if (D == 64) return causal ? launch_fwd_t<64, true>(tq, tk, tv, p, stream)
+                             : launch_fwd_t<64, false>(tq, tk, tv, p, stream);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace pasa_b200

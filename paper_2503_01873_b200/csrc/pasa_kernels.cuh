@@ -1,0 +1,33 @@
+// pasa_kernels.cuh -- shared parameter blocks for the PASA B200 kernels.
+#pragma once
+#include <cstdint>
+
+namespace pasa_b200 {
+
+constexpr int kTile = 128;  // query tile rows (s1 on the device) and the KV block s2
+
+// Key pre-pass: K'_j = K_j^T * M (reference pasa.cpp:53-56) in the kernel's
+// K-major layout kp[(b, h, j*s2 + c), t] = K'_j[t][c], plus max|V| per (b, h).
+struct KprepParams {
+  const uint16_t* k;   // (B, Hkv, S2, D) fp16
+  const uint16_t* v;   // (B, Hkv, S2, D) fp16 (only read for vmax)
+  uint16_t* kp;        // (B, Hkv, S2, D) fp16
+  float* vmax;         // (B * Hkv) max |V|, zeroed by the launcher
+  int S2;
+  int D;
+  float diag;          // fl16((1 - beta/s2)/alpha)     (pasa.cpp:26)
+  float off;           // fl16(-beta/(alpha*s2))        (pasa.cpp:27)
+  float lscale;        // 1 reproduces the reference; log2(e) for the fused kernel
+};
+
+// Fused PASA forward.  All scores live in the log2 domain (K' carries log2 e).
+struct FwdParams {
+  int B, Hq, Hkv, S1, S2;
+  int nq, nkv, group;     // S1/128, S2/128, Hq/Hkv
+  int tiles_per_kv;       // group * nq
+  float inva;             // beta / (1 - beta)       (pasa.cpp:85)
+  const float* vmax;      // per (b, kv head), from the pre-pass
+  uint16_t* out;          // (B, Hq, S1, D) fp16
+};
+
+}  // namespace pasa_b200
