@@ -404,7 +404,7 @@ static void prepass_block(const double* kb, size_t s2, size_t d, double diag,
         else if (p_acc == P16) acc = fl16(acc + fl16(prod));
         else acc = acc + prod;
       }
-      if (lscale != 1.0) acc = fl32(acc * lscale);
+      if (lscale != 1.0) acc = fl32(acc * (double)(float)lscale); /* FP32 multiply */
       kp[c * d + t] = rnd(p_store, acc);
     }
   }
