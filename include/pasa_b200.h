@@ -103,9 +103,18 @@ PASA_B200_API int pasa_b200_attention_fwd(const pasa_b200_desc* desc, const void
                             const void* v, void* o, void* workspace, size_t workspace_bytes,
                             pasa_b200_diag* diag, void* stream);
 
-/* Same, from HOST buffers (binary16 bit patterns): copies in, runs, copies
- * O back and synchronizes.  The drop-in for a CPU caller of pasa_attention
- * (the reference's `sweep`, bench.cpp:224). */
+/* The fused forward on keys already pre-processed by pasa_b200_preprocess_keys
+ * with lscale = log2(e) (kp in the K-major layout above, vmax = max|V| per
+ * (b, kv head)).  Lets a caller keep K' resident and reuse it across calls. */
+PASA_B200_API int pasa_b200_attention_fwd_prepped(const pasa_b200_desc* desc, const void* q,
+                                                  const void* kp, const void* v, const float* vmax,
+                                                  void* o, void* stream);
+
+/* pasa_b200_attention_fwd from HOST buffers (binary16 bit patterns): copies
+ * Q, K, V in, runs, copies O back and synchronizes.  The drop-in for a CPU
+ * caller of pasa_attention (the reference's `sweep`, bench.cpp:224).  Device
+ * buffers are cached per thread and device; pinned host buffers copy at DMA
+ * speed, pageable ones through the driver's staging path. */
 PASA_B200_API int pasa_b200_attention_host(const pasa_b200_desc* desc, const uint16_t* q, const uint16_t* k,
                              const uint16_t* v, uint16_t* o);
 

@@ -186,28 +186,16 @@ int pasa_b200_preprocess_keys(const pasa_b200_desc* d, const void* k, const void
   return PASA_B200_OK;
 }
 
-int pasa_b200_attention_fwd(const pasa_b200_desc* d, const void* q, const void* k, const void* v,
-                            void* o, void* workspace, size_t workspace_bytes,
-                            pasa_b200_diag* diag, void* stream) {
+int pasa_b200_attention_fwd_prepped(const pasa_b200_desc* d, const void* q, const void* kp,
+                                    const void* v, const float* vmax, void* o, void* stream) {
   g_last_error.clear();
   int rc = check_desc(d);
   if (rc) return rc;
-  if (!q || !k || !v || !o || !workspace)
-    return fail(PASA_B200_EINVAL, "attention_fwd: NULL tensor or workspace");
-  if (workspace_bytes < pasa_b200_workspace_size(d))
-    return fail(PASA_B200_EINVAL, "attention_fwd: workspace too small");
-  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) |
-       reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(o) |
-       reinterpret_cast<uintptr_t>(workspace)) & 15)
+  if (!q || !kp || !v || !o || !vmax)
+    return fail(PASA_B200_EINVAL, "attention_fwd: NULL tensor");
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(kp) |
+       reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(o)) & 15)
     return fail(PASA_B200_EINVAL, "attention_fwd: tensors must be 16-byte aligned");
-  (void)diag;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  uint8_t* ws = static_cast<uint8_t*>(workspace);
-  void* kp = ws;
-  float* vmax = reinterpret_cast<float*>(ws + align_up(kp_bytes(d), 256));
-  rc = pasa_b200_preprocess_keys(d, k, v, kp, vmax, static_cast<float>(kLog2e), stream);
-  if (rc) return rc;
-
   CUtensorMap tq, tk, tv;
   if ((rc = make_tmap(&tq, q, d->head_dim, d->seq_q, d->batch * d->heads_q))) return rc;
   if ((rc = make_tmap(&tk, kp, d->head_dim, d->seq_kv, d->batch * d->heads_kv))) return rc;
@@ -225,9 +213,29 @@ int pasa_b200_attention_fwd(const pasa_b200_desc* d, const void* q, const void* 
   p.inva = static_cast<float>(d->beta / (1.0 - d->beta));  // pasa.cpp:85
   p.vmax = vmax;
   p.out = static_cast<uint16_t*>(o);
-  cudaError_t e = launch_fwd(d->head_dim, d->causal != 0, tq, tk, tv, p, st);
+  cudaError_t e = launch_fwd(d->head_dim, d->causal != 0, tq, tk, tv, p,
+                             static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "pasa_fwd launch");
   return PASA_B200_OK;
+}
+
+int pasa_b200_attention_fwd(const pasa_b200_desc* d, const void* q, const void* k, const void* v,
+                            void* o, void* workspace, size_t workspace_bytes,
+                            pasa_b200_diag* diag, void* stream) {
+  g_last_error.clear();
+  int rc = check_desc(d);
+  if (rc) return rc;
+  if (!q || !k || !v || !o || !workspace)
+    return fail(PASA_B200_EINVAL, "attention_fwd: NULL tensor or workspace");
+  if (workspace_bytes < pasa_b200_workspace_size(d))
+    return fail(PASA_B200_EINVAL, "attention_fwd: workspace too small");
+  (void)diag;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  void* kp = ws;
+  float* vmax = reinterpret_cast<float*>(ws + align_up(kp_bytes(d), 256));
+  rc = pasa_b200_preprocess_keys(d, k, v, kp, vmax, static_cast<float>(kLog2e), stream);
+  if (rc) return rc;
+  return pasa_b200_attention_fwd_prepped(d, q, kp, v, vmax, o, stream);
 }
 
 int pasa_b200_attention_host(const pasa_b200_desc* d, const uint16_t* q, const uint16_t* k,
@@ -235,35 +243,49 @@ int pasa_b200_attention_host(const pasa_b200_desc* d, const uint16_t* q, const u
   g_last_error.clear();
   int rc = check_desc(d);
   if (rc) return rc;
-  int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-    return fail(PASA_B200_ENODEV, "no CUDA device");
+  if (!q || !k || !v || !o) return fail(PASA_B200_EINVAL, "attention_host: NULL buffer");
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(PASA_B200_ENODEV, "no CUDA device");
+  // Per-thread, per-device cache of the device copies and a private stream.
+  struct Cache {
+    int dev = -1;
+    uint8_t* buf = nullptr;
+    size_t bytes = 0;
+    cudaStream_t stream = nullptr;
+  };
+  thread_local Cache cache;
   const size_t nq = static_cast<size_t>(d->batch) * d->heads_q * d->seq_q * d->head_dim * 2;
   const size_t nk = kp_bytes(d);
   const size_t ws = pasa_b200_workspace_size(d);
-  uint8_t* buf = nullptr;
   const size_t total = 2 * align_up(nq, 256) + 2 * align_up(nk, 256) + ws;
-  cudaError_t e = cudaMalloc(&buf, total);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-  uint8_t* dq = buf;
+  cudaError_t e = cudaSuccess;
+  if (cache.dev != dev || cache.bytes < total) {
+    if (cache.buf) cudaFree(cache.buf);
+    if (cache.stream && cache.dev != dev) cudaStreamDestroy(cache.stream), cache.stream = nullptr;
+    cache.buf = nullptr;
+    cache.bytes = 0;
+    if ((e = cudaMalloc(&cache.buf, total)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    cache.bytes = total;
+    cache.dev = dev;
+  }
+  if (!cache.stream && (e = cudaStreamCreateWithFlags(&cache.stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return cuda_fail(e, "cudaStreamCreate");
+  uint8_t* dq = cache.buf;
   uint8_t* dk = dq + align_up(nq, 256);
   uint8_t* dv = dk + align_up(nk, 256);
   uint8_t* dout = dv + align_up(nk, 256);
   uint8_t* dws = dout + align_up(nq, 256);
-  e = cudaMemcpy(dq, q, nq, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(dk, k, nk, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(dv, v, nk, cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) {
-    cudaFree(buf);
-    return cuda_fail(e, "H2D copy");
-  }
-  rc = pasa_b200_attention_fwd(d, dq, dk, dv, dout, dws, ws, nullptr, nullptr);
-  if (rc == PASA_B200_OK) {
-    e = cudaMemcpy(o, dout, nq, cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) rc = cuda_fail(e, "D2H copy / kernel");
-  }
-  cudaFree(buf);
-  return rc;
+  cudaStream_t st = cache.stream;
+  e = cudaMemcpyAsync(dq, q, nq, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dk, k, nk, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dv, v, nk, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+  rc = pasa_b200_attention_fwd(d, dq, dk, dv, dout, dws, ws, nullptr, st);
+  if (rc) return rc;
+  e = cudaMemcpyAsync(o, dout, nq, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H copy / kernel");
+  return PASA_B200_OK;
 }
 
 }  // extern "C"
