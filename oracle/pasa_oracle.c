@@ -530,7 +530,7 @@ ORC_API int orc_pasa_ref(const orc_shape* sh, const double* q, const double* k,
 /* exact in real arithmetic:                                                 */
 /*  - every score lives in the L domain (lscale = log2 e: 2^x replaces e^x), */
 /*  - row statistics (sum of S', mean, F, corrections, running max, l) are   */
-/*    FP32; the S' and P row sums run as two chains (even / odd columns),    */
+/*    FP32; the S' and P row sums run as eight chains (kernel order),        */
 /*  - F_j = F_{j-1} + (Sbar - F_{j-1}) / j (no (j-1)*F product),             */
 /*  - e_cur is folded into P: P = 2^(fl16(S' - c_j) ) with                   */
 /*    c_j = fl16(m_j - dm_cur + c0), c0 >= 0 a per-head inflation that      */
@@ -620,17 +620,21 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
         const double* qr = row_ptr(q, sh->Hq, sh->S1, d, b, h, i * s1 + r);
         const size_t pos = row0 + r;
         for (size_t c = 0; c < s2; ++c) S[c] = tc_dot(qr, 1, kpj + c * d, 1, d, mp->tc_mode);
-        float se = 0.f, so = 0.f;
+        /* eight FP32 chains: column c -> chain 2*((c/2)%4) + c%2 (the kernel's
+         * pair-register order), combined ((t0+t1)+(t2+t3)), t_r = a_2r + a_2r+1 */
+        float sacc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         double mloc = -INFINITY;
-        for (size_t c = 0; c < s2; c += 2) {
-          se = se + (float)S[c];
-          so = so + (float)S[c + 1];
+        for (size_t c = 0; c < s2; ++c) {
+          const int ch = 2 * (int)((c / 2) % 4) + (int)(c % 2);
+          sacc[ch] = sacc[ch] + (float)S[c];
         }
         for (size_t c = 0; c < s2; ++c) {
           const int masked = sh->causal && (j * s2 + c > pos);
           if (!masked && S[c] > mloc) mloc = S[c];
         }
-        const float sbar = (se + so) * (1.0f / (float)s2);
+        const float ssum = ((sacc[0] + sacc[1]) + (sacc[2] + sacc[3])) +
+                           ((sacc[4] + sacc[5]) + (sacc[6] + sacc[7]));
+        const float sbar = ssum * (1.0f / (float)s2);
         float fnew = (jc == 1) ? sbar : fbar[r] + (sbar - fbar[r]) / (float)jc;
         const float dmc = inva * (sbar - fnew);
         const float dmp = (jc == 1) ? 0.f : inva * (fbar[r] - fnew);
@@ -643,15 +647,16 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
           const float earg = (m[r] + dmp) - mnew;
           ep = fl16(log2dom ? exp2((double)earg) : exp((double)earg));
         }
-        float le = 0.f, lo = 0.f; /* two chains: even / odd columns */
+        float lacc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}; /* same chains */
         for (size_t c = 0; c < s2; ++c) {
           const int masked = sh->causal && (j * s2 + c > pos);
           const double a = fl16(S[c] - cj);
           S[c] = masked ? 0.0 : fl16(log2dom ? exp2(a) : exp(a));
-          if (c & 1) lo = lo + (float)S[c];
-          else le = le + (float)S[c];
+          const int ch = 2 * (int)((c / 2) % 4) + (int)(c % 2);
+          lacc[ch] = lacc[ch] + (float)S[c];
         }
-        const float lloc = le + lo;
+        const float lloc = ((lacc[0] + lacc[1]) + (lacc[2] + lacc[3])) +
+                           ((lacc[4] + lacc[5]) + (lacc[6] + lacc[7]));
         l[r] = (jc == 1) ? lloc : (float)ep * l[r] + lloc;
         double* orow = oacc + r * d;
         for (size_t n = 0; n < d; ++n) {

@@ -67,6 +67,62 @@ __device__ __forceinline__ TileInfo tile_info(const FwdParams& p, int hkv, int i
   return ti;
 }
 
+// Column mask of the diagonal block for this row: keep lo/hi of pair i?
+__device__ __forceinline__ uint32_t diag_keep(int i, int row) {
+  return (2 * i + 1 <= row) ? 0xFFFFFFFFu : (2 * i <= row ? 0x0000FFFFu : 0u);
+}
+
+// Pass 1 over one S' row (64 packed pairs): max over unmasked columns and the
+// FP32 sum over all s2 columns.  Eight sum chains (pair i -> chain i % 4,
+// lo/hi) and four max chains keep the dependency depth at 16; the reduction
+// order is restated in oracle/pasa_oracle.c (orc_model_pasa).
+template <bool DIAG>
+__device__ __forceinline__ void row_max_sum(const uint32_t* s, int row, float& mloc, float& ssum) {
+  float acc[8];
+  uint32_t mx[4];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) mx[k] = 0xFC00FC00u;  // (-inf, -inf)
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    const uint32_t v = s[i];
+    acc[2 * (i & 3)] = add_lo_f16(acc[2 * (i & 3)], v);
+    acc[2 * (i & 3) + 1] = add_hi_f16(acc[2 * (i & 3) + 1], v);
+    uint32_t vm = v;
+    if (DIAG) {
+      const uint32_t keep = diag_keep(i, row);
+      vm = (v & keep) | (0xFC00FC00u & ~keep);
+    }
+    mx[i & 3] = h2_as_u32(__hmax2(u32_as_h2(mx[i & 3]), u32_as_h2(vm)));
+  }
+  const uint32_t m01 = h2_as_u32(__hmax2(u32_as_h2(mx[0]), u32_as_h2(mx[1])));
+  const uint32_t m23 = h2_as_u32(__hmax2(u32_as_h2(mx[2]), u32_as_h2(mx[3])));
+  const uint32_t m = h2_as_u32(__hmax2(u32_as_h2(m01), u32_as_h2(m23)));
+  mloc = fmaxf(lo_f(m), hi_f(m));
+  ssum = __fadd_rn(__fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3])),
+                   __fadd_rn(__fadd_rn(acc[4], acc[5]), __fadd_rn(acc[6], acc[7])));
+}
+
+// Pass 2: P = 2^(S' - c_j) in place (masked -> 0) and its FP32 row sum,
+// same eight-chain order as pass 1.
+template <bool DIAG>
+__device__ __forceinline__ float row_exp_sum(uint32_t* s, int row, uint32_t cj2) {
+  float acc[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    uint32_t pv = ex2_f16x2(h2_as_u32(__hsub2(u32_as_h2(s[i]), u32_as_h2(cj2))));
+    if (DIAG) pv &= diag_keep(i, row);
+    acc[2 * (i & 3)] = add_lo_f16(acc[2 * (i & 3)], pv);
+    acc[2 * (i & 3) + 1] = add_hi_f16(acc[2 * (i & 3) + 1], pv);
+    s[i] = pv;
+  }
+  return __fadd_rn(__fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3])),
+                   __fadd_rn(__fadd_rn(acc[4], acc[5]), __fadd_rn(acc[6], acc[7])));
+}
+
 }  // namespace
 
 template <int D, bool CAUSAL>
@@ -247,22 +303,10 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         for (int c = 0; c < 4; ++c) tmem_ld_32cols_pack16(t_s + c * 32, s + c * 16);
         tmem_wait_ld();
         const bool diag = CAUSAL && (j == ti.nblk - 1);
-        // pass 1: local max over unmasked columns, FP32 sum over all columns
-        uint32_t mx = 0xFC00FC00u;  // (-inf, -inf)
-        float se = 0.f, so = 0.f;
-#pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          uint32_t v = s[i];
-          se = add_lo_f16(se, v);
-          so = add_hi_f16(so, v);
-          if (diag) {
-            const uint32_t keep = (2 * i + 1 <= row) ? 0xFFFFFFFFu : (2 * i <= row ? 0x0000FFFFu : 0u);
-            v = (v & keep) | (0xFC00FC00u & ~keep);
-          }
-          mx = h2_as_u32(__hmax2(u32_as_h2(mx), u32_as_h2(v)));
-        }
-        const float mloc = fmaxf(lo_f(mx), hi_f(mx));
-        const float sbar = __fmul_rn(__fadd_rn(se, so), 1.0f / 128.0f);
+        float mloc, ssum;
+        if (diag) row_max_sum<true>(s, row, mloc, ssum);
+        else row_max_sum<false>(s, row, mloc, ssum);
+        const float sbar = __fmul_rn(ssum, 1.0f / 128.0f);
         const int jc = j + 1;
         const float fnew =
             (jc == 1) ? sbar : __fadd_rn(fbar, __fdiv_rn(__fsub_rn(sbar, fbar), static_cast<float>(jc)));
@@ -275,25 +319,13 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         const float ep = (jc == 1) ? 0.f : __half2float(__float2half_rn(ex2_f32(__fsub_rn(mprev, mnew))));
         // pass 2: P = 2^(S' - c_j) in f16x2, masked entries -> 0, FP32 row sum
         const uint32_t cj2 = h2_as_u32(__half2half2(cj));
-        float le = 0.f, lo = 0.f;
-#pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          uint32_t pv = ex2_f16x2(h2_as_u32(__hsub2(u32_as_h2(s[i]), u32_as_h2(cj2))));
-          if (diag) {
-            const uint32_t keep = (2 * i + 1 <= row) ? 0xFFFFFFFFu : (2 * i <= row ? 0x0000FFFFu : 0u);
-            pv &= keep;
-          }
-          le = add_lo_f16(le, pv);
-          lo = add_hi_f16(lo, pv);
-          s[i] = pv;
-        }
+        const float lsum = diag ? row_exp_sum<true>(s, row, cj2) : row_exp_sum<false>(s, row, cj2);
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_st_16cols_b32(t_s + c * 16, s + c * 16);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[t]);
-        const float lsum = __fadd_rn(le, lo);
         l_run = (jc == 1) ? lsum : __fadd_rn(__fmul_rn(ep, l_run), lsum);
         m_run = mnew;
         fbar = fnew;

@@ -5,7 +5,6 @@
 #pragma once
 #include <cstdint>
 #include <cuda_fp16.h>
-#include <cstdio>
 
 namespace pasa_b200 {
 namespace sm100 {
@@ -57,19 +56,14 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 // Wait for the phase with the given parity.  A pipeline bug must not hang the
-// GPU: after ~2^34 cycles (several seconds) the CTA traps instead.
-__device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
+// GPU: after ~2^33 cycles (seconds) the CTA traps instead.  Kept inline and
+// call-free so waiting never forces the caller's live registers to spill.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
-    if (clock64() - t0 > (1ll << 34)) {
-      printf("pasa_b200: mbarrier wait timeout (block %d,%d thread %d, parity %u)\n", blockIdx.x,
-             blockIdx.y, threadIdx.x, parity);
-      __trap();
-    }
+    if (clock64() - t0 > (1ll << 33)) asm volatile("trap;");
   }
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  if (!mbar_try_wait(bar, parity)) mbar_wait_slow(bar, parity);
 }
 
 // ---------------------------------------------------------------- TMA
