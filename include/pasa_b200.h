@@ -95,6 +95,14 @@ PASA_B200_API size_t pasa_b200_workspace_size(const pasa_b200_desc* desc);
 PASA_B200_API int pasa_b200_preprocess_keys(const pasa_b200_desc* desc, const void* k, const void* v,
                               void* kp, float* vmax, float lscale, void* stream);
 
+/* The key pre-pass from HOST buffers with the shifting matrix given by its
+ * two entries (as PasaParams::m holds them; they must be FP16 values): the
+ * drop-in for preprocess_keys (pasa.hpp:34-36) called per block by a CPU
+ * caller (the reference's range_report, bench.cpp:136).  lscale = 1, so the
+ * result carries the reference's bits.  Synchronous. */
+PASA_B200_API int pasa_b200_preprocess_keys_host(const pasa_b200_desc* desc, const uint16_t* k,
+                                                 uint16_t* kp, double m_diag, double m_off);
+
 /* The PASA forward, device pointers, stream-ordered, asynchronous.
  * Replaces pasa::pasa_attention (pasa.hpp:95-99, pasa.cpp:196-293) for the
  * PASA_FP16 policy.  workspace must hold pasa_b200_workspace_size() bytes.

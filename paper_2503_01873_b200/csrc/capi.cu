@@ -150,19 +150,12 @@ size_t pasa_b200_workspace_size(const pasa_b200_desc* d) {
   return align_up(kp_bytes(d), 256) + align_up(static_cast<size_t>(d->batch) * d->heads_kv * 4, 256);
 }
 
-int pasa_b200_preprocess_keys(const pasa_b200_desc* d, const void* k, const void* v, void* kp,
-                              float* vmax, float lscale, void* stream) {
-  g_last_error.clear();
-  if (!d || !k || !kp) return fail(PASA_B200_EINVAL, "preprocess_keys: NULL argument");
+static int preprocess_impl(const pasa_b200_desc* d, const void* k, const void* v, void* kp, float* vmax,
+                    float lscale, __half dg, __half of, cudaStream_t st) {
   if (d->head_dim != 64 && d->head_dim != 128)
     return fail(PASA_B200_EUNSUPPORTED, "head_dim must be 64 or 128");
   if (d->s2 != kTile || d->seq_kv % kTile != 0)
     return fail(PASA_B200_EUNSUPPORTED, "s2 must be 128 and divide S2");
-  if (!(d->beta >= 0.0 && d->beta <= 1.0) || !(d->alpha > 0.0))
-    return fail(PASA_B200_EINVAL, "shifting matrix: invalid beta/alpha");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  __half dg, of;
-  shift_scalars(d->s2, d->beta, d->alpha, &dg, &of);
   KprepParams p{};
   p.k = static_cast<const uint16_t*>(k);
   p.v = static_cast<const uint16_t*>(v ? v : k);
@@ -184,6 +177,40 @@ int pasa_b200_preprocess_keys(const pasa_b200_desc* d, const void* k, const void
   if (scratch) cudaFreeAsync(scratch, st);
   if (e != cudaSuccess) return cuda_fail(e, "pasa_kprep launch");
   return PASA_B200_OK;
+}
+
+int pasa_b200_preprocess_keys(const pasa_b200_desc* d, const void* k, const void* v, void* kp,
+                              float* vmax, float lscale, void* stream) {
+  g_last_error.clear();
+  if (!d || !k || !kp) return fail(PASA_B200_EINVAL, "preprocess_keys: NULL argument");
+  if (!(d->beta >= 0.0 && d->beta <= 1.0) || !(d->alpha > 0.0))
+    return fail(PASA_B200_EINVAL, "shifting matrix: invalid beta/alpha");
+  __half dg, of;
+  shift_scalars(d->s2, d->beta, d->alpha, &dg, &of);
+  return preprocess_impl(d, k, v, kp, vmax, lscale, dg, of, static_cast<cudaStream_t>(stream));
+}
+
+int pasa_b200_preprocess_keys_host(const pasa_b200_desc* d, const uint16_t* k, uint16_t* kp,
+                                   double m_diag, double m_off) {
+  g_last_error.clear();
+  if (!d || !k || !kp) return fail(PASA_B200_EINVAL, "preprocess_keys: NULL argument");
+  const __half dg = __double2half(m_diag), of = __double2half(m_off);
+  if (static_cast<double>(__half2float(dg)) != m_diag || static_cast<double>(__half2float(of)) != m_off)
+    return fail(PASA_B200_EINVAL, "preprocess_keys: shifting-matrix entries must be FP16 values");
+  const size_t nk = kp_bytes(d);
+  uint8_t* buf = nullptr;
+  cudaError_t e = cudaMalloc(&buf, 2 * align_up(nk, 256));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  uint8_t* dk = buf;
+  uint8_t* dkp = buf + align_up(nk, 256);
+  e = cudaMemcpy(dk, k, nk, cudaMemcpyHostToDevice);
+  int rc = PASA_B200_OK;
+  if (e != cudaSuccess) rc = cuda_fail(e, "H2D copy");
+  if (rc == PASA_B200_OK) rc = preprocess_impl(d, dk, nullptr, dkp, nullptr, 1.0f, dg, of, nullptr);
+  if (rc == PASA_B200_OK && (e = cudaMemcpy(kp, dkp, nk, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    rc = cuda_fail(e, "D2H copy / kernel");
+  cudaFree(buf);
+  return rc;
 }
 
 int pasa_b200_attention_fwd_prepped(const pasa_b200_desc* d, const void* q, const void* kp,

@@ -231,3 +231,27 @@ def test_host_entry_point_matches_device(dev, orc):
     assert o_host.device.type == "cpu"
     assert torch.equal(o_host, o_dev.cpu())
     assert diag.out_total == o_host.numel() and diag.out_nonfinite == 0
+
+
+def test_reference_harness_on_b200(dev):
+    """The reference's own sweep (bench.cpp:170-247) linked against the B200
+    drop-in (integration/pasa_shim.cpp instead of pasa.o): PASA_FP16 cells run
+    on the GPU, FA_PARTIAL_FP16 on the reference CPU path, same CSV schema."""
+    import csv
+    import io
+    import subprocess
+    exe = os.path.join(os.path.dirname(HERE), "integration", "_build", "ref_sweep_b200")
+    if not os.path.exists(exe):
+        pytest.skip("integration binary not built")
+    r = subprocess.run([exe, "2", "1280"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    rows = list(csv.DictReader(io.StringIO(r.stdout)))
+    pasa_rows = [x for x in rows if x["policy"] == "PASA_FP16"]
+    fa_rows = [x for x in rows if x["policy"] == "FA_PARTIAL_FP16"]
+    assert len(pasa_rows) == 6 and len(fa_rows) == 6
+    # reference PASA_FP16 RMSE on these cells (SURVEY.md 6B, 16 heads); Tier 1 bound
+    ref_rmse = [9.10e-3, 1.05e-1, 1.15e-1, 2.77e-2, 2.21e-2, 2.08e-2]
+    for row, rr in zip(pasa_rows, ref_rmse):
+        assert float(row["nan_pct"]) == 0.0
+        assert float(row["rmse"]) <= 1.25 * rr + 1e-3, (row, rr)
+    assert float(fa_rows[0]["nan_pct"]) == 100.0 and float(fa_rows[3]["nan_pct"]) == 100.0
