@@ -255,3 +255,21 @@ def test_reference_harness_on_b200(dev):
         assert float(row["nan_pct"]) == 0.0
         assert float(row["rmse"]) <= 1.25 * rr + 1e-3, (row, rr)
     assert float(fa_rows[0]["nan_pct"]) == 100.0 and float(fa_rows[3]["nan_pct"]) == 100.0
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_bit_identical(dev, orc, world):
+    """O must be bit-identical at 1/2/4/8 GPUs.  The shards of a
+    G-GPU run are computed one after another on this GPU and reassembled."""
+    from paper_2503_01873_b200 import pasa_attention_fwd
+    from paper_2503_01873_b200.multi import partition, shard_forward
+    q, k, v = orc.generate("hybrid", 0.0, 10.0, 21, 2, 8, 1024, 128, Hkv=4)
+    qt, kt, vt = (torch.from_numpy(x).half().to(dev) for x in (q, k, v))
+    full = pasa_attention_fwd(qt, kt, vt, causal=True)
+    out = torch.empty_like(full)
+    for sh in partition(2, 4, world):
+        for u, o in shard_forward(qt, kt, vt, sh, causal=True):
+            b, h = divmod(u, 4)
+            out[b:b + 1, 2 * h:2 * h + 2] = o
+    torch.cuda.synchronize()
+    assert torch.equal(out, full)
