@@ -351,7 +351,7 @@ def run_b200(args):
         from oracle.oracle import ref_available, RefLib
         if ref_available():
             cores = cpu_cores()
-            qs, ks, vs, nb = reference_sample(cores, SEQ)
+            qs, ks, vs, nb = reference_sample(8 * cores, SEQ)  # ~10 s of reference work
             dt, _ = time_reference_step(RefLib(), qs, ks, vs)
             cpu_base = {"value": 4.0 * nb * 128 * SEQ * D / dt / 1e12, "unit": UNIT,
                         "cores": cores, "kind": "reference",
