@@ -32,28 +32,33 @@ def _stale(obj: str, src: str) -> bool:
     return any(os.path.getmtime(d) > os.path.getmtime(obj) for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(OUT, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, trace: bool = False) -> str:
+    """Build libpasa_b200.so (or, with trace=True, the clock64-timeline profiling
+    variant libpasa_b200_trace.so used by tools/trace_fwd.py)."""
+    out_dir = os.path.join(OUT, "trace") if trace else OUT
+    so = os.path.join(OUT, "libpasa_b200_trace.so") if trace else SO
+    extra = ["-DPASA_TRACE"] if trace else []
+    os.makedirs(out_dir, exist_ok=True)
     objs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OUT, src.replace(".cu", ".o"))
+        o = os.path.join(out_dir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, s):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
+            cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", s, "-o", o]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if verbose or r.returncode:
                 sys.stderr.write(r.stdout + r.stderr)
             if r.returncode:
                 raise RuntimeError(f"nvcc failed on {src}")
-    if force or not os.path.exists(SO) or any(os.path.getmtime(o) > os.path.getmtime(SO) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", SO, *objs]
+    if force or not os.path.exists(so) or any(os.path.getmtime(o) > os.path.getmtime(so) for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", so, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link failed")
-    return SO
+    return so
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, trace="--trace" in sys.argv))

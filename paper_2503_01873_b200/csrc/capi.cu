@@ -28,6 +28,7 @@ using namespace pasa_b200;
 namespace {
 
 thread_local std::string g_last_error;
+long long* g_trace = nullptr;  // PASA_TRACE builds: clock64 timeline buffer
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -240,6 +241,7 @@ int pasa_b200_attention_fwd_prepped(const pasa_b200_desc* d, const void* q, cons
   p.inva = static_cast<float>(d->beta / (1.0 - d->beta));  // pasa.cpp:85
   p.vmax = vmax;
   p.out = static_cast<uint16_t*>(o);
+  p.trace = g_trace;
   cudaError_t e = launch_fwd(d->head_dim, d->causal != 0, tq, tk, tv, p,
                              static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "pasa_fwd launch");
@@ -314,5 +316,14 @@ int pasa_b200_attention_host(const pasa_b200_desc* d, const uint16_t* q, const u
   if (e != cudaSuccess) return cuda_fail(e, "D2H copy / kernel");
   return PASA_B200_OK;
 }
+
+#ifdef PASA_TRACE
+// Profiling builds only (libpasa_b200_trace.so): device buffer of
+// kTraceCtas * 3 * 32 * 8 int64 that the fused kernel fills with clock64().
+__attribute__((visibility("default"))) int pasa_b200_debug_set_trace(void* device_buf) {
+  g_trace = static_cast<long long*>(device_buf);
+  return PASA_B200_OK;
+}
+#endif
 
 }  // extern "C"

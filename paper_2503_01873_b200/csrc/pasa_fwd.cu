@@ -30,6 +30,24 @@
 namespace pasa_b200 {
 using namespace sm100;
 
+// PASA_TRACE (profiling builds only): CTAs whose blockIdx.x == 0 and blockIdx.y
+// < kTraceCtas record clock64() at fixed points of the first kTraceIters
+// blocks -- per softmax warpgroup (warp quadrant 0, lane 0) and for the MMA
+// issuer -- into p.trace[cta][role][iter][event].
+constexpr int kTraceCtas = 4, kTraceIters = 32, kTraceEvents = 8, kTraceRoles = 3;
+#ifdef PASA_TRACE
+#define PASA_TR(role, it, ev)                                                                  \
+  do {                                                                                        \
+    if (p.trace && blockIdx.x == 0 && blockIdx.y < kTraceCtas && (it) < kTraceIters)          \
+      p.trace[((blockIdx.y * kTraceRoles + (role)) * kTraceIters + (it)) * kTraceEvents + (ev)] = \
+          clock64();                                                                          \
+  } while (0)
+#else
+#define PASA_TR(role, it, ev) \
+  do {                        \
+  } while (0)
+#endif
+
 template <int D>
 struct FwdCfg {
   static constexpr int NT = 2;
@@ -254,10 +272,13 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         bool k_next = false;
         for (int t = 0; t < NT; ++t) {
           if (j >= tl[t].nblk) continue;
+          PASA_TR(2, j, 4 * t + 0);
           mbar_wait(&p_full[t], j & 1);
+          PASA_TR(2, j, 4 * t + 1);
           mbar_wait(&t_empty[t], (j & 1) ^ 1);
           tc_fence_after();
           issue_pv(t, vs);
+          PASA_TR(2, j, 4 * t + 2);
           tc_commit(&t_full[t]);
           if (j + 1 < tl[t].nblk) {
             const int ks = (j + 1) % KS;
@@ -268,6 +289,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
             }
             issue_s(t, ks);
             tc_commit(&s_full[t]);
+            PASA_TR(2, j, 4 * t + 3);
           }
         }
         tc_commit(&v_empty[vs]);
@@ -297,11 +319,15 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       uint32_t s[64];
       float m_run = 0.f, l_run = 0.f, fbar = 0.f;
       for (int j = 0; j < ti.nblk; ++j) {
+        const bool tr = quad == 0 && lane == 0;
+        if (tr) PASA_TR(t, j, 0);
         mbar_wait(&s_full[t], j & 1);
+        if (tr) PASA_TR(t, j, 1);
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld_32cols_pack16(t_s + c * 32, s + c * 16);
         tmem_wait_ld();
+        if (tr) PASA_TR(t, j, 2);
         const bool diag = CAUSAL && (j == ti.nblk - 1);
         float mloc, ssum;
         if (diag) row_max_sum<true>(s, row, mloc, ssum);
@@ -318,6 +344,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         const __half cj = __float2half_rn(__fadd_rn(__fsub_rn(mnew, dmc), c0));
         const float ep = (jc == 1) ? 0.f : __half2float(__float2half_rn(ex2_f32(__fsub_rn(mprev, mnew))));
         // pass 2: P = 2^(S' - c_j) in f16x2, masked entries -> 0, FP32 row sum
+        if (tr) PASA_TR(t, j, 3);
         const uint32_t cj2 = h2_as_u32(__half2half2(cj));
         const float lsum = diag ? row_exp_sum<true>(s, row, cj2) : row_exp_sum<false>(s, row, cj2);
 #pragma unroll
@@ -326,11 +353,13 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[t]);
+        if (tr) PASA_TR(t, j, 4);
         l_run = (jc == 1) ? lsum : __fadd_rn(__fmul_rn(ep, l_run), lsum);
         m_run = mnew;
         fbar = fnew;
         // T = P V_j -> O
         mbar_wait(&t_full[t], j & 1);
+        if (tr) PASA_TR(t, j, 5);
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) tmem_ld_32cols_pack16(t_t + c * 32, s + c * 16);
@@ -338,6 +367,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&t_empty[t]);
+        if (tr) PASA_TR(t, j, 6);
         if (jc == 1) {
 #pragma unroll
           for (int i = 0; i < D / 2; ++i) o[i] = s[i];

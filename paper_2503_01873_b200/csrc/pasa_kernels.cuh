@@ -28,6 +28,7 @@ struct FwdParams {
   float inva;             // beta / (1 - beta)       (pasa.cpp:85)
   const float* vmax;      // per (b, kv head), from the pre-pass
   uint16_t* out;          // (B, Hq, S1, D) fp16
+  long long* trace;       // PASA_TRACE builds only: clock64 timeline (see pasa_fwd.cu)
 };
 
 }  // namespace pasa_b200

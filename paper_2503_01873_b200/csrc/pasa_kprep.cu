@@ -6,9 +6,10 @@
 // M[p][c]) for p = 0..s2-1 and rounds once to FP16.  K and M are FP16 values,
 // so each product is exact in FP32 and one FFMA per step reproduces it.  M
 // has only two distinct entries, so the chains for all columns c share the
-// prefix p < c (all `off`); each thread owns one head-dim index t, walks c
-// upwards carrying the shared prefix, and finishes column c's chain from
-// there -- half the FMAs of the dense product, no selects, identical bits.
+// prefix p < c (all `off`); a thread owns one head-dim index t and four groups
+// of eight columns, carries the shared prefix upwards and runs each group's
+// eight chains in lock-step from there -- half the FMAs of the dense product,
+// eight-way ILP, identical bits.
 //
 // The K block is staged in shared memory transposed (t-major, p contiguous,
 // rows padded by 16 B) so a thread reads eight consecutive p with one
@@ -20,20 +21,22 @@
 namespace pasa_b200 {
 
 template <int D>
-__global__ void __launch_bounds__(D) pasa_kprep_kernel(const KprepParams p) {
+__global__ void __launch_bounds__(D * 4) pasa_kprep_kernel(const KprepParams p) {
   constexpr int S2 = kTile;
-  constexpr int ROW = S2 + 8;  // halves per transposed row (16 B pad)
+  constexpr int ROW = S2 + 8;  // halves per transposed row (16 B pad: conflict-free 16 B loads)
   __shared__ __align__(16) __half kt[D * ROW];
-  __shared__ float red[D / 32];
+  __shared__ float red[D * 4 / 32];
 
   const int j = blockIdx.x;    // KV block
   const int bh = blockIdx.y;   // b * Hkv + h
   const int t = threadIdx.x;   // head-dim index owned by this thread
+  const int y = threadIdx.y;   // column-group slot 0..3
+  const int tid = y * D + t;
   const size_t base = (static_cast<size_t>(bh) * p.S2 + static_cast<size_t>(j) * S2) * D;
   const __half* kg = reinterpret_cast<const __half*>(p.k) + base;
 
   // Stage K_j transposed: kt[t][p] = K[p][t].
-  for (int e = threadIdx.x * 8; e < S2 * D; e += D * 8) {
+  for (int e = tid * 8; e < S2 * D; e += D * 4 * 8) {
     const uint4 w = *reinterpret_cast<const uint4*>(kg + e);
     const __half* h = reinterpret_cast<const __half*>(&w);
     const int pr = e / D, tc = e % D;
@@ -44,7 +47,7 @@ __global__ void __launch_bounds__(D) pasa_kprep_kernel(const KprepParams p) {
   {
     const __half* vg = reinterpret_cast<const __half*>(p.v) + base;
     float vm = 0.f;
-    for (int e = threadIdx.x * 8; e < S2 * D; e += D * 8) {
+    for (int e = tid * 8; e < S2 * D; e += D * 4 * 8) {
       const uint4 w = *reinterpret_cast<const uint4*>(vg + e);
       const __half* h = reinterpret_cast<const __half*>(&w);
 #pragma unroll
@@ -52,47 +55,70 @@ __global__ void __launch_bounds__(D) pasa_kprep_kernel(const KprepParams p) {
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) vm = fmaxf(vm, __shfl_xor_sync(0xffffffffu, vm, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = vm;
+    if ((tid & 31) == 0) red[tid / 32] = vm;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     float vm = 0.f;
-    for (int w = 0; w < D / 32; ++w) vm = fmaxf(vm, red[w]);
+    for (int w = 0; w < D * 4 / 32; ++w) vm = fmaxf(vm, red[w]);
     atomicMax(reinterpret_cast<int*>(p.vmax) + bh, __float_as_int(vm));  // vm >= 0
   }
 
+  // Thread (t, y) owns the 8-column groups {y, 7-y, 8+y, 15-y} (equal work per
+  // slot, increasing order).  Column c's chain is prefix(c) (all `off`), then
+  // `diag` at p = c, then `off` to the end; the eight chains of a group walk the
+  // same p together, so one K value feeds eight independent FFMAs.
   const __half* col = kt + t * ROW;
   __half* out = reinterpret_cast<__half*>(p.kp) + base + t;
   const float diag = p.diag, off = p.off, L = p.lscale;
-  float prefix = 0.f;  // chain over p < c, every step with `off`
-  for (int c = 0; c < S2; ++c) {
-    const float kc = __half2float(col[c]);
-    float acc = __fmaf_rn(kc, diag, prefix);
-    int q = c + 1;
-    // walk to the next multiple of 8, then eight at a time
-    for (; q < S2 && (q & 7); ++q) acc = __fmaf_rn(__half2float(col[q]), off, acc);
-    for (; q < S2; q += 8) {
-      const uint4 w = *reinterpret_cast<const uint4*>(col + q);
-      const __half2* h = reinterpret_cast<const __half2*>(&w);
+  const int groups[4] = {y, 7 - y, 8 + y, 15 - y};
+  float prefix = 0.f;
+  int pdone = 0;
+#pragma unroll 1
+  for (int gi = 0; gi < 4; ++gi) {
+    const int c0 = 8 * groups[gi];
+    for (int q = pdone; q < c0; ++q) prefix = __fmaf_rn(__half2float(col[q]), off, prefix);
+    pdone = c0;
+    float acc[8];
+    {
+      // p = c0 .. c0+7: column c0+cc takes `diag` at p == c0+cc
+      const uint4 w = *reinterpret_cast<const uint4*>(col + c0);
+      const __half* h = reinterpret_cast<const __half*>(&w);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 f = __half22float2(h[k]);
-        acc = __fmaf_rn(f.x, off, acc);
-        acc = __fmaf_rn(f.y, off, acc);
+      for (int cc = 0; cc < 8; ++cc) acc[cc] = prefix;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float kv = __half2float(h[k]);
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) acc[cc] = __fmaf_rn(kv, k == cc ? diag : off, acc[cc]);
       }
     }
-    if (L != 1.0f) acc = __fmul_rn(acc, L);
-    out[static_cast<size_t>(c) * D] = __float2half_rn(acc);
-    prefix = __fmaf_rn(kc, off, prefix);
+#pragma unroll 2
+    for (int q = c0 + 8; q < S2; q += 8) {
+      const uint4 w = *reinterpret_cast<const uint4*>(col + q);
+      const __half* h = reinterpret_cast<const __half*>(&w);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float kv = __half2float(h[k]);
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) acc[cc] = __fmaf_rn(kv, off, acc[cc]);
+      }
+    }
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      float a = acc[cc];
+      if (L != 1.0f) a = __fmul_rn(a, L);
+      out[static_cast<size_t>(c0 + cc) * D] = __float2half_rn(a);
+    }
   }
 }
 
 cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stream) {
   dim3 grid(p.S2 / kTile, B * Hkv);
   if (p.D == 128) {
-    pasa_kprep_kernel<128><<<grid, 128, 0, stream>>>(p);
+    pasa_kprep_kernel<128><<<grid, dim3(128, 4), 0, stream>>>(p);
   } else if (p.D == 64) {
-    pasa_kprep_kernel<64><<<grid, 64, 0, stream>>>(p);
+    pasa_kprep_kernel<64><<<grid, dim3(64, 4), 0, stream>>>(p);
   } else {
     return cudaErrorInvalidValue;
   }
