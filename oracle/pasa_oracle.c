@@ -531,7 +531,7 @@ ORC_API int orc_pasa_ref(const orc_shape* sh, const double* q, const double* k,
 /*  - every score lives in the L domain (lscale = log2 e: 2^x replaces e^x), */
 /*  - row statistics (sum of S', mean, F, corrections, running max, l) are   */
 /*    FP32; the S' and P row sums run as eight chains (kernel order),        */
-/*  - F_j = F_{j-1} + (Sbar - F_{j-1}) / j (no (j-1)*F product),             */
+/*  - F_j = F_{j-1} + (Sbar - F_{j-1}) * fl32(1/j) (no (j-1)*F product),     */
 /*  - e_cur is folded into P: P = 2^(fl16(S' - c_j) ) with                   */
 /*    c_j = fl16(m_j - dm_cur + c0), c0 >= 0 a per-head inflation that      */
 /*    bounds O and l below 65504 (see kernel), so O <- fl16(e_p * O + T),    */
@@ -635,7 +635,8 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
         const float ssum = ((sacc[0] + sacc[1]) + (sacc[2] + sacc[3])) +
                            ((sacc[4] + sacc[5]) + (sacc[6] + sacc[7]));
         const float sbar = ssum * (1.0f / (float)s2);
-        float fnew = (jc == 1) ? sbar : fbar[r] + (sbar - fbar[r]) / (float)jc;
+        const float rcp = 1.0f / (float)jc; /* the kernel multiplies by 1/j */
+        float fnew = (jc == 1) ? sbar : fbar[r] + (sbar - fbar[r]) * rcp;
         const float dmc = inva * (sbar - fnew);
         const float dmp = (jc == 1) ? 0.f : inva * (fbar[r] - fnew);
         const float cand = (float)mloc + dmc;

@@ -123,7 +123,8 @@ __device__ __forceinline__ void row_max_sum(const uint32_t* s, int row, float& m
 }
 
 // Pass 2: P = 2^(S' - c_j) in place (masked -> 0) and its FP32 row sum,
-// same eight-chain order as pass 1.
+// same eight-chain order as pass 1.  Half the pairs use MUFU ex2.approx.f16x2,
+// half the FMA-pipe polynomial (sm100.cuh), both within 1 ulp of 2^x.
 template <bool DIAG>
 __device__ __forceinline__ float row_exp_sum(uint32_t* s, int row, uint32_t cj2) {
   float acc[8];
@@ -131,7 +132,9 @@ __device__ __forceinline__ float row_exp_sum(uint32_t* s, int row, uint32_t cj2)
   for (int k = 0; k < 8; ++k) acc[k] = 0.f;
 #pragma unroll
   for (int i = 0; i < 64; ++i) {
-    uint32_t pv = ex2_f16x2(h2_as_u32(__hsub2(u32_as_h2(s[i]), u32_as_h2(cj2))));
+    const uint32_t x = h2_as_u32(__hsub2(u32_as_h2(s[i]), u32_as_h2(cj2)));
+    // odd pairs on the FMA pipe, even pairs on MUFU: both pipes busy at once
+    uint32_t pv = (i & 1) ? ex2_poly_f16x2(x) : ex2_f16x2(x);
     if (DIAG) pv &= diag_keep(i, row);
     acc[2 * (i & 3)] = add_lo_f16(acc[2 * (i & 3)], pv);
     acc[2 * (i & 3) + 1] = add_hi_f16(acc[2 * (i & 3) + 1], pv);
@@ -318,6 +321,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       uint32_t o[D / 2];
       uint32_t s[64];
       float m_run = 0.f, l_run = 0.f, fbar = 0.f;
+      float rcp_j = 1.0f;  // 1/(j+1), computed off the critical path
       for (int j = 0; j < ti.nblk; ++j) {
         const bool tr = quad == 0 && lane == 0;
         if (tr) PASA_TR(t, j, 0);
@@ -335,7 +339,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         const float sbar = __fmul_rn(ssum, 1.0f / 128.0f);
         const int jc = j + 1;
         const float fnew =
-            (jc == 1) ? sbar : __fadd_rn(fbar, __fdiv_rn(__fsub_rn(sbar, fbar), static_cast<float>(jc)));
+            (jc == 1) ? sbar : __fadd_rn(fbar, __fmul_rn(__fsub_rn(sbar, fbar), rcp_j));
         const float dmc = __fmul_rn(p.inva, __fsub_rn(sbar, fnew));
         const float dmp = (jc == 1) ? 0.f : __fmul_rn(p.inva, __fsub_rn(fbar, fnew));
         const float cand = __fadd_rn(mloc, dmc);
@@ -357,6 +361,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         l_run = (jc == 1) ? lsum : __fadd_rn(__fmul_rn(ep, l_run), lsum);
         m_run = mnew;
         fbar = fnew;
+        rcp_j = __frcp_rn(static_cast<float>(jc + 1));
         // T = P V_j -> O
         mbar_wait(&t_full[t], j & 1);
         if (tr) PASA_TR(t, j, 5);

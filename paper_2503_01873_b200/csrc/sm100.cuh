@@ -208,6 +208,25 @@ __device__ __forceinline__ uint32_t ex2_f16x2(uint32_t x) {
   asm("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(x));
   return r;
 }
+// 2^x for x <= 0 on a half2, on the FMA/ALU pipes instead of MUFU (the two
+// run concurrently, so splitting a row between them doubles exp throughput).
+// x is clamped to [-25, 0]; n = round(x) comes from the 1049 = 1024 + 25 magic
+// add (t's low mantissa bits hold n + 25); f = x - n in [-0.5, 0.5]; 2^f is a
+// cubic in f16x2 (Chebyshev least squares, FP16 coefficients); 2^(n+10) is
+// built from t's bits and the final x 2^-10 rounds once into the subnormal
+// range, so the result is within 1 ulp of the correctly rounded FP16 2^x
+// (93 % exact; tools/mufu_probe.cu).
+__device__ __forceinline__ uint32_t ex2_poly_f16x2(uint32_t xr) {
+  const __half2 x = __hmax2(u32_as_h2(xr), u32_as_h2(0xCE40CE40u));  // -25
+  const __half2 magic = u32_as_h2(0x64196419u);                      // 1049
+  const __half2 t = __hadd2(x, magic);
+  const __half2 f = __hsub2(x, __hsub2(t, magic));
+  __half2 p = __hfma2(f, u32_as_h2(0x2B0D2B0Du), u32_as_h2(0x33C333C3u));  // 0.05508, 0.2426
+  p = __hfma2(p, f, u32_as_h2(0x398C398Cu));                              // 0.6934
+  p = __hfma2(p, f, u32_as_h2(0x3C003C00u));                              // 1.0
+  const uint32_t e = (h2_as_u32(t) & 0x001F001Fu) << 10;  // 2^(n+10), 0 for n = -25
+  return h2_as_u32(__hmul2(__hmul2(p, u32_as_h2(e)), u32_as_h2(0x14001400u)));  // x 2^-10
+}
 __device__ __forceinline__ float ex2_f32(float x) {
   float r;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
