@@ -605,7 +605,7 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
       c0 = orc_model_inflation(vmax, sh->S2, L);
     }
     float* m = calloc(s1, sizeof(float));
-    float* l = calloc(s1, sizeof(float));
+    float* l = calloc(2 * s1, sizeof(float)); /* per half-row partial l */
     float* fbar = calloc(s1, sizeof(float));
     double* oacc = calloc(s1 * d, sizeof(double));
     double* S = malloc(sizeof(double) * s2);
@@ -620,20 +620,25 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
         const double* qr = row_ptr(q, sh->Hq, sh->S1, d, b, h, i * s1 + r);
         const size_t pos = row0 + r;
         for (size_t c = 0; c < s2; ++c) S[c] = tc_dot(qr, 1, kpj + c * d, 1, d, mp->tc_mode);
-        /* eight FP32 chains: column c -> chain 2*((c/2)%4) + c%2 (the kernel's
-         * pair-register order), combined ((t0+t1)+(t2+t3)), t_r = a_2r + a_2r+1 */
-        float sacc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        /* Two threads per row (columns [0, s2/2) and [s2/2, s2)); in each half
+         * eight FP32 chains: column c -> chain 2*((c/2)%4) + c%2 (the kernel's
+         * pair-register order), combined ((t0+t1)+(t2+t3)), t_r = a_2r + a_2r+1;
+         * the row total is half0 + half1. */
+        float sacc[2][8] = {{0.f}};
         double mloc = -INFINITY;
         for (size_t c = 0; c < s2; ++c) {
           const int ch = 2 * (int)((c / 2) % 4) + (int)(c % 2);
-          sacc[ch] = sacc[ch] + (float)S[c];
+          sacc[c >= s2 / 2][ch] = sacc[c >= s2 / 2][ch] + (float)S[c];
         }
         for (size_t c = 0; c < s2; ++c) {
           const int masked = sh->causal && (j * s2 + c > pos);
           if (!masked && S[c] > mloc) mloc = S[c];
         }
-        const float ssum = ((sacc[0] + sacc[1]) + (sacc[2] + sacc[3])) +
-                           ((sacc[4] + sacc[5]) + (sacc[6] + sacc[7]));
+        float shalf[2];
+        for (int hh = 0; hh < 2; ++hh)
+          shalf[hh] = ((sacc[hh][0] + sacc[hh][1]) + (sacc[hh][2] + sacc[hh][3])) +
+                      ((sacc[hh][4] + sacc[hh][5]) + (sacc[hh][6] + sacc[hh][7]));
+        const float ssum = shalf[0] + shalf[1];
         const float sbar = ssum * (1.0f / (float)s2);
         const float rcp = 1.0f / (float)jc; /* the kernel multiplies by 1/j */
         float fnew = (jc == 1) ? sbar : fbar[r] + (sbar - fbar[r]) * rcp;
@@ -648,17 +653,19 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
           const float earg = (m[r] + dmp) - mnew;
           ep = fl16(log2dom ? exp2((double)earg) : exp((double)earg));
         }
-        float lacc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}; /* same chains */
+        float lacc[2][8] = {{0.f}}; /* same chains, per half row */
         for (size_t c = 0; c < s2; ++c) {
           const int masked = sh->causal && (j * s2 + c > pos);
           const double a = fl16(S[c] - cj);
           S[c] = masked ? 0.0 : fl16(log2dom ? exp2(a) : exp(a));
           const int ch = 2 * (int)((c / 2) % 4) + (int)(c % 2);
-          lacc[ch] = lacc[ch] + (float)S[c];
+          lacc[c >= s2 / 2][ch] = lacc[c >= s2 / 2][ch] + (float)S[c];
         }
-        const float lloc = ((lacc[0] + lacc[1]) + (lacc[2] + lacc[3])) +
-                           ((lacc[4] + lacc[5]) + (lacc[6] + lacc[7]));
-        l[r] = (jc == 1) ? lloc : (float)ep * l[r] + lloc;
+        for (int hh = 0; hh < 2; ++hh) { /* each half keeps its own partial l */
+          const float lloc = ((lacc[hh][0] + lacc[hh][1]) + (lacc[hh][2] + lacc[hh][3])) +
+                             ((lacc[hh][4] + lacc[hh][5]) + (lacc[hh][6] + lacc[hh][7]));
+          l[2 * r + hh] = (jc == 1) ? lloc : (float)ep * l[2 * r + hh] + lloc;
+        }
         double* orow = oacc + r * d;
         for (size_t n = 0; n < d; ++n) {
           const double tn = tc_dot(S, 1, vj + n, d, s2, mp->tc_mode);
@@ -670,7 +677,7 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
     }
     for (size_t r = 0; r < s1; ++r) {
       double* dst = o + ((b * sh->Hq + h) * sh->S1 + i * s1 + r) * d;
-      const float invl = 1.0f / l[r];
+      const float invl = 1.0f / (l[2 * r] + l[2 * r + 1]);
       for (size_t n = 0; n < d; ++n) dst[n] = fl16((float)oacc[r * d + n] * invl);
     }
     free(m); free(l); free(fbar); free(oacc); free(S);

@@ -7,8 +7,9 @@
 //   warp 0      TMA producer: Q tiles once, then a K'/V ring (2 stages each)
 //   warp 1      MMA issuer (one elected lane) + TMEM owner (512 columns)
 //   warps 2-3   idle (warpgroup 0 gives its registers away via setmaxnreg)
-//   warps 4-7   softmax/correction warpgroup for tile 0 (thread = row)
-//   warps 8-11  softmax/correction warpgroup for tile 1
+//   warps 4-11  softmax/correction for tile 0: two threads per row (warps
+//               4-7 hold S' columns 0-63, warps 8-11 columns 64-127)
+//   warps 12-19 the same for tile 1
 //
 // Per KV block j and tile t (reference pasa.cpp:256-278, Algorithm 1):
 //   S'_t  = Q_t K'_j^T      tcgen05.mma kind::f16, SS, F16 accumulator in TMEM
@@ -34,6 +35,9 @@ using namespace sm100;
 // < kTraceCtas record clock64() at fixed points of the first kTraceIters
 // blocks -- per softmax warpgroup (warp quadrant 0, lane 0) and for the MMA
 // issuer -- into p.trace[cta][role][iter][event].
+// Alternate the two softmax warpgroups' exp passes (named barriers 1, 2).
+constexpr bool kPingPong = true;
+
 constexpr int kTraceCtas = 4, kTraceIters = 32, kTraceEvents = 8, kTraceRoles = 3;
 #ifdef PASA_TRACE
 #define PASA_TR(role, it, ev)                                                                  \
@@ -61,8 +65,11 @@ struct FwdCfg {
   static constexpr int SMEM_V = SMEM_K + KS * TILE_BYTES;
   static constexpr int SMEM_BAR = SMEM_V + VS * TILE_BYTES;
   static constexpr int NUM_BARS = NT + 2 * KS + 2 * VS + 4 * NT;
-  static constexpr int SMEM_BYTES = SMEM_BAR + NUM_BARS * 8 + 16 + 1024;
-  static constexpr int THREADS = 128 + NT * 128;  // WG0: TMA, MMA, 2 idle; WG1..NT: softmax
+  static constexpr int HALVES = 2;  // threads per row: each owns 64 S' columns, D/2 outputs
+  static constexpr int SMEM_XCH = SMEM_BAR + NUM_BARS * 8 + 16;  // row max/sum exchange
+  static constexpr int XCH_BYTES = 2 * NT * HALVES * kTile * 8;  // [j&1][t][half][row] float2
+  static constexpr int SMEM_BYTES = SMEM_XCH + XCH_BYTES + 1024;
+  static constexpr int THREADS = 128 + NT * HALVES * 128;  // WG0: TMA, MMA, 2 idle; 4 softmax WGs
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t TMEM_TILE = 256;               // S/P at +0, T at +128
 };
@@ -90,12 +97,14 @@ __device__ __forceinline__ uint32_t diag_keep(int i, int row) {
   return (2 * i + 1 <= row) ? 0xFFFFFFFFu : (2 * i <= row ? 0x0000FFFFu : 0u);
 }
 
-// Pass 1 over one S' row (64 packed pairs): max over unmasked columns and the
-// FP32 sum over all s2 columns.  Eight sum chains (pair i -> chain i % 4,
-// lo/hi) and four max chains keep the dependency depth at 16; the reduction
-// order is restated in oracle/pasa_oracle.c (orc_model_pasa).
-template <bool DIAG>
-__device__ __forceinline__ void row_max_sum(const uint32_t* s, int row, float& mloc, float& ssum) {
+// Pass 1 over this thread's half of an S' row (32 packed pairs, global pair
+// index pbase + i): max over unmasked columns and the FP32 sum over all of its
+// columns.  Eight sum chains (pair i -> chain i % 4, lo/hi) and four max
+// chains keep the dependency depth at 8; the reduction order is restated in
+// oracle/pasa_oracle.c (orc_model_pasa).
+template <bool DIAG, int NP>
+__device__ __forceinline__ void row_max_sum(const uint32_t* s, int row, int pbase, float& mloc,
+                                            float& ssum) {
   float acc[8];
   uint32_t mx[4];
 #pragma unroll
@@ -103,13 +112,13 @@ __device__ __forceinline__ void row_max_sum(const uint32_t* s, int row, float& m
 #pragma unroll
   for (int k = 0; k < 4; ++k) mx[k] = 0xFC00FC00u;  // (-inf, -inf)
 #pragma unroll
-  for (int i = 0; i < 64; ++i) {
+  for (int i = 0; i < NP; ++i) {
     const uint32_t v = s[i];
     acc[2 * (i & 3)] = add_lo_f16(acc[2 * (i & 3)], v);
     acc[2 * (i & 3) + 1] = add_hi_f16(acc[2 * (i & 3) + 1], v);
     uint32_t vm = v;
     if (DIAG) {
-      const uint32_t keep = diag_keep(i, row);
+      const uint32_t keep = diag_keep(pbase + i, row);
       vm = (v & keep) | (0xFC00FC00u & ~keep);
     }
     mx[i & 3] = h2_as_u32(__hmax2(u32_as_h2(mx[i & 3]), u32_as_h2(vm)));
@@ -122,20 +131,21 @@ __device__ __forceinline__ void row_max_sum(const uint32_t* s, int row, float& m
                    __fadd_rn(__fadd_rn(acc[4], acc[5]), __fadd_rn(acc[6], acc[7])));
 }
 
-// Pass 2: P = 2^(S' - c_j) in place (masked -> 0) and its FP32 row sum,
-// same eight-chain order as pass 1.  Half the pairs use MUFU ex2.approx.f16x2,
-// half the FMA-pipe polynomial (sm100.cuh), both within 1 ulp of 2^x.
-template <bool DIAG>
-__device__ __forceinline__ float row_exp_sum(uint32_t* s, int row, uint32_t cj2) {
+// Pass 2: P = 2^(S' - c_j) in place (masked -> 0) and its FP32 sum, same
+// eight-chain order as pass 1.  Three pairs in four use MUFU ex2.approx.f16x2,
+// one the FMA-pipe polynomial (sm100.cuh); both are within 1 ulp of 2^x.
+template <bool DIAG, int NP>
+__device__ __forceinline__ float row_exp_sum(uint32_t* s, int row, int pbase, uint32_t cj2) {
   float acc[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc[k] = 0.f;
 #pragma unroll
-  for (int i = 0; i < 64; ++i) {
+  for (int i = 0; i < NP; ++i) {
     const uint32_t x = h2_as_u32(__hsub2(u32_as_h2(s[i]), u32_as_h2(cj2)));
-    // odd pairs on the FMA pipe, even pairs on MUFU: both pipes busy at once
-    uint32_t pv = (i & 1) ? ex2_poly_f16x2(x) : ex2_f16x2(x);
-    if (DIAG) pv &= diag_keep(i, row);
+    // one pair in four on the FMA pipe, the rest on MUFU: balances MUFU time
+    // (8 cycles / pair / SMSP) against issue slots (poly ~11 vs MUFU 3 per pair)
+    uint32_t pv = ((i & 3) == 3) ? ex2_poly_f16x2(x) : ex2_f16x2(x);
+    if (DIAG) pv &= diag_keep(pbase + i, row);
     acc[2 * (i & 3)] = add_lo_f16(acc[2 * (i & 3)], pv);
     acc[2 * (i & 3) + 1] = add_hi_f16(acc[2 * (i & 3) + 1], pv);
     s[i] = pv;
@@ -183,9 +193,9 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     for (int t = 0; t < NT; ++t) {
       mbar_init(&q_full[t], 1);
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], 4);
+      mbar_init(&p_full[t], 4 * Cfg::HALVES);
       mbar_init(&t_full[t], 1);
-      mbar_init(&t_empty[t], 4);
+      mbar_init(&t_empty[t], 4 * Cfg::HALVES);
     }
     for (int s = 0; s < KS; ++s) {
       mbar_init(&k_full[s], 1);
@@ -204,7 +214,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
   const uint32_t tmem_base = *tmem_holder;
 
   if (warp < 4) {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
@@ -301,14 +311,25 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     }
   }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
     // ------------------------------------------------------------ softmax WGs
-    const int t = (warp - 4) / 4;
+    // Two threads per row: warps 4-7 / 8-11 hold columns 0-63 / 64-127 of
+    // tile 0's rows, warps 12-15 / 16-19 those of tile 1.  Row max and sum are
+    // exchanged through shared memory (named barrier per quadrant pair); each
+    // thread keeps its own partial l and D/2 output columns.
+    const int sw = warp - 4;
+    const int t = sw / 8;
+    const int h = (sw / 4) & 1;
     const int quad = warp % 4;  // TMEM lane quadrant this warp may access
     const int row = quad * 32 + lane;
     const TileInfo ti = tile_info(p, hkv, blockIdx.y * NT + t, CAUSAL);
     const uint32_t t_s = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + t * Cfg::TMEM_TILE;
     const uint32_t t_t = t_s + 128;
+    float2* xch = reinterpret_cast<float2*>(smem + Cfg::SMEM_XCH);
+    auto xslot = [&](int parity, int half) -> float2* {
+      return xch + ((parity * NT + t) * Cfg::HALVES + half) * kTile + row;
+    };
+    const uint32_t xbar = 3 + t * 4 + quad;  // named barrier of this row quadrant's two warps
     if (ti.nblk > 0) {
       // Inflation c0 (log2 units) keeping l * max|V| below 2^14.
       const float vm = p.vmax[b * p.Hkv + hkv];
@@ -318,24 +339,34 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         const int e = ilogbf(need);
         c0 = static_cast<float>(ldexpf(1.0f, e) == need ? e : e + 1);
       }
-      uint32_t o[D / 2];
-      uint32_t s[64];
+      constexpr int NP = 32;  // pairs per thread
+      uint32_t o[D / 4];
+      uint32_t s[NP];
       float m_run = 0.f, l_run = 0.f, fbar = 0.f;
       float rcp_j = 1.0f;  // 1/(j+1), computed off the critical path
+      // both tiles' block counts (identical in every thread of the CTA)
+      const int nmin = min(tile_info(p, hkv, blockIdx.y * NT, CAUSAL).nblk,
+                           tile_info(p, hkv, blockIdx.y * NT + 1, CAUSAL).nblk);
+      const bool pingpong = kPingPong;
       for (int j = 0; j < ti.nblk; ++j) {
-        const bool tr = quad == 0 && lane == 0;
+        const bool tr = h == 0 && quad == 0 && lane == 0;
         if (tr) PASA_TR(t, j, 0);
         mbar_wait(&s_full[t], j & 1);
         if (tr) PASA_TR(t, j, 1);
         tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld_32cols_pack16(t_s + c * 32, s + c * 16);
+        tmem_ld_32cols_pack16(t_s + 64 * h, s);
+        tmem_ld_32cols_pack16(t_s + 64 * h + 32, s + 16);
         tmem_wait_ld();
         if (tr) PASA_TR(t, j, 2);
         const bool diag = CAUSAL && (j == ti.nblk - 1);
-        float mloc, ssum;
-        if (diag) row_max_sum<true>(s, row, mloc, ssum);
-        else row_max_sum<false>(s, row, mloc, ssum);
+        float mh, sh;
+        if (diag) row_max_sum<true, NP>(s, row, NP * h, mh, sh);
+        else row_max_sum<false, NP>(s, row, NP * h, mh, sh);
+        *xslot(j & 1, h) = make_float2(mh, sh);
+        named_bar_sync(xbar, 64);
+        const float2 other = *xslot(j & 1, 1 - h);
+        const float mloc = fmaxf(mh, other.x);
+        const float ssum = h == 0 ? __fadd_rn(sh, other.y) : __fadd_rn(other.y, sh);
         const float sbar = __fmul_rn(ssum, 1.0f / 128.0f);
         const int jc = j + 1;
         const float fnew =
@@ -347,12 +378,19 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         const float mnew = (jc == 1) ? cand : fmaxf(mprev, cand);
         const __half cj = __float2half_rn(__fadd_rn(__fsub_rn(mnew, dmc), c0));
         const float ep = (jc == 1) ? 0.f : __half2float(__float2half_rn(ex2_f32(__fsub_rn(mprev, mnew))));
-        // pass 2: P = 2^(S' - c_j) in f16x2, masked entries -> 0, FP32 row sum
         if (tr) PASA_TR(t, j, 3);
+        // Ping-pong the MUFU-heavy exp pass between the two tiles:
+        // turns go T0(0), T1(0), T0(1), T1(1), ... while both tiles have blocks.
+        if (pingpong && j < nmin && (t == 1 || j > 0)) named_bar_sync(1 + t, 512);
         const uint32_t cj2 = h2_as_u32(__half2half2(cj));
-        const float lsum = diag ? row_exp_sum<true>(s, row, cj2) : row_exp_sum<false>(s, row, cj2);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_st_16cols_b32(t_s + c * 16, s + c * 16);
+        const float lsum = diag ? row_exp_sum<true, NP>(s, row, NP * h, cj2)
+                                : row_exp_sum<false, NP>(s, row, NP * h, cj2);
+        if (pingpong && ((t == 0 && j < nmin) || (t == 1 && j + 1 < nmin)))
+          named_bar_arrive(2 - t, 512);
+        if (tr) PASA_TR(t, j, 7);
+        // P packed two per column: this half's 32 pairs -> columns [32h, 32h + 32)
+        tmem_st_16cols_b32(t_s + NP * h, s);
+        tmem_st_16cols_b32(t_s + NP * h + 16, s + 16);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -362,12 +400,12 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         m_run = mnew;
         fbar = fnew;
         rcp_j = __frcp_rn(static_cast<float>(jc + 1));
-        // T = P V_j -> O
+        // T = P V_j -> this half's D/2 output columns
         mbar_wait(&t_full[t], j & 1);
         if (tr) PASA_TR(t, j, 5);
         tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) tmem_ld_32cols_pack16(t_t + c * 32, s + c * 16);
+        for (int c = 0; c < D / 64; ++c) tmem_ld_32cols_pack16(t_t + (D / 2) * h + c * 32, s + c * 16);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
@@ -375,20 +413,24 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         if (tr) PASA_TR(t, j, 6);
         if (jc == 1) {
 #pragma unroll
-          for (int i = 0; i < D / 2; ++i) o[i] = s[i];
+          for (int i = 0; i < D / 4; ++i) o[i] = s[i];
         } else {
           const __half2 ep2 = __float2half2_rn(ep);
 #pragma unroll
-          for (int i = 0; i < D / 2; ++i)
+          for (int i = 0; i < D / 4; ++i)
             o[i] = h2_as_u32(__hfma2(ep2, u32_as_h2(o[i]), u32_as_h2(s[i])));
         }
       }
       // Epilogue: global recovering O / l (pasa.cpp:184-194), fp16 store.
-      const float inv_l = __frcp_rn(l_run);
+      *xslot(ti.nblk & 1, h) = make_float2(l_run, 0.f);
+      named_bar_sync(xbar, 64);
+      const float lo_other = xslot(ti.nblk & 1, 1 - h)->x;
+      const float l_tot = h == 0 ? __fadd_rn(l_run, lo_other) : __fadd_rn(lo_other, l_run);
+      const float inv_l = __frcp_rn(l_tot);
       uint16_t* dst = p.out + ((static_cast<size_t>(b) * p.Hq + ti.hq) * p.S1 +
-                               static_cast<size_t>(ti.i) * kTile + row) * D;
+                               static_cast<size_t>(ti.i) * kTile + row) * D + (D / 2) * h;
 #pragma unroll
-      for (int i = 0; i < D / 2; i += 4) {
+      for (int i = 0; i < D / 4; i += 4) {
         uint32_t w[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {

@@ -57,7 +57,7 @@ def main():
         rel = np.where(t[c] > 0, t[c] - base, -1)
         res[c] = rel.tolist()
         print(f"=== CTA y={c}")
-        print(" j | WG0: waitS  ldS  p1+sc  p2+st  waitT  ldT  O   | WG1: waitS  ldS  p1+sc  p2+st  waitT  ldT  O | period0 period1")
+        print(" j | WG0: waitS  ldS  p1+sc  p2  stP  waitT  ldT  O   | WG1: waitS  ldS  p1+sc  p2  stP  waitT  ldT  O | period0 period1")
         for j in range(1, ITERS - 1):
             row = []
             for w in range(2):
@@ -67,8 +67,8 @@ def main():
                     continue
                 nxt = rel[w, j + 1][0]
                 row.append(" ".join(f"{x:5d}" for x in [e[1] - e[0], e[2] - e[1], e[3] - e[2],
-                                                         e[4] - e[3], e[5] - e[4], e[6] - e[5],
-                                                         (nxt - e[6]) if nxt > 0 else -1]))
+                                                         e[7] - e[3], e[4] - e[7], e[5] - e[4],
+                                                         e[6] - e[5], (nxt - e[6]) if nxt > 0 else -1]))
             per = [rel[w, j + 1][0] - rel[w, j][0] if rel[w, j + 1][0] > 0 else -1 for w in range(2)]
             print(f"{j:2d} | {row[0]} | {row[1]} | {per[0]:6d} {per[1]:6d}")
         m = rel[2]
