@@ -213,8 +213,10 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
+  // Register budget: 640 threads x 96 at launch = 61440 per CTA; setmaxnreg
+  // moves registers only within the CTA: 128 x 56 + 512 x 104 = 60416.
   if (warp < 4) {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     }
   }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 112;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
     // ------------------------------------------------------------ softmax WGs
     // Two threads per row: warps 4-7 / 8-11 hold columns 0-63 / 64-127 of
     // tile 0's rows, warps 12-15 / 16-19 those of tile 1.  Row max and sum are
