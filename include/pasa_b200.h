@@ -54,7 +54,7 @@ typedef struct pasa_b200_desc {
   int32_t s2;        /* KV block = shifting-matrix size; this build: 128       */
   int32_t causal;    /* 0: reference semantics; 1: causal (requires S1 == S2) */
   int32_t reserved;
-  double beta;       /* shift fraction in (0, 1) (pasa.cpp:98-101)              */
+  double beta;       /* shift fraction in [0, 1) (pasa.cpp:98-101); 0 = FP16 FA */
   double alpha;      /* static scale, must equal sqrt(d) (pasa.cpp:206-208)     */
 } pasa_b200_desc;
 
@@ -105,7 +105,8 @@ PASA_B200_API int pasa_b200_preprocess_keys_host(const pasa_b200_desc* desc, con
 
 /* The PASA forward, device pointers, stream-ordered, asynchronous.
  * Replaces pasa::pasa_attention (pasa.hpp:95-99, pasa.cpp:196-293) for the
- * PASA_FP16 policy.  workspace must hold pasa_b200_workspace_size() bytes.
+ * PASA_FP16 policy; beta == 0 runs pasa_b200_flash_fp16_fwd like the reference
+ * (pasa.cpp:212-221).  workspace must hold pasa_b200_workspace_size() bytes.
  * stream is a cudaStream_t (NULL = legacy default stream). */
 PASA_B200_API int pasa_b200_attention_fwd(const pasa_b200_desc* desc, const void* q, const void* k,
                             const void* v, void* o, void* workspace, size_t workspace_bytes,
@@ -117,6 +118,15 @@ PASA_B200_API int pasa_b200_attention_fwd(const pasa_b200_desc* desc, const void
 PASA_B200_API int pasa_b200_attention_fwd_prepped(const pasa_b200_desc* desc, const void* q,
                                                   const void* kp, const void* v, const float* vmax,
                                                   void* o, void* stream);
+
+/* The naive FP16 FlashAttention on the same pipeline: flash_attention with
+ * the FA_PARTIAL_FP16 policy (attention.cpp:92-180): raw K, FP16 score store,
+ * the 1/alpha scale applied AFTER the store (so |QK^T| > 65504 overflows to
+ * inf and the output to NaN, :134-136), FP16 running max, no shift.  desc->beta
+ * is ignored; pasa_b200_attention_fwd routes beta == 0 here (pasa.cpp:212-221).
+ * The baseline PASA is measured against. */
+PASA_B200_API int pasa_b200_flash_fp16_fwd(const pasa_b200_desc* desc, const void* q,
+                                           const void* k, const void* v, void* o, void* stream);
 
 /* pasa_b200_attention_fwd from HOST buffers (binary16 bit patterns): copies
  * Q, K, V in, runs, copies O back and synchronizes.  The drop-in for a CPU

@@ -120,6 +120,7 @@ class Oracle:
         L.orc_model_inflation.argtypes = [C.c_double, C.c_size_t, C.c_double]
         L.orc_model_pasa.argtypes = [C.POINTER(Shape), _dp, _dp, _dp, _dp,
                                      C.POINTER(ModelParams), C.c_int]
+        L.orc_model_fa16.argtypes = [C.POINTER(Shape), _dp, _dp, _dp, _dp, C.c_int, C.c_int]
 
     # -- scalars -----------------------------------------------------------
     def f16(self, x):
@@ -239,6 +240,17 @@ class Oracle:
                                      C.byref(mp), threads)
         if rc:
             raise ValueError(f"model_pasa: rc={rc}")
+        return o
+
+
+    def model_fa16(self, pb: Problem, tc_mode: int = 1, threads: int = 0) -> np.ndarray:
+        """The kernel's beta == 0 mode: naive FP16 FlashAttention (see pasa_oracle.c)."""
+        o = np.empty(pb.q.shape)
+        sh = pb.shape()
+        rc = self.lib.orc_model_fa16(C.byref(sh), _f64(pb.q), _f64(pb.k), _f64(pb.v), o, tc_mode,
+                                     threads)
+        if rc:
+            raise ValueError(f"model_fa16: rc={rc}")
         return o
 
 

@@ -685,3 +685,83 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
   free(kp);
   return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Model of the kernel's FA16 mode (the naive FP16 FlashAttention, beta = 0, */
+/* attention.cpp:92-180 with FA_PARTIAL_FP16): raw K, FP16 score store (F16  */
+/* accumulator), scale applied after the store by one HFMA2                  */
+/* x = fl16(S * fl16(s) - fl16(m * s)) with s = fl32(log2 e / alpha), FP32   */
+/* running max of the stored scores, P = fl16(2^x), FP32 half-row l, FP16 O  */
+/* via fl16(e_p * O + T).  Overflow of the store propagates to NaN exactly   */
+/* like the reference.                                                       */
+/* ------------------------------------------------------------------------ */
+ORC_API int orc_model_fa16(const orc_shape* sh, const double* q, const double* k,
+                           const double* v, double* o, int tc_mode, int threads) {
+  if (sh->Hq % sh->Hkv) return -1;
+  if (sh->S1 % sh->s1 || sh->S2 % sh->s2) return -2;
+  if (sh->causal && sh->S1 + sh->q_offset > sh->S2) return -4;
+  const size_t s1 = sh->s1, s2 = sh->s2, d = sh->d;
+  const size_t nq = sh->S1 / s1, nkv = sh->S2 / s2, grp = sh->Hq / sh->Hkv;
+  const float scale_f = (float)(1.4426950408889634 / sqrt((double)d));
+  const double scale_h = fl16((double)scale_f);
+  const int nt = resolve_threads(threads);
+#pragma omp parallel for num_threads(nt) schedule(dynamic)
+  for (long long x = 0; x < (long long)(sh->B * sh->Hq * nq); ++x) {
+    const size_t i = (size_t)x % nq;
+    const size_t h = ((size_t)x / nq) % sh->Hq;
+    const size_t b = (size_t)x / (nq * sh->Hq);
+    const size_t hk = h / grp;
+    float* m = calloc(s1, sizeof(float));
+    float* l = calloc(2 * s1, sizeof(float));
+    double* oacc = calloc(s1 * d, sizeof(double));
+    double* S = malloc(sizeof(double) * s2);
+    size_t jc = 0;
+    for (size_t j = 0; j < nkv; ++j) {
+      const size_t row0 = sh->q_offset + i * s1;
+      if (sh->causal && j * s2 > row0 + s1 - 1) break;
+      ++jc;
+      const double* kj = row_ptr(k, sh->Hkv, sh->S2, d, b, hk, j * s2);
+      const double* vj = row_ptr(v, sh->Hkv, sh->S2, d, b, hk, j * s2);
+      for (size_t r = 0; r < s1; ++r) {
+        const double* qr = row_ptr(q, sh->Hq, sh->S1, d, b, h, i * s1 + r);
+        const size_t pos = row0 + r;
+        double mloc = -INFINITY;
+        for (size_t c = 0; c < s2; ++c) {
+          S[c] = tc_dot(qr, 1, kj + c * d, 1, d, tc_mode);
+          const int masked = sh->causal && (j * s2 + c > pos);
+          if (!masked && S[c] > mloc) mloc = S[c];
+        }
+        const float mnew = (jc == 1) ? (float)mloc : fmaxf(m[r], (float)mloc);
+        double ep = 0.0;
+        if (jc > 1) ep = fl16(exp2((double)((m[r] - mnew) * scale_f)));
+        const double ms = fl16((double)(mnew * scale_f));
+        float lacc[2][8] = {{0.f}};
+        for (size_t c = 0; c < s2; ++c) {
+          const int masked = sh->causal && (j * s2 + c > pos);
+          const double a = fl16(S[c] * scale_h - ms);
+          S[c] = masked ? 0.0 : fl16(exp2(a));
+          const int ch = 2 * (int)((c / 2) % 4) + (int)(c % 2);
+          lacc[c >= s2 / 2][ch] = lacc[c >= s2 / 2][ch] + (float)S[c];
+        }
+        for (int hh = 0; hh < 2; ++hh) {
+          const float lloc = ((lacc[hh][0] + lacc[hh][1]) + (lacc[hh][2] + lacc[hh][3])) +
+                             ((lacc[hh][4] + lacc[hh][5]) + (lacc[hh][6] + lacc[hh][7]));
+          l[2 * r + hh] = (jc == 1) ? lloc : (float)ep * l[2 * r + hh] + lloc;
+        }
+        double* orow = oacc + r * d;
+        for (size_t n = 0; n < d; ++n) {
+          const double tn = tc_dot(S, 1, vj + n, d, s2, tc_mode);
+          orow[n] = (jc == 1) ? tn : fl16(ep * orow[n] + tn);
+        }
+        m[r] = mnew;
+      }
+    }
+    for (size_t r = 0; r < s1; ++r) {
+      double* dst = o + ((b * sh->Hq + h) * sh->S1 + i * s1 + r) * d;
+      const float invl = 1.0f / (l[2 * r] + l[2 * r + 1]);
+      for (size_t n = 0; n < d; ++n) dst[n] = fl16((float)oacc[r * d + n] * invl);
+    }
+    free(m); free(l); free(oacc); free(S);
+  }
+  return 0;
+}

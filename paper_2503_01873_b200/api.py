@@ -254,6 +254,40 @@ def pasa_attention_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, beta: 
     return out
 
 
+def flash_fp16_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: bool = False,
+                   s1: int = 128, s2: int = 128, out: torch.Tensor | None = None,
+                   stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """The naive FP16 FlashAttention baseline on the same pipeline (FA_PARTIAL_FP16
+    semantics of flash_attention, attention.cpp:92-180): scale after the FP16 score
+    store, so inputs whose |QK^T| exceeds 65504 produce NaN -- the failure PASA removes."""
+    L = _lib.load()
+    q, k, v = (t if t.is_contiguous() else t.contiguous() for t in (q, k, v))
+    desc = _desc(q, k, s1, s2, 0.0, math.sqrt(float(q.shape[-1])), causal)
+    _lib.check(L.pasa_b200_check(C.byref(desc)))
+    if out is None:
+        out = torch.empty_like(q)
+    st = (stream or torch.cuda.current_stream(q.device)).cuda_stream
+    _lib.check(L.pasa_b200_flash_fp16_fwd(C.byref(desc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                          out.data_ptr(), st))
+    return out
+
+
+def flash_attention(problem: AttentionProblem, policy: PrecisionPolicy | PolicyId,
+                    opts: AttnOptions | None = None) -> torch.Tensor:
+    """attention.hpp:57-60 on the B200: the FA_PARTIAL_FP16 policy only (the
+    reference's partial-FP16 FlashAttention); FP64/FP32 policies are CPU-oracle features."""
+    opts = opts or AttnOptions()
+    pol = policy if isinstance(policy, PrecisionPolicy) else policy_for(policy)
+    if (pol.gemm_accum, pol.gemm_store, pol.vector_prec) != (Prec.FP32, Prec.FP16, Prec.FP16):
+        raise ValueError(f"flash_attention on B200 implements FA_PARTIAL_FP16 only, got {pol.id.name}")
+    if opts.m0 != M0Mode.NEG_INF:
+        raise ValueError("flash_attention on B200 implements m0 = -inf only")
+    q, k, v = problem.q, problem.k, problem.v
+    if not q.is_cuda:
+        raise ValueError("flash_attention on B200 expects CUDA tensors")
+    return flash_fp16_fwd(q, k, v, opts.causal, problem.s1, problem.s2)
+
+
 def preprocess_keys(k: torch.Tensor, params: PasaParams, lscale: float = 1.0,
                     v: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
     """Batched K'_j = K_j^T M on device (pasa.cpp:53-56, loop :231-240).
@@ -286,6 +320,8 @@ def pasa_attention(problem: AttentionProblem, params: PasaParams,
         raise ValueError("pasa: params.alpha does not match sqrt(d)")
     if params.beta == 1.0:
         raise ValueError("pasa: beta == 1 has no recovery")
+    if params.beta == 0.0:  # degrades to the blocked FP16 attention (pasa.cpp:212-221)
+        return flash_attention(problem, pol, opts)
     if pol.id != PolicyId.PASA_FP16:
         raise ValueError(f"pasa_attention on B200 implements PASA_FP16 only, got {pol.id.name}")
     q, k, v = problem.q, problem.k, problem.v

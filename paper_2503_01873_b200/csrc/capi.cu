@@ -19,7 +19,7 @@
 
 namespace pasa_b200 {
 cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stream);
-cudaError_t launch_fwd(int D, bool causal, const CUtensorMap& tq, const CUtensorMap& tk,
+cudaError_t launch_fwd(int D, bool causal, int mode, const CUtensorMap& tq, const CUtensorMap& tk,
                        const CUtensorMap& tv, const FwdParams& p, cudaStream_t stream);
 }  // namespace pasa_b200
 
@@ -98,9 +98,6 @@ int check_desc(const pasa_b200_desc* d) {
   if (d->alpha != std::sqrt(static_cast<double>(d->head_dim)))
     return fail(PASA_B200_EINVAL, "pasa: params.alpha does not match sqrt(d)");  // pasa.cpp:206-208
   // ---- limits of this build (valid for the reference, unsupported here)
-  if (d->beta == 0.0)
-    return fail(PASA_B200_EUNSUPPORTED,
-                "beta == 0 routes to flash_attention (pasa.cpp:212-221); not in this build");
   if (d->head_dim != 64 && d->head_dim != 128)
     return fail(PASA_B200_EUNSUPPORTED, "head_dim must be 64 or 128");
   if (d->s2 != kTile) return fail(PASA_B200_EUNSUPPORTED, "s2 must be 128");
@@ -214,19 +211,15 @@ int pasa_b200_preprocess_keys_host(const pasa_b200_desc* d, const uint16_t* k, u
   return rc;
 }
 
-int pasa_b200_attention_fwd_prepped(const pasa_b200_desc* d, const void* q, const void* kp,
-                                    const void* v, const float* vmax, void* o, void* stream) {
-  g_last_error.clear();
-  int rc = check_desc(d);
-  if (rc) return rc;
-  if (!q || !kp || !v || !o || !vmax)
-    return fail(PASA_B200_EINVAL, "attention_fwd: NULL tensor");
-  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(kp) |
+static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, const void* keys,
+                          const void* v, const float* vmax, void* o, void* stream) {
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(keys) |
        reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(o)) & 15)
     return fail(PASA_B200_EINVAL, "attention_fwd: tensors must be 16-byte aligned");
+  int rc;
   CUtensorMap tq, tk, tv;
   if ((rc = make_tmap(&tq, q, d->head_dim, d->seq_q, d->batch * d->heads_q))) return rc;
-  if ((rc = make_tmap(&tk, kp, d->head_dim, d->seq_kv, d->batch * d->heads_kv))) return rc;
+  if ((rc = make_tmap(&tk, keys, d->head_dim, d->seq_kv, d->batch * d->heads_kv))) return rc;
   if ((rc = make_tmap(&tv, v, d->head_dim, d->seq_kv, d->batch * d->heads_kv))) return rc;
   FwdParams p{};
   p.B = d->batch;
@@ -239,13 +232,35 @@ int pasa_b200_attention_fwd_prepped(const pasa_b200_desc* d, const void* q, cons
   p.group = d->heads_q / d->heads_kv;
   p.tiles_per_kv = p.group * p.nq;
   p.inva = static_cast<float>(d->beta / (1.0 - d->beta));  // pasa.cpp:85
+  p.qk_scale = static_cast<float>(kLog2e / d->alpha);
   p.vmax = vmax;
   p.out = static_cast<uint16_t*>(o);
   p.trace = g_trace;
-  cudaError_t e = launch_fwd(d->head_dim, d->causal != 0, tq, tk, tv, p,
+  cudaError_t e = launch_fwd(d->head_dim, d->causal != 0, mode, tq, tk, tv, p,
                              static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "pasa_fwd launch");
   return PASA_B200_OK;
+}
+
+int pasa_b200_attention_fwd_prepped(const pasa_b200_desc* d, const void* q, const void* kp,
+                                    const void* v, const float* vmax, void* o, void* stream) {
+  g_last_error.clear();
+  int rc = check_desc(d);
+  if (rc) return rc;
+  if (!q || !kp || !v || !o || !vmax)
+    return fail(PASA_B200_EINVAL, "attention_fwd: NULL tensor");
+  if (d->beta == 0.0)
+    return fail(PASA_B200_EINVAL, "attention_fwd_prepped: beta == 0 has no key pre-pass");
+  return launch_forward(d, kModePasa, q, kp, v, vmax, o, stream);
+}
+
+int pasa_b200_flash_fp16_fwd(const pasa_b200_desc* d, const void* q, const void* k, const void* v,
+                             void* o, void* stream) {
+  g_last_error.clear();
+  int rc = check_desc(d);
+  if (rc) return rc;
+  if (!q || !k || !v || !o) return fail(PASA_B200_EINVAL, "flash_fp16_fwd: NULL tensor");
+  return launch_forward(d, kModeFa16, q, k, v, nullptr, o, stream);
 }
 
 int pasa_b200_attention_fwd(const pasa_b200_desc* d, const void* q, const void* k, const void* v,
@@ -259,6 +274,8 @@ int pasa_b200_attention_fwd(const pasa_b200_desc* d, const void* q, const void* 
   if (workspace_bytes < pasa_b200_workspace_size(d))
     return fail(PASA_B200_EINVAL, "attention_fwd: workspace too small");
   (void)diag;
+  // beta == 0 degrades to the blocked FP16 attention (pasa.cpp:212-221)
+  if (d->beta == 0.0) return launch_forward(d, kModeFa16, q, k, v, nullptr, o, stream);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   void* kp = ws;
   float* vmax = reinterpret_cast<float*>(ws + align_up(kp_bytes(d), 256));

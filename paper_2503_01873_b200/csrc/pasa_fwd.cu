@@ -102,7 +102,7 @@ __device__ __forceinline__ uint32_t diag_keep(int i, int row) {
 // columns.  Eight sum chains (pair i -> chain i % 4, lo/hi) and four max
 // chains keep the dependency depth at 8; the reduction order is restated in
 // oracle/pasa_oracle.c (orc_model_pasa).
-template <bool DIAG, int NP>
+template <bool DIAG, int NP, bool SUM = true>
 __device__ __forceinline__ void row_max_sum(const uint32_t* s, int row, int pbase, float& mloc,
                                             float& ssum) {
   float acc[8];
@@ -114,8 +114,10 @@ __device__ __forceinline__ void row_max_sum(const uint32_t* s, int row, int pbas
 #pragma unroll
   for (int i = 0; i < NP; ++i) {
     const uint32_t v = s[i];
-    acc[2 * (i & 3)] = add_lo_f16(acc[2 * (i & 3)], v);
-    acc[2 * (i & 3) + 1] = add_hi_f16(acc[2 * (i & 3) + 1], v);
+    if (SUM) {
+      acc[2 * (i & 3)] = add_lo_f16(acc[2 * (i & 3)], v);
+      acc[2 * (i & 3) + 1] = add_hi_f16(acc[2 * (i & 3) + 1], v);
+    }
     uint32_t vm = v;
     if (DIAG) {
       const uint32_t keep = diag_keep(pbase + i, row);
@@ -134,14 +136,17 @@ __device__ __forceinline__ void row_max_sum(const uint32_t* s, int row, int pbas
 // Pass 2: P = 2^(S' - c_j) in place (masked -> 0) and its FP32 sum, same
 // eight-chain order as pass 1.  Three pairs in four use MUFU ex2.approx.f16x2,
 // one the FMA-pipe polynomial (sm100.cuh); both are within 1 ulp of 2^x.
-template <bool DIAG, int NP>
-__device__ __forceinline__ float row_exp_sum(uint32_t* s, int row, int pbase, uint32_t cj2) {
+template <bool DIAG, int NP, bool FA = false>
+__device__ __forceinline__ float row_exp_sum(uint32_t* s, int row, int pbase, uint32_t cj2,
+                                             uint32_t scale2 = 0) {
   float acc[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc[k] = 0.f;
 #pragma unroll
   for (int i = 0; i < NP; ++i) {
-    const uint32_t x = h2_as_u32(__hsub2(u32_as_h2(s[i]), u32_as_h2(cj2)));
+    // PASA: x = S' - c_j.  FA16: x = S*(log2e/alpha) - m*(log2e/alpha) in one HFMA2.
+    const uint32_t x = FA ? h2_as_u32(__hfma2(u32_as_h2(s[i]), u32_as_h2(scale2), u32_as_h2(cj2)))
+                          : h2_as_u32(__hsub2(u32_as_h2(s[i]), u32_as_h2(cj2)));
     // one pair in four on the FMA pipe, the rest on MUFU: balances MUFU time
     // (8 cycles / pair / SMSP) against issue slots (poly ~11 vs MUFU 3 per pair)
     uint32_t pv = ((i & 3) == 3) ? ex2_poly_f16x2(x) : ex2_f16x2(x);
@@ -156,7 +161,7 @@ __device__ __forceinline__ float row_exp_sum(uint32_t* s, int row, int pbase, ui
 
 }  // namespace
 
-template <int D, bool CAUSAL>
+template <int D, bool CAUSAL, int MODE>
 __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     pasa_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_kp,
@@ -334,10 +339,10 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     const uint32_t xbar = 3 + t * 4 + quad;  // named barrier of this row quadrant's two warps
     if (ti.nblk > 0) {
       // Inflation c0 (log2 units) keeping l * max|V| below 2^14.
-      const float vm = p.vmax[b * p.Hkv + hkv];
+      const float vm = MODE == kModePasa ? p.vmax[b * p.Hkv + hkv] : 0.f;
       const float need = __fmul_rn(__fmul_rn(static_cast<float>(p.S2), vm), 1.0f / 16384.0f);
       float c0 = 0.f;
-      if (need > 1.0f) {
+      if (MODE == kModePasa && need > 1.0f) {
         const int e = ilogbf(need);
         c0 = static_cast<float>(ldexpf(1.0f, e) == need ? e : e + 1);
       }
@@ -361,32 +366,45 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         tmem_wait_ld();
         if (tr) PASA_TR(t, j, 2);
         const bool diag = CAUSAL && (j == ti.nblk - 1);
-        float mh, sh;
-        if (diag) row_max_sum<true, NP>(s, row, NP * h, mh, sh);
-        else row_max_sum<false, NP>(s, row, NP * h, mh, sh);
+        constexpr bool kSum = MODE == kModePasa;
+        float mh, sh = 0.f;
+        if (diag) row_max_sum<true, NP, kSum>(s, row, NP * h, mh, sh);
+        else row_max_sum<false, NP, kSum>(s, row, NP * h, mh, sh);
         *xslot(j & 1, h) = make_float2(mh, sh);
         named_bar_sync(xbar, 64);
         const float2 other = *xslot(j & 1, 1 - h);
         const float mloc = fmaxf(mh, other.x);
-        const float ssum = h == 0 ? __fadd_rn(sh, other.y) : __fadd_rn(other.y, sh);
-        const float sbar = __fmul_rn(ssum, 1.0f / 128.0f);
         const int jc = j + 1;
-        const float fnew =
-            (jc == 1) ? sbar : __fadd_rn(fbar, __fmul_rn(__fsub_rn(sbar, fbar), rcp_j));
-        const float dmc = __fmul_rn(p.inva, __fsub_rn(sbar, fnew));
-        const float dmp = (jc == 1) ? 0.f : __fmul_rn(p.inva, __fsub_rn(fbar, fnew));
-        const float cand = __fadd_rn(mloc, dmc);
-        const float mprev = __fadd_rn(m_run, dmp);
-        const float mnew = (jc == 1) ? cand : fmaxf(mprev, cand);
-        const __half cj = __float2half_rn(__fadd_rn(__fsub_rn(mnew, dmc), c0));
-        const float ep = (jc == 1) ? 0.f : __half2float(__float2half_rn(ex2_f32(__fsub_rn(mprev, mnew))));
+        float mnew, ep, fnew = 0.f;
+        uint32_t cj2, scale2 = 0;
+        if (MODE == kModePasa) {
+          const float ssum = h == 0 ? __fadd_rn(sh, other.y) : __fadd_rn(other.y, sh);
+          const float sbar = __fmul_rn(ssum, 1.0f / 128.0f);
+          fnew = (jc == 1) ? sbar : __fadd_rn(fbar, __fmul_rn(__fsub_rn(sbar, fbar), rcp_j));
+          const float dmc = __fmul_rn(p.inva, __fsub_rn(sbar, fnew));
+          const float dmp = (jc == 1) ? 0.f : __fmul_rn(p.inva, __fsub_rn(fbar, fnew));
+          const float cand = __fadd_rn(mloc, dmc);
+          const float mprev = __fadd_rn(m_run, dmp);
+          mnew = (jc == 1) ? cand : fmaxf(mprev, cand);
+          const __half cj = __float2half_rn(__fadd_rn(__fsub_rn(mnew, dmc), c0));
+          ep = (jc == 1) ? 0.f : __half2float(__float2half_rn(ex2_f32(__fsub_rn(mprev, mnew))));
+          cj2 = h2_as_u32(__half2half2(cj));
+        } else {
+          // naive FP16 FA (attention.cpp:92-180): running max of the FP16-stored
+          // scores, P = 2^(S*s - m*s) with s = log2(e)/alpha applied after the store
+          mnew = (jc == 1) ? mloc : fmaxf(m_run, mloc);
+          ep = (jc == 1) ? 0.f
+                         : __half2float(__float2half_rn(ex2_f32(__fmul_rn(__fsub_rn(m_run, mnew), p.qk_scale))));
+          cj2 = h2_as_u32(__half2half2(__hneg(__float2half_rn(__fmul_rn(mnew, p.qk_scale)))));
+          scale2 = h2_as_u32(__half2half2(__float2half_rn(p.qk_scale)));
+        }
         if (tr) PASA_TR(t, j, 3);
         // Ping-pong the MUFU-heavy exp pass between the two tiles:
         // turns go T0(0), T1(0), T0(1), T1(1), ... while both tiles have blocks.
         if (pingpong && j < nmin && (t == 1 || j > 0)) named_bar_sync(1 + t, 512);
-        const uint32_t cj2 = h2_as_u32(__half2half2(cj));
-        const float lsum = diag ? row_exp_sum<true, NP>(s, row, NP * h, cj2)
-                                : row_exp_sum<false, NP>(s, row, NP * h, cj2);
+        constexpr bool kFa = MODE == kModeFa16;
+        const float lsum = diag ? row_exp_sum<true, NP, kFa>(s, row, NP * h, cj2, scale2)
+                                : row_exp_sum<false, NP, kFa>(s, row, NP * h, cj2, scale2);
         if (pingpong && ((t == 0 && j < nmin) || (t == 1 && j + 1 < nmin)))
           named_bar_arrive(2 - t, 512);
         if (tr) PASA_TR(t, j, 7);
@@ -451,11 +469,11 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
 }
 
 // ---------------------------------------------------------------- launcher
-template <int D, bool CAUSAL>
+template <int D, bool CAUSAL, int MODE>
 cudaError_t launch_fwd_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                          const FwdParams& p, cudaStream_t stream) {
   using Cfg = FwdCfg<D>;
-  auto kern = pasa_fwd_kernel<D, CAUSAL>;
+  auto kern = pasa_fwd_kernel<D, CAUSAL, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        Cfg::SMEM_BYTES);
   if (e != cudaSuccess) return e;
@@ -465,12 +483,19 @@ cudaError_t launch_fwd_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
   return cudaGetLastError();
 }
 
-cudaError_t launch_fwd(int D, bool causal, const CUtensorMap& tq, const CUtensorMap& tk,
+cudaError_t launch_fwd(int D, bool causal, int mode, const CUtensorMap& tq, const CUtensorMap& tk,
                        const CUtensorMap& tv, const FwdParams& p, cudaStream_t stream) {
-  if (D == 128) return causal ? launch_fwd_t<128, true>(tq, tk, tv, p, stream)
-                              : launch_fwd_t<128, false>(tq, tk, tv, p, stream);
-  if (D == 64) return causal ? launch_fwd_t<64, true>(tq, tk, tv, p, stream)
-                             : launch_fwd_t<64, false>(tq, tk, tv, p, stream);
+#define PASA_LAUNCH(DD, CC, MM) \
+  if (D == DD && causal == CC && mode == MM) return launch_fwd_t<DD, CC, MM>(tq, tk, tv, p, stream);
+  PASA_LAUNCH(128, false, kModePasa)
+  PASA_LAUNCH(128, true, kModePasa)
+  PASA_LAUNCH(64, false, kModePasa)
+  PASA_LAUNCH(64, true, kModePasa)
+  PASA_LAUNCH(128, false, kModeFa16)
+  PASA_LAUNCH(128, true, kModeFa16)
+  PASA_LAUNCH(64, false, kModeFa16)
+  PASA_LAUNCH(64, true, kModeFa16)
+#undef PASA_LAUNCH
   return cudaErrorInvalidValue;
 }
 

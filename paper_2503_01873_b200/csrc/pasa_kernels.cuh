@@ -20,13 +20,18 @@ struct KprepParams {
   float lscale;        // 1 reproduces the reference; log2(e) for the fused kernel
 };
 
-// Fused PASA forward.  All scores live in the log2 domain (K' carries log2 e).
+// Fused forward.  PASA mode: scores live in the log2 domain (K' carries log2 e).
+// FA16 mode (beta == 0, pasa.cpp:212-221 -> attention.cpp:92-180): raw K, the
+// 1/alpha scale is applied after the FP16 store, FP16 running max, no
+// pseudo-average shift and no O inflation -- the naive FP16 FlashAttention.
+enum FwdMode : int { kModePasa = 0, kModeFa16 = 1 };
 struct FwdParams {
   int B, Hq, Hkv, S1, S2;
   int nq, nkv, group;     // S1/128, S2/128, Hq/Hkv
   int tiles_per_kv;       // group * nq
   float inva;             // beta / (1 - beta)       (pasa.cpp:85)
-  const float* vmax;      // per (b, kv head), from the pre-pass
+  float qk_scale;         // FA16 mode only: log2(e) / alpha applied after the FP16 store
+  const float* vmax;      // per (b, kv head), from the pre-pass (PASA mode)
   uint16_t* out;          // (B, Hq, S1, D) fp16
   long long* trace;       // PASA_TRACE builds only: clock64 timeline (see pasa_fwd.cu)
 };

@@ -273,3 +273,57 @@ def test_sharded_bit_identical(dev, orc, world):
             out[b:b + 1, 2 * h:2 * h + 2] = o
     torch.cuda.synchronize()
     assert torch.equal(out, full)
+
+
+# ----------------------------------------------------------------- FA16 mode (beta = 0)
+
+@pytest.mark.parametrize("case", [("hybrid", 0.0, 10.0, 1, 1, 2, 2, 512, 128, False),
+                                  ("hybrid", 0.0, 10.0, 4, 1, 7, 1, 640, 128, True),
+                                  ("hybrid", 3.0, 5.0, 2, 2, 2, 2, 384, 64, False)],
+                         ids=["d128", "gqa7_causal", "d64"])
+def test_fa16_vs_model(dev, orc, case):
+    from paper_2503_01873_b200 import flash_fp16_fwd
+    kind, x0, am, seed, B, Hq, Hkv, S, D, causal = case
+    q, k, v = orc.generate(kind, x0, am, seed, B, Hq, S, D, Hkv=Hkv)
+    qt, kt, vt = (torch.from_numpy(x).half().to(dev) for x in (q, k, v))
+    o = flash_fp16_fwd(qt, kt, vt, causal=causal)
+    torch.cuda.synchronize()
+    pb = Problem(q, k, v, causal=causal)
+    model, gold = orc.model_fa16(pb), orc.golden(pb)
+    on = o.double().cpu().numpy()
+    r_model = orc.rmse(model, gold)
+    assert orc.rmse(on, gold) <= 1.25 * r_model + 2e-4
+    assert orc.rmse(on, model) <= 0.75 * r_model + 2e-4
+
+
+@pytest.mark.parametrize("cell", [APPENDIX_E[0], APPENDIX_E[3], APPENDIX_E[4]],
+                         ids=["uniform_30_0.5", "hybrid_30_10", "hybrid_20_50"])
+def test_fa16_overflows_where_reference_fa_does(dev, orc, cell):
+    """Same hardware, same pipeline: beta = 0 (naive FP16 FA) overflows exactly where
+    the reference's FA_PARTIAL_FP16 does; PASA (beta*) does not."""
+    from paper_2503_01873_b200 import pasa_attention_fwd
+    kind, x0, am = cell
+    q, k, v = orc.generate(kind, x0, am, 0, 1, 4, 1280, 128)
+    pb = Problem(q, k, v)
+    o_fa, _ = run_fwd(dev, q, k, v, beta=0.0)       # pasa_attention with beta = 0 routes to FA16
+    o_pasa, _ = run_fwd(dev, q, k, v)
+    nan_fa = orc.nan_pct(o_fa.double().cpu().numpy())
+    nan_ref = orc.nan_pct(orc.flash_ref(pb))
+    assert nan_fa == pytest.approx(nan_ref, abs=1.0), (nan_fa, nan_ref)
+    assert orc.nan_pct(o_pasa.double().cpu().numpy()) == 0.0
+
+
+def test_fwd_long_n_sampled_rows(dev, orc):
+    """Tier 1 at N = 32768: the last query block of two heads against all keys
+    (the reference is exact per block row)."""
+    S = 32768
+    q, k, v = orc.generate("hybrid", 0.0, 10.0, 3, 1, 2, S, 128)
+    qs = np.ascontiguousarray(q[:, :, S - 128:])
+    pb = Problem(qs, k, v)
+    o, _ = run_fwd(dev, qs, k, v)
+    on = o.double().cpu().numpy()
+    gold, refo = orc.golden(pb), orc.pasa_ref(pb)
+    r_ref = orc.rmse(refo, gold)
+    assert orc.nan_pct(on) == 0.0
+    assert orc.rmse(on, gold) <= 1.25 * r_ref + 1e-3
+    assert orc.rmse(on, refo) <= 2.0 * r_ref + 1e-3
