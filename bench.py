@@ -324,6 +324,27 @@ def run_b200(args):
         del _
     sweep[str(SEQ)] = {"tflops": value, "fwd_kernel_tflops": achieved}
 
+    # ---------------- the naive FP16 FA (beta = 0) on the same pipeline and inputs
+    fa_ms = []
+    o_fa = torch.empty_like(o)
+    desc0 = _lib.Desc(1, HQ, HKV, SEQ, SEQ, D, 128, 128, 1, 0, 0.0, math.sqrt(D))
+    for i in range(args.warmup + max(3, args.steps // 3)):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _lib.check(L.pasa_b200_flash_fp16_fwd(C.byref(desc0), q.data_ptr(), k.data_ptr(),
+                                              v.data_ptr(), o_fa.data_ptr(), sh))
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if i >= args.warmup:
+            fa_ms.append(e0.elapsed_time(e1))
+    fa_tflops = flops_rank / (max_over_ranks(statistics.mean(fa_ms)) / 1e3) / 1e12
+    fa16 = {"fwd_kernel_tflops": fa_tflops, "pasa_over_fa16_time": fa_tflops / achieved,
+            "nonfinite_outputs": int((~torch.isfinite(o_fa)).sum().item()),
+            "note": "beta = 0: scale after the FP16 score store (attention.cpp:134-136); "
+                    "the Qwen-like bias overflows FP16 there, PASA has 0 non-finite outputs"}
+    del o_fa
+
     # ---------------- e2e through the public host entry point (pinned buffers)
     qh = q.cpu().pin_memory()
     kh = k.cpu().pin_memory()
@@ -390,6 +411,7 @@ def run_b200(args):
         "gpu_launches": 2 * args.steps,
         "clocks": clocks,
         "rmse_vs_fp32": rmse_fp32, "nonfinite_outputs": nonfinite,
+        "fa16_baseline": fa16,
         "sweep": sweep,
     }
     if rank == 0:
