@@ -39,6 +39,10 @@ using namespace sm100;
 constexpr bool kPingPong = true;
 
 constexpr int kTraceCtas = 4, kTraceIters = 32, kTraceEvents = 8, kTraceRoles = 3;
+// ... followed by a per-block row-state dump (CTA (0,0), tile 0, row kTraceRow,
+// half 0): kStateIters x 8 floats {mloc, ssum, fnew, mnew, cj, ep, lsum, l_run}.
+constexpr int kTraceRow = 2, kStateIters = 512;
+constexpr int kTraceStateOffset = kTraceCtas * kTraceRoles * kTraceIters * kTraceEvents;
 #ifdef PASA_TRACE
 #define PASA_TR(role, it, ev)                                                                  \
   do {                                                                                        \
@@ -46,7 +50,16 @@ constexpr int kTraceCtas = 4, kTraceIters = 32, kTraceEvents = 8, kTraceRoles = 
       p.trace[((blockIdx.y * kTraceRoles + (role)) * kTraceIters + (it)) * kTraceEvents + (ev)] = \
           clock64();                                                                          \
   } while (0)
+#define PASA_STATE(j, k, val)                                                                \
+  do {                                                                                      \
+    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && t == 0 && h == 0 && row == kTraceRow && \
+        (j) < kStateIters)                                                                  \
+      reinterpret_cast<float*>(p.trace + kTraceStateOffset)[(j) * 8 + (k)] = (val);          \
+  } while (0)
 #else
+#define PASA_STATE(j, k, val) \
+  do {                        \
+  } while (0)
 #define PASA_TR(role, it, ev) \
   do {                        \
   } while (0)
@@ -407,6 +420,13 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
                                 : row_exp_sum<false, NP, kFa>(s, row, NP * h, cj2, scale2);
         if (pingpong && ((t == 0 && j < nmin) || (t == 1 && j + 1 < nmin)))
           named_bar_arrive(2 - t, 512);
+        PASA_STATE(j, 0, mloc);
+        PASA_STATE(j, 1, MODE == kModePasa ? (h == 0 ? __fadd_rn(sh, other.y) : 0.f) : 0.f);
+        PASA_STATE(j, 2, fnew);
+        PASA_STATE(j, 3, mnew);
+        PASA_STATE(j, 4, __half2float(__low2half(u32_as_h2(cj2))));
+        PASA_STATE(j, 5, ep);
+        PASA_STATE(j, 6, lsum);
         if (tr) PASA_TR(t, j, 7);
         // P packed two per column: this half's 32 pairs -> columns [32h, 32h + 32)
         tmem_st_16cols_b32(t_s + NP * h, s);
@@ -417,6 +437,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         if (lane == 0) mbar_arrive(&p_full[t]);
         if (tr) PASA_TR(t, j, 4);
         l_run = (jc == 1) ? lsum : __fadd_rn(__fmul_rn(ep, l_run), lsum);
+        PASA_STATE(j, 7, l_run);
         m_run = mnew;
         fbar = fnew;
         rcp_j = __frcp_rn(static_cast<float>(jc + 1));
