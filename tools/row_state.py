@@ -42,7 +42,7 @@ for j in range(S // 128):
     mloc = np.float32(Sp.max())
     ch = [2 * ((c // 2) % 4) + (c % 2) for c in range(128)]
     sacc = np.zeros((2, 8), np.float32)
-    for c in range(128): sacc[c >= 64, ch[c]] += np.float32(Sp[c])
+    for c in range(128): sacc[int(c >= 64), ch[c]] += np.float32(Sp[c])
     sh_ = [((sacc[h, 0] + sacc[h, 1]) + (sacc[h, 2] + sacc[h, 3])) + ((sacc[h, 4] + sacc[h, 5]) + (sacc[h, 6] + sacc[h, 7])) for h in range(2)]
     ssum = np.float32(sh_[0] + sh_[1]); sbar = np.float32(ssum * np.float32(1 / 128))
     jc = j + 1
@@ -54,7 +54,7 @@ for j in range(S // 128):
     ep = 0.0 if jc == 1 else f16(2.0 ** float(np.float32(mprev - mnew)))
     P = np.array([f16(2.0 ** f16(x - cj)) for x in Sp])
     lacc = np.zeros((2, 8), np.float32)
-    for c in range(128): lacc[c >= 64, ch[c]] += np.float32(P[c])
+    for c in range(128): lacc[int(c >= 64), ch[c]] += np.float32(P[c])
     lsum0 = ((lacc[0, 0] + lacc[0, 1]) + (lacc[0, 2] + lacc[0, 3])) + ((lacc[0, 4] + lacc[0, 5]) + (lacc[0, 6] + lacc[0, 7]))
     l = lsum0 if jc == 1 else np.float32(np.float32(np.float32(ep) * l) + lsum0)
     k_ = st[j]
