@@ -253,20 +253,21 @@ def run_b200(args):
         desc = _lib.Desc(1, HQ, HKV, S, S, D, 128, 128, 1, 0, BETA, math.sqrt(D))
         _lib.check(L.pasa_b200_check(C.byref(desc)))
         kp = torch.empty_like(k)
+        vp = torch.empty_like(v)
         vmax = torch.zeros(HKV, dtype=torch.float32, device=dev)
         o = torch.empty_like(q)
-        return q, k, v, kp, vmax, o, desc
+        return q, k, v, kp, vp, vmax, o, desc
 
     def launch(bufs, evs=None):
-        q, k, v, kp, vmax, o, desc = bufs
+        q, k, v, kp, vp, vmax, o, desc = bufs
         if evs:
             evs[0].record(stream)
-        _lib.check(L.pasa_b200_preprocess_keys(C.byref(desc), k.data_ptr(), v.data_ptr(),
-                                               kp.data_ptr(), vmax.data_ptr(), LOG2E, sh))
+        _lib.check(L.pasa_b200_preprocess(C.byref(desc), k.data_ptr(), v.data_ptr(), kp.data_ptr(),
+                                          vp.data_ptr(), vmax.data_ptr(), sh))
         if evs:
             evs[1].record(stream)
         _lib.check(L.pasa_b200_attention_fwd_prepped(C.byref(desc), q.data_ptr(), kp.data_ptr(),
-                                                     v.data_ptr(), vmax.data_ptr(), o.data_ptr(), sh))
+                                                     vp.data_ptr(), vmax.data_ptr(), o.data_ptr(), sh))
         if evs:
             evs[2].record(stream)
 
@@ -298,7 +299,7 @@ def run_b200(args):
     peak_burst, peak_sust, peak_kind = peaks()
 
     # ---------------- numerics on the measured output: RMSE vs FP32, non-finite count
-    q, k, v, kp, vmax, o, desc = bufs
+    q, k, v, kp, vp, vmax, o, desc = bufs
     nonfinite = int((~torch.isfinite(o)).sum().item())
     rows = 256
     r0 = SEQ - rows
@@ -408,7 +409,7 @@ def run_b200(args):
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": bytes_in,
                 "d2h_bytes_per_step": bytes_out,
                 "api": "pasa_b200_attention_host (C-ABI, pinned host buffers)"},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": 3 * args.steps,  # key pre-pass, V scale, fused forward
         "clocks": clocks,
         "rmse_vs_fp32": rmse_fp32, "nonfinite_outputs": nonfinite,
         "fa16_baseline": fa16,

@@ -82,8 +82,8 @@ PASA_B200_API int pasa_b200_shift_entries(int32_t s2, double beta, double alpha,
  * pasa_attention (pasa.cpp:200-211); 0 if the fused path accepts it. */
 PASA_B200_API int pasa_b200_check(const pasa_b200_desc* desc);
 
-/* Bytes of device workspace pasa_b200_attention_fwd needs (K' for every KV
- * head and block, plus per-head statistics). */
+/* Bytes of device workspace pasa_b200_attention_fwd needs (K' and the
+ * scaled V' for every KV head and block, plus per-head statistics). */
 PASA_B200_API size_t pasa_b200_workspace_size(const pasa_b200_desc* desc);
 
 /* Key pre-pass K'_j = K_j^T M for every (b, kv head, j) (pasa.cpp:53-56, the
@@ -112,11 +112,19 @@ PASA_B200_API int pasa_b200_attention_fwd(const pasa_b200_desc* desc, const void
                             const void* v, void* o, void* workspace, size_t workspace_bytes,
                             pasa_b200_diag* diag, void* stream);
 
-/* The fused forward on keys already pre-processed by pasa_b200_preprocess_keys
- * with lscale = log2(e) (kp in the K-major layout above, vmax = max|V| per
- * (b, kv head)).  Lets a caller keep K' resident and reuse it across calls. */
+/* The full pre-pass of the fused kernel, device pointers, stream-ordered:
+ * kp = K'^T blocks with lscale = log2(e) (as pasa_b200_preprocess_keys),
+ * vmax = max|V| per (b, kv head), and vp = V * 2^-c0 per head with
+ * c0 = max(0, ceil(log2(S2 * vmax / 2^14))) -- the exact power-of-two scale
+ * that keeps the FP16 O accumulator bounded. */
+PASA_B200_API int pasa_b200_preprocess(const pasa_b200_desc* desc, const void* k, const void* v,
+                                       void* kp, void* vp, float* vmax, void* stream);
+
+/* The fused forward on pre-processed keys and values (kp, vp, vmax from
+ * pasa_b200_preprocess).  Lets a caller keep K'/V' resident and reuse them
+ * across calls (same keys, many query batches). */
 PASA_B200_API int pasa_b200_attention_fwd_prepped(const pasa_b200_desc* desc, const void* q,
-                                                  const void* kp, const void* v, const float* vmax,
+                                                  const void* kp, const void* vp, const float* vmax,
                                                   void* o, void* stream);
 
 /* The naive FP16 FlashAttention on the same pipeline: flash_attention with

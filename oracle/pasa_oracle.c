@@ -532,9 +532,10 @@ ORC_API int orc_pasa_ref(const orc_shape* sh, const double* q, const double* k,
 /*  - row statistics (sum of S', mean, F, corrections, running max, l) are   */
 /*    FP32; the S' and P row sums run as eight chains (kernel order),        */
 /*  - F_j = F_{j-1} + (Sbar - F_{j-1}) * fl32(1/j) (no (j-1)*F product),     */
-/*  - e_cur is folded into P: P = 2^(fl16(S' - c_j) ) with                   */
-/*    c_j = fl16(m_j - dm_cur + c0), c0 >= 0 a per-head inflation that      */
-/*    bounds O and l below 65504 (see kernel), so O <- fl16(e_p * O + T),    */
+/*  - e_cur is folded into P: P = 2^(fl16(S' - c_j)) with c_j = fl16(m_j -   */
+/*    dm_cur), so O <- fl16(e_p * O + T); V enters as V' = fl16(V 2^-c0) with */
+/*    c0 >= 0 the per-head bound exponent (O < 2^14) and the epilogue scales  */
+/*    by 2^c0,                                                               */
 /*  - causal: the block mean uses all s2 columns, masked entries get P = 0,  */
 /*    fully masked blocks are skipped and j counts consumed blocks.          */
 /* tc_mode: 0 = GEMMs accumulate sequentially in FP32 then round once to    */
@@ -564,13 +565,14 @@ typedef struct {
   double c0; /* inflation in L units; < 0 selects the kernel's automatic rule */
 } orc_model_params;
 
-/* The kernel's automatic inflation (pasa_fwd.cu, kInflate): with vmax the
- * largest |V| of the (b, kv-head) and S2 keys, c0 = max(0, log_L(S2 * vmax
- * / 16384)) rounded up to an integer, so l * vmax stays below 16384 * 2^0. */
+/* The kernel's O-bounding exponent (pasa_kernels.cuh: pasa_inflation): the
+ * smallest integer c0 >= 0 with S2 * vmax <= 2^14 * 2^c0, in FP32 exactly as
+ * the device computes it.  V is scaled by 2^-c0 before PV; the epilogue
+ * multiplies by 2^c0.  (lscale is accepted for API compatibility.) */
 ORC_API double orc_model_inflation(double vmax, size_t S2, double lscale) {
+  (void)lscale;
   const float need = (float)S2 * (float)vmax * (1.0f / 16384.0f);
   if (!(need > 1.0f)) return 0.0;
-  if (lscale == 1.0) return ceil(log((double)need)); /* natural domain */
   int e = ilogbf(need); /* floor(log2 need), exact */
   return (double)(ldexpf(1.0f, e) == need ? e : e + 1);
 }
@@ -596,14 +598,16 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
     const size_t h = ((size_t)x / nq) % sh->Hq;
     const size_t b = (size_t)x / (nq * sh->Hq);
     const size_t hk = h / grp;
-    /* inflation for this kv head */
+    /* O-bound exponent for this kv head and the scaled V' = fl16(V 2^-c0) */
+    const double* vh = row_ptr(v, sh->Hkv, sh->S2, d, b, hk, 0);
     double c0 = mp->c0;
     if (c0 < 0.0) {
       double vmax = 0.0;
-      const double* vh = row_ptr(v, sh->Hkv, sh->S2, d, b, hk, 0);
       for (size_t e = 0; e < sh->S2 * d; ++e) vmax = fmax(vmax, fabs(vh[e]));
       c0 = orc_model_inflation(vmax, sh->S2, L);
     }
+    double* vsc = malloc(sizeof(double) * sh->S2 * d);
+    for (size_t e = 0; e < sh->S2 * d; ++e) vsc[e] = fl16(vh[e] * ldexp(1.0, -(int)c0));
     float* m = calloc(s1, sizeof(float));
     float* l = calloc(2 * s1, sizeof(float)); /* per half-row partial l */
     float* fbar = calloc(s1, sizeof(float));
@@ -615,7 +619,7 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
       if (sh->causal && j * s2 > row0 + s1 - 1) break; /* fully masked */
       ++jc;
       const double* kpj = kp + ((b * sh->Hkv + hk) * sh->S2 + j * s2) * d;
-      const double* vj = row_ptr(v, sh->Hkv, sh->S2, d, b, hk, j * s2);
+      const double* vj = vsc + j * s2 * d;
       for (size_t r = 0; r < s1; ++r) {
         const double* qr = row_ptr(q, sh->Hq, sh->S1, d, b, h, i * s1 + r);
         const size_t pos = row0 + r;
@@ -646,7 +650,7 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
         const float dmp = (jc == 1) ? 0.f : inva * (fbar[r] - fnew);
         const float cand = (float)mloc + dmc;
         float mnew = (jc == 1) ? cand : fmaxf(m[r] + dmp, cand);
-        const float cjf = (mnew - dmc) + (float)c0;
+        const float cjf = mnew - dmc;
         const double cj = fl16((double)cjf);
         double ep = 0.0;
         if (jc > 1) {
@@ -677,10 +681,10 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
     }
     for (size_t r = 0; r < s1; ++r) {
       double* dst = o + ((b * sh->Hq + h) * sh->S1 + i * s1 + r) * d;
-      const float invl = 1.0f / (l[2 * r] + l[2 * r + 1]);
+      const float invl = (1.0f / (l[2 * r] + l[2 * r + 1])) * ldexpf(1.0f, (int)c0);
       for (size_t n = 0; n < d; ++n) dst[n] = fl16((float)oacc[r * d + n] * invl);
     }
-    free(m); free(l); free(fbar); free(oacc); free(S);
+    free(m); free(l); free(fbar); free(oacc); free(S); free(vsc);
   }
   free(kp);
   return 0;

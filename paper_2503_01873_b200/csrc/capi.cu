@@ -19,6 +19,7 @@
 
 namespace pasa_b200 {
 cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stream);
+cudaError_t launch_vscale(const VscaleParams& p, cudaStream_t stream);
 cudaError_t launch_fwd(int D, bool causal, int mode, const CUtensorMap& tq, const CUtensorMap& tk,
                        const CUtensorMap& tv, const FwdParams& p, cudaStream_t stream);
 }  // namespace pasa_b200
@@ -145,7 +146,9 @@ int pasa_b200_check(const pasa_b200_desc* desc) {
 
 size_t pasa_b200_workspace_size(const pasa_b200_desc* d) {
   if (!d || d->batch <= 0 || d->heads_kv <= 0 || d->seq_kv <= 0 || d->head_dim <= 0) return 0;
-  return align_up(kp_bytes(d), 256) + align_up(static_cast<size_t>(d->batch) * d->heads_kv * 4, 256);
+  // K' | V' | max|V| per head
+  return 2 * align_up(kp_bytes(d), 256) +
+         align_up(static_cast<size_t>(d->batch) * d->heads_kv * 4, 256);
 }
 
 static int preprocess_impl(const pasa_b200_desc* d, const void* k, const void* v, void* kp, float* vmax,
@@ -211,6 +214,29 @@ int pasa_b200_preprocess_keys_host(const pasa_b200_desc* d, const uint16_t* k, u
   return rc;
 }
 
+int pasa_b200_preprocess(const pasa_b200_desc* d, const void* k, const void* v, void* kp,
+                         void* vp, float* vmax, void* stream) {
+  g_last_error.clear();
+  if (!d || !k || !v || !kp || !vp || !vmax) return fail(PASA_B200_EINVAL, "preprocess: NULL argument");
+  if (!(d->beta > 0.0 && d->beta < 1.0) || !(d->alpha > 0.0))
+    return fail(PASA_B200_EINVAL, "preprocess: beta must lie in (0, 1), alpha > 0");
+  __half dg, of;
+  shift_scalars(d->s2, d->beta, d->alpha, &dg, &of);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = preprocess_impl(d, k, v, kp, vmax, static_cast<float>(kLog2e), dg, of, st);
+  if (rc) return rc;
+  VscaleParams vs{};
+  vs.v = static_cast<const uint16_t*>(v);
+  vs.vp = static_cast<uint16_t*>(vp);
+  vs.vmax = vmax;
+  vs.per_head = static_cast<long long>(d->seq_kv) * d->head_dim;
+  vs.total = vs.per_head * d->batch * d->heads_kv;
+  vs.S2 = d->seq_kv;
+  cudaError_t e = launch_vscale(vs, st);
+  if (e != cudaSuccess) return cuda_fail(e, "pasa_vscale launch");
+  return PASA_B200_OK;
+}
+
 static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, const void* keys,
                           const void* v, const float* vmax, void* o, void* stream) {
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(keys) |
@@ -243,15 +269,15 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
 }
 
 int pasa_b200_attention_fwd_prepped(const pasa_b200_desc* d, const void* q, const void* kp,
-                                    const void* v, const float* vmax, void* o, void* stream) {
+                                    const void* vp, const float* vmax, void* o, void* stream) {
   g_last_error.clear();
   int rc = check_desc(d);
   if (rc) return rc;
-  if (!q || !kp || !v || !o || !vmax)
+  if (!q || !kp || !vp || !o || !vmax)
     return fail(PASA_B200_EINVAL, "attention_fwd: NULL tensor");
   if (d->beta == 0.0)
     return fail(PASA_B200_EINVAL, "attention_fwd_prepped: beta == 0 has no key pre-pass");
-  return launch_forward(d, kModePasa, q, kp, v, vmax, o, stream);
+  return launch_forward(d, kModePasa, q, kp, vp, vmax, o, stream);
 }
 
 int pasa_b200_flash_fp16_fwd(const pasa_b200_desc* d, const void* q, const void* k, const void* v,
@@ -278,10 +304,11 @@ int pasa_b200_attention_fwd(const pasa_b200_desc* d, const void* q, const void* 
   if (d->beta == 0.0) return launch_forward(d, kModeFa16, q, k, v, nullptr, o, stream);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   void* kp = ws;
-  float* vmax = reinterpret_cast<float*>(ws + align_up(kp_bytes(d), 256));
-  rc = pasa_b200_preprocess_keys(d, k, v, kp, vmax, static_cast<float>(kLog2e), stream);
+  void* vp = ws + align_up(kp_bytes(d), 256);
+  float* vmax = reinterpret_cast<float*>(ws + 2 * align_up(kp_bytes(d), 256));
+  rc = pasa_b200_preprocess(d, k, v, kp, vp, vmax, stream);
   if (rc) return rc;
-  return pasa_b200_attention_fwd_prepped(d, q, kp, v, vmax, o, stream);
+  return pasa_b200_attention_fwd_prepped(d, q, kp, vp, vmax, o, stream);
 }
 
 int pasa_b200_attention_host(const pasa_b200_desc* d, const uint16_t* q, const uint16_t* k,

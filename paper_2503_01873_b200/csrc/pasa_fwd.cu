@@ -18,7 +18,7 @@
 //   tcgen05.st P back over the S' columns (packed 2 x f16 per column)
 //   T_t   = P V_j           tcgen05.mma kind::f16, TS (P from TMEM), F16 acc
 //   softmax WG: O <- e_prev * O + T in half2 registers (HFMA2)
-// Epilogue ("global recovering"): O / l, fp16 store.
+// Epilogue ("global recovering"): O * 2^c0 / l, fp16 store (V' = V 2^-c0).
 //
 // Numerics are documented in DESIGN.md section 4 and restated on the CPU in
 // oracle/pasa_oracle.c:orc_model_pasa (the tight oracle for this kernel).
@@ -351,14 +351,9 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     };
     const uint32_t xbar = 3 + t * 4 + quad;  // named barrier of this row quadrant's two warps
     if (ti.nblk > 0) {
-      // Inflation c0 (log2 units) keeping l * max|V| below 2^14.
-      const float vm = MODE == kModePasa ? p.vmax[b * p.Hkv + hkv] : 0.f;
-      const float need = __fmul_rn(__fmul_rn(static_cast<float>(p.S2), vm), 1.0f / 16384.0f);
-      float c0 = 0.f;
-      if (MODE == kModePasa && need > 1.0f) {
-        const int e = ilogbf(need);
-        c0 = static_cast<float>(ldexpf(1.0f, e) == need ? e : e + 1);
-      }
+      // O-bounding exponent: V arrives pre-scaled by 2^-c0; the
+      // epilogue multiplies by 2^c0.
+      const int c0 = MODE == kModePasa ? pasa_inflation(p.S2, p.vmax[b * p.Hkv + hkv]) : 0;
       constexpr int NP = 32;  // pairs per thread
       uint32_t o[D / 4];
       uint32_t s[NP];
@@ -399,7 +394,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
           const float cand = __fadd_rn(mloc, dmc);
           const float mprev = __fadd_rn(m_run, dmp);
           mnew = (jc == 1) ? cand : fmaxf(mprev, cand);
-          const __half cj = __float2half_rn(__fadd_rn(__fsub_rn(mnew, dmc), c0));
+          const __half cj = __float2half_rn(__fsub_rn(mnew, dmc));
           ep = (jc == 1) ? 0.f : __half2float(__float2half_rn(ex2_f32(__fsub_rn(mprev, mnew))));
           cj2 = h2_as_u32(__half2half2(cj));
         } else {
@@ -467,7 +462,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       named_bar_sync(xbar, 64);
       const float lo_other = xslot(ti.nblk & 1, 1 - h)->x;
       const float l_tot = h == 0 ? __fadd_rn(l_run, lo_other) : __fadd_rn(lo_other, l_run);
-      const float inv_l = __frcp_rn(l_tot);
+      const float inv_l = __fmul_rn(__frcp_rn(l_tot), ldexpf(1.0f, c0));  // exact 2^c0
       uint16_t* dst = p.out + ((static_cast<size_t>(b) * p.Hq + ti.hq) * p.S1 +
                                static_cast<size_t>(ti.i) * kTile + row) * D + (D / 2) * h;
 #pragma unroll

@@ -20,6 +20,27 @@ struct KprepParams {
   float lscale;        // 1 reproduces the reference; log2(e) for the fused kernel
 };
 
+// O-bounding exponent c0 >= 0: the smallest integer with
+// S2 * max|V| <= 2^14 * 2^c0, computed identically on host and device.  The
+// pre-pass scales V by the exact power of two 2^-c0, so T = P V and the FP16 O
+// stay below 2^14 while P keeps its full (0, 1] range (no subnormal P).
+__host__ __device__ inline int pasa_inflation(int S2, float vmax) {
+  const float need = static_cast<float>(S2) * vmax * (1.0f / 16384.0f);
+  if (!(need > 1.0f)) return 0;
+  const int e = ilogbf(need);  // floor(log2 need), exact
+  return ldexpf(1.0f, e) == need ? e : e + 1;
+}
+
+// V' = V * 2^-c0 per (b, kv head), written by the pre-pass for the fused kernel.
+struct VscaleParams {
+  const uint16_t* v;   // (B, Hkv, S2, D) fp16
+  uint16_t* vp;        // (B, Hkv, S2, D) fp16
+  const float* vmax;   // (B * Hkv)
+  long long per_head;  // S2 * D
+  long long total;     // B * Hkv * S2 * D
+  int S2;
+};
+
 // Fused forward.  PASA mode: scores live in the log2 domain (K' carries log2 e).
 // FA16 mode (beta == 0, pasa.cpp:212-221 -> attention.cpp:92-180): raw K, the
 // 1/alpha scale is applied after the FP16 store, FP16 running max, no
@@ -31,7 +52,7 @@ struct FwdParams {
   int tiles_per_kv;       // group * nq
   float inva;             // beta / (1 - beta)       (pasa.cpp:85)
   float qk_scale;         // FA16 mode only: log2(e) / alpha applied after the FP16 store
-  const float* vmax;      // per (b, kv head), from the pre-pass (PASA mode)
+  const float* vmax;      // per (b, kv head), from the pre-pass (PASA mode: V is pre-scaled)
   uint16_t* out;          // (B, Hq, S1, D) fp16
   long long* trace;       // PASA_TRACE builds only: clock64 timeline (see pasa_fwd.cu)
 };

@@ -113,6 +113,31 @@ __global__ void __launch_bounds__(D * 4) pasa_kprep_kernel(const KprepParams p) 
   }
 }
 
+// V' = V * 2^-c0 (exact power-of-two scaling; RNE only where V' is subnormal).
+__global__ void __launch_bounds__(256) pasa_vscale_kernel(const VscaleParams p) {
+  const long long n8 = p.total / 8;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n8;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int bh = static_cast<int>((i * 8) / p.per_head);
+    const int c0 = pasa_inflation(p.S2, p.vmax[bh]);
+    const __half2 sc = __half2half2(__float2half_rn(ldexpf(1.0f, -c0)));
+    uint4 w = reinterpret_cast<const uint4*>(p.v)[i];
+    __half2* h = reinterpret_cast<__half2*>(&w);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = __hmul2(h[k], sc);
+    reinterpret_cast<uint4*>(p.vp)[i] = w;
+  }
+}
+
+cudaError_t launch_vscale(const VscaleParams& p, cudaStream_t stream) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const long long n8 = p.total / 8;
+  const int blocks = static_cast<int>(n8 / 256 + 1 < 8LL * sms ? n8 / 256 + 1 : 8LL * sms);
+  pasa_vscale_kernel<<<blocks, 256, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stream) {
   dim3 grid(p.S2 / kTile, B * Hkv);
   if (p.D == 128) {

@@ -50,7 +50,7 @@ for j in range(S // 128):
     dmc = np.float32(inva * np.float32(sbar - fnew)); dmp = np.float32(0) if jc == 1 else np.float32(inva * np.float32(fbar - fnew))
     cand = np.float32(mloc + dmc); mprev = np.float32(m + dmp)
     mnew = cand if jc == 1 else max(mprev, cand)
-    cj = f16(np.float32(np.float32(mnew - dmc) + np.float32(c0)))
+    cj = f16(np.float32(mnew - dmc))
     ep = 0.0 if jc == 1 else f16(2.0 ** float(np.float32(mprev - mnew)))
     P = np.array([f16(2.0 ** f16(x - cj)) for x in Sp])
     lacc = np.zeros((2, 8), np.float32)

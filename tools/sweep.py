@@ -70,6 +70,7 @@ def run(L, name, kind, B, Hq, Hkv, S, d, causal, iters, dev):
     desc = _lib.Desc(B, Hq, Hkv, S, S, d, 128, 128, int(causal), 0, BETA, math.sqrt(d))
     _lib.check(L.pasa_b200_check(C.byref(desc)))
     kp = torch.empty_like(k)
+    vp = torch.empty_like(v)
     vmax = torch.zeros(B * Hkv, device=dev)
     o = torch.empty_like(q)
     st = torch.cuda.current_stream().cuda_stream
@@ -78,12 +79,12 @@ def run(L, name, kind, B, Hq, Hkv, S, d, causal, iters, dev):
     def launch(ev=None):
         if ev:
             ev[0].record()
-        _lib.check(L.pasa_b200_preprocess_keys(C.byref(desc), k.data_ptr(), v.data_ptr(),
-                                               kp.data_ptr(), vmax.data_ptr(), LOG2E, st))
+        _lib.check(L.pasa_b200_preprocess(C.byref(desc), k.data_ptr(), v.data_ptr(), kp.data_ptr(),
+                                          vp.data_ptr(), vmax.data_ptr(), st))
         if ev:
             ev[1].record()
         _lib.check(L.pasa_b200_attention_fwd_prepped(C.byref(desc), q.data_ptr(), kp.data_ptr(),
-                                                     v.data_ptr(), vmax.data_ptr(), o.data_ptr(), st))
+                                                     vp.data_ptr(), vmax.data_ptr(), o.data_ptr(), st))
         if ev:
             ev[2].record()
     for _ in range(3):
@@ -114,7 +115,7 @@ def run(L, name, kind, B, Hq, Hkv, S, d, causal, iters, dev):
            "rmse_vs_fp32_sampled": math.sqrt(err / nrm),
            "nonfinite": int((~torch.isfinite(o)).sum().item())}
     print(json.dumps(res), flush=True)
-    del q, k, v, kp, o, flush
+    del q, k, v, kp, vp, o, flush
     torch.cuda.empty_cache()
     return res
 
