@@ -198,11 +198,16 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
 
   const int warp = static_cast<int>(warp_id());
   const int lane = threadIdx.x & 31;
-  const int b = blockIdx.x / p.Hkv;
-  const int hkv = blockIdx.x % p.Hkv;
+  // Causal: heads vary fastest so the longest (LPT-first) units of every head
+  // start first.  Non-causal: units vary fastest so the CTAs in flight share
+  // one head's K'/V in L2 instead of streaming all heads at once.
+  const int head_id = CAUSAL ? blockIdx.x : blockIdx.y;
+  const int unit = CAUSAL ? blockIdx.y : blockIdx.x;
+  const int b = head_id / p.Hkv;
+  const int hkv = head_id % p.Hkv;
   TileInfo tl[NT];
 #pragma unroll
-  for (int t = 0; t < NT; ++t) tl[t] = tile_info(p, hkv, blockIdx.y * NT + t, CAUSAL);
+  for (int t = 0; t < NT; ++t) tl[t] = tile_info(p, hkv, unit * NT + t, CAUSAL);
   int nmax = 0;
 #pragma unroll
   for (int t = 0; t < NT; ++t) nmax = max(nmax, tl[t].nblk);
@@ -342,7 +347,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     const int h = (sw / 4) & 1;
     const int quad = warp % 4;  // TMEM lane quadrant this warp may access
     const int row = quad * 32 + lane;
-    const TileInfo ti = tile_info(p, hkv, blockIdx.y * NT + t, CAUSAL);
+    const TileInfo ti = tile_info(p, hkv, unit * NT + t, CAUSAL);
     const uint32_t t_s = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + t * Cfg::TMEM_TILE;
     const uint32_t t_t = t_s + 128;
     float2* xch = reinterpret_cast<float2*>(smem + Cfg::SMEM_XCH);
@@ -360,8 +365,8 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       float m_run = 0.f, l_run = 0.f, fbar = 0.f;
       float rcp_j = 1.0f;  // 1/(j+1), computed off the critical path
       // both tiles' block counts (identical in every thread of the CTA)
-      const int nmin = min(tile_info(p, hkv, blockIdx.y * NT, CAUSAL).nblk,
-                           tile_info(p, hkv, blockIdx.y * NT + 1, CAUSAL).nblk);
+      const int nmin = min(tile_info(p, hkv, unit * NT, CAUSAL).nblk,
+                           tile_info(p, hkv, unit * NT + 1, CAUSAL).nblk);
       const bool pingpong = kPingPong;
       for (int j = 0; j < ti.nblk; ++j) {
         const bool tr = h == 0 && quad == 0 && lane == 0;
@@ -494,7 +499,7 @@ cudaError_t launch_fwd_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
                                        Cfg::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int units = (p.tiles_per_kv + Cfg::NT - 1) / Cfg::NT;
-  dim3 grid(p.B * p.Hkv, units);
+  const dim3 grid = CAUSAL ? dim3(p.B * p.Hkv, units) : dim3(units, p.B * p.Hkv);
   kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(tq, tk, tv, p);
   return cudaGetLastError();
 }
