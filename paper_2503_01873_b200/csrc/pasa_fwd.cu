@@ -7,10 +7,9 @@
 //   warp 0      TMA producer: Q tiles once, then a K'/V ring (2 stages each)
 //   warp 1      MMA issuer (one elected lane) + TMEM owner (512 columns)
 //   warps 2-3   idle (warpgroup 0 gives its registers away via setmaxnreg)
-//   warps 4-19  softmax/correction: four threads per row (warps 4+4w..7+4w
-//               hold S' columns [32w, 32w+32) and D/4 output columns); all 16
-//               warps process tile 0 then tile 1, so each tile's softmax is
-//               short and overlaps the tensor core's work on the other tile
+//   warps 4-11  softmax/correction for tile 0: two threads per row (warps
+//               4-7 hold S' columns 0-63, warps 8-11 columns 64-127)
+//   warps 12-19 the same for tile 1
 //
 // Per KV block j and tile t (reference pasa.cpp:256-278, Algorithm 1):
 //   S'_t  = Q_t K'_j^T      tcgen05.mma kind::f16, SS, F16 accumulator in TMEM
@@ -36,6 +35,8 @@ using namespace sm100;
 // < kTraceCtas record clock64() at fixed points of the first kTraceIters
 // blocks -- per softmax warpgroup (warp quadrant 0, lane 0) and for the MMA
 // issuer -- into p.trace[cta][role][iter][event].
+// Alternate the two softmax warpgroups' exp passes (named barriers 1, 2).
+constexpr bool kPingPong = true;
 
 constexpr int kTraceCtas = 4, kTraceIters = 32, kTraceEvents = 8, kTraceRoles = 3;
 // ... followed by a per-block row-state dump (CTA (0,0), tile 0, row kTraceRow,
@@ -49,20 +50,13 @@ constexpr int kTraceStateOffset = kTraceCtas * kTraceRoles * kTraceIters * kTrac
       p.trace[((blockIdx.y * kTraceRoles + (role)) * kTraceIters + (it)) * kTraceEvents + (ev)] = \
           clock64();                                                                          \
   } while (0)
-#define PASA_TR_IF(cond, role, it, ev) \
-  do {                                 \
-    if (cond) PASA_TR(role, it, ev);   \
-  } while (0)
 #define PASA_STATE(j, k, val)                                                                \
   do {                                                                                      \
-    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && t == 0 && w == 0 && row == kTraceRow && \
+    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && t == 0 && h == 0 && row == kTraceRow && \
         (j) < kStateIters)                                                                  \
       reinterpret_cast<float*>(p.trace + kTraceStateOffset)[(j) * 8 + (k)] = (val);          \
   } while (0)
 #else
-#define PASA_TR_IF(cond, role, it, ev) \
-  do {                                 \
-  } while (0)
 #define PASA_STATE(j, k, val) \
   do {                        \
   } while (0)
@@ -84,11 +78,11 @@ struct FwdCfg {
   static constexpr int SMEM_V = SMEM_K + KS * TILE_BYTES;
   static constexpr int SMEM_BAR = SMEM_V + VS * TILE_BYTES;
   static constexpr int NUM_BARS = NT + 2 * KS + 2 * VS + 4 * NT;
-  static constexpr int SLICES = 4;  // threads per row: each owns 32 S' columns, D/4 outputs
+  static constexpr int HALVES = 2;  // threads per row: each owns 64 S' columns, D/2 outputs
   static constexpr int SMEM_XCH = SMEM_BAR + NUM_BARS * 8 + 16;  // row max/sum exchange
-  static constexpr int XCH_BYTES = 2 * NT * SLICES * kTile * 8;  // [j&1][t][slice][row] float2
+  static constexpr int XCH_BYTES = 2 * NT * HALVES * kTile * 8;  // [j&1][t][half][row] float2
   static constexpr int SMEM_BYTES = SMEM_XCH + XCH_BYTES + 1024;
-  static constexpr int THREADS = 128 + SLICES * 128;  // WG0: TMA, MMA, 2 idle; 4 softmax WGs
+  static constexpr int THREADS = 128 + NT * HALVES * 128;  // WG0: TMA, MMA, 2 idle; 4 softmax WGs
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t TMEM_TILE = 256;               // S/P at +0, T at +128
 };
@@ -222,9 +216,9 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     for (int t = 0; t < NT; ++t) {
       mbar_init(&q_full[t], 1);
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], 4 * Cfg::SLICES);
+      mbar_init(&p_full[t], 4 * Cfg::HALVES);
       mbar_init(&t_full[t], 1);
-      mbar_init(&t_empty[t], 4 * Cfg::SLICES);
+      mbar_init(&t_empty[t], 4 * Cfg::HALVES);
     }
     for (int s = 0; s < KS; ++s) {
       mbar_init(&k_full[s], 1);
@@ -344,165 +338,148 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
     // ------------------------------------------------------------ softmax WGs
-    // All 16 softmax warps work on one tile at a time, four threads per row:
-    // warps 4+4w..7+4w own S' columns [32w, 32w+32) and output columns
-    // [D/4 w, D/4 (w+1)) of both tiles.  The tiles alternate (softmax of tile 0,
-    // softmax of tile 1, O updates in between), so while one tile's softmax runs
-    // the tensor core computes the other tile's P V and next S'.  Row max and sum
-    // are combined through shared memory under a per-quadrant named barrier.
-    const int w = (warp - 4) / 4;  // column slice
-    const int quad = warp % 4;     // TMEM lane quadrant this warp may access
+    // Two threads per row: warps 4-7 / 8-11 hold columns 0-63 / 64-127 of
+    // tile 0's rows, warps 12-15 / 16-19 those of tile 1.  Row max and sum are
+    // exchanged through shared memory (named barrier per quadrant pair); each
+    // thread keeps its own partial l and D/2 output columns.
+    const int sw = warp - 4;
+    const int t = sw / 8;
+    const int h = (sw / 4) & 1;
+    const int quad = warp % 4;  // TMEM lane quadrant this warp may access
     const int row = quad * 32 + lane;
-    const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+    const TileInfo ti = tile_info(p, hkv, unit * NT + t, CAUSAL);
+    const uint32_t t_s = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + t * Cfg::TMEM_TILE;
+    const uint32_t t_t = t_s + 128;
     float2* xch = reinterpret_cast<float2*>(smem + Cfg::SMEM_XCH);
-    auto xslot = [&](int parity, int t, int slice) -> float2* {
-      return xch + ((parity * NT + t) * Cfg::SLICES + slice) * kTile + row;
+    auto xslot = [&](int parity, int half) -> float2* {
+      return xch + ((parity * NT + t) * Cfg::HALVES + half) * kTile + row;
     };
-    const uint32_t xbar = 1 + quad;  // named barrier of this quadrant's four warps
-    constexpr int NP = 16;           // pairs per thread
-    constexpr int NO = D / 8;        // output half2 registers per thread
-    const TileInfo ti0 = tile_info(p, hkv, unit * NT, CAUSAL);
-    const TileInfo ti1 = tile_info(p, hkv, unit * NT + 1, CAUSAL);
-    const int nblk[2] = {ti0.nblk, ti1.nblk};
-    // O-bounding exponent: V arrives pre-scaled by 2^-c0; the
-    // epilogue multiplies by 2^c0.
-    const int c0 = MODE == kModePasa ? pasa_inflation(p.S2, p.vmax[b * p.Hkv + hkv]) : 0;
-    uint32_t s[NP];
-    uint32_t o[NT][NO];
-    float m_run[NT] = {0.f, 0.f}, l_run[NT] = {0.f, 0.f}, fbar[NT] = {0.f, 0.f};
-    float ep_last[NT] = {0.f, 0.f};
-    float rcp_j = 1.0f;  // 1/(j+1), computed off the critical path
-
-    // ---- softmax of tile t, block j: S' -> P in TMEM, running statistics
-    auto softmax = [&](const int t, const int j) {
-      const uint32_t t_s = lane_base + t * Cfg::TMEM_TILE;
-      const bool tr = t == 0 && w == 0 && quad == 0 && lane == 0;
-      (void)tr;
-      PASA_TR_IF(tr, t, j, 0);
-      mbar_wait(&s_full[t], j & 1);
-      PASA_TR_IF(tr, t, j, 1);
-      tc_fence_after();
-      tmem_ld_32cols_pack16(t_s + 32 * w, s);
-      tmem_wait_ld();
-      PASA_TR_IF(tr, t, j, 2);
-      const bool diag = CAUSAL && (j == nblk[t] - 1);
-      constexpr bool kSum = MODE == kModePasa;
-      float mh, sh = 0.f;
-      if (diag) row_max_sum<true, NP, kSum>(s, row, NP * w, mh, sh);
-      else row_max_sum<false, NP, kSum>(s, row, NP * w, mh, sh);
-      *xslot(j & 1, t, w) = make_float2(mh, sh);
-      named_bar_sync(xbar, 128);
-      const float2 x0 = *xslot(j & 1, t, 0), x1 = *xslot(j & 1, t, 1);
-      const float2 x2 = *xslot(j & 1, t, 2), x3 = *xslot(j & 1, t, 3);
-      const float mloc = fmaxf(fmaxf(x0.x, x1.x), fmaxf(x2.x, x3.x));
-      const int jc = j + 1;
-      float mnew, ep, fnew = 0.f;
-      uint32_t cj2, scale2 = 0;
-      if (MODE == kModePasa) {
-        const float ssum = __fadd_rn(__fadd_rn(x0.y, x1.y), __fadd_rn(x2.y, x3.y));
-        const float sbar = __fmul_rn(ssum, 1.0f / 128.0f);
-        fnew = (jc == 1) ? sbar : __fadd_rn(fbar[t], __fmul_rn(__fsub_rn(sbar, fbar[t]), rcp_j));
-        const float dmc = __fmul_rn(p.inva, __fsub_rn(sbar, fnew));
-        const float dmp = (jc == 1) ? 0.f : __fmul_rn(p.inva, __fsub_rn(fbar[t], fnew));
-        const float cand = __fadd_rn(mloc, dmc);
-        const float mprev = __fadd_rn(m_run[t], dmp);
-        mnew = (jc == 1) ? cand : fmaxf(mprev, cand);
-        const __half cj = __float2half_rn(__fsub_rn(mnew, dmc));
-        ep = (jc == 1) ? 0.f : __half2float(__float2half_rn(ex2_f32(__fsub_rn(mprev, mnew))));
-        cj2 = h2_as_u32(__half2half2(cj));
-        PASA_STATE(j, 1, ssum);
-      } else {
-        // naive FP16 FA (attention.cpp:92-180): running max of the FP16-stored
-        // scores, P = 2^(S*s - m*s) with s = log2(e)/alpha applied after the store
-        mnew = (jc == 1) ? mloc : fmaxf(m_run[t], mloc);
-        ep = (jc == 1) ? 0.f
-                       : __half2float(__float2half_rn(ex2_f32(__fmul_rn(__fsub_rn(m_run[t], mnew), p.qk_scale))));
-        cj2 = h2_as_u32(__half2half2(__hneg(__float2half_rn(__fmul_rn(mnew, p.qk_scale)))));
-        scale2 = h2_as_u32(__half2half2(__float2half_rn(p.qk_scale)));
+    const uint32_t xbar = 3 + t * 4 + quad;  // named barrier of this row quadrant's two warps
+    if (ti.nblk > 0) {
+      // O-bounding exponent: V arrives pre-scaled by 2^-c0; the
+      // epilogue multiplies by 2^c0.
+      const int c0 = MODE == kModePasa ? pasa_inflation(p.S2, p.vmax[b * p.Hkv + hkv]) : 0;
+      constexpr int NP = 32;  // pairs per thread
+      uint32_t o[D / 4];
+      uint32_t s[NP];
+      float m_run = 0.f, l_run = 0.f, fbar = 0.f;
+      float rcp_j = 1.0f;  // 1/(j+1), computed off the critical path
+      // both tiles' block counts (identical in every thread of the CTA)
+      const int nmin = min(tile_info(p, hkv, unit * NT, CAUSAL).nblk,
+                           tile_info(p, hkv, unit * NT + 1, CAUSAL).nblk);
+      const bool pingpong = kPingPong;
+      for (int j = 0; j < ti.nblk; ++j) {
+        const bool tr = h == 0 && quad == 0 && lane == 0;
+        if (tr) PASA_TR(t, j, 0);
+        mbar_wait(&s_full[t], j & 1);
+        if (tr) PASA_TR(t, j, 1);
+        tc_fence_after();
+        tmem_ld_32cols_pack16(t_s + 64 * h, s);
+        tmem_ld_32cols_pack16(t_s + 64 * h + 32, s + 16);
+        tmem_wait_ld();
+        if (tr) PASA_TR(t, j, 2);
+        const bool diag = CAUSAL && (j == ti.nblk - 1);
+        constexpr bool kSum = MODE == kModePasa;
+        float mh, sh = 0.f;
+        if (diag) row_max_sum<true, NP, kSum>(s, row, NP * h, mh, sh);
+        else row_max_sum<false, NP, kSum>(s, row, NP * h, mh, sh);
+        *xslot(j & 1, h) = make_float2(mh, sh);
+        named_bar_sync(xbar, 64);
+        const float2 other = *xslot(j & 1, 1 - h);
+        const float mloc = fmaxf(mh, other.x);
+        const int jc = j + 1;
+        float mnew, ep, fnew = 0.f;
+        uint32_t cj2, scale2 = 0;
+        if (MODE == kModePasa) {
+          const float ssum = h == 0 ? __fadd_rn(sh, other.y) : __fadd_rn(other.y, sh);
+          const float sbar = __fmul_rn(ssum, 1.0f / 128.0f);
+          fnew = (jc == 1) ? sbar : __fadd_rn(fbar, __fmul_rn(__fsub_rn(sbar, fbar), rcp_j));
+          const float dmc = __fmul_rn(p.inva, __fsub_rn(sbar, fnew));
+          const float dmp = (jc == 1) ? 0.f : __fmul_rn(p.inva, __fsub_rn(fbar, fnew));
+          const float cand = __fadd_rn(mloc, dmc);
+          const float mprev = __fadd_rn(m_run, dmp);
+          mnew = (jc == 1) ? cand : fmaxf(mprev, cand);
+          const __half cj = __float2half_rn(__fsub_rn(mnew, dmc));
+          ep = (jc == 1) ? 0.f : __half2float(__float2half_rn(ex2_f32(__fsub_rn(mprev, mnew))));
+          cj2 = h2_as_u32(__half2half2(cj));
+        } else {
+          // naive FP16 FA (attention.cpp:92-180): running max of the FP16-stored
+          // scores, P = 2^(S*s - m*s) with s = log2(e)/alpha applied after the store
+          mnew = (jc == 1) ? mloc : fmaxf(m_run, mloc);
+          ep = (jc == 1) ? 0.f
+                         : __half2float(__float2half_rn(ex2_f32(__fmul_rn(__fsub_rn(m_run, mnew), p.qk_scale))));
+          cj2 = h2_as_u32(__half2half2(__hneg(__float2half_rn(__fmul_rn(mnew, p.qk_scale)))));
+          scale2 = h2_as_u32(__half2half2(__float2half_rn(p.qk_scale)));
+        }
+        if (tr) PASA_TR(t, j, 3);
+        // Ping-pong the MUFU-heavy exp pass between the two tiles:
+        // turns go T0(0), T1(0), T0(1), T1(1), ... while both tiles have blocks.
+        if (pingpong && j < nmin && (t == 1 || j > 0)) named_bar_sync(1 + t, 512);
+        constexpr bool kFa = MODE == kModeFa16;
+        const float lsum = diag ? row_exp_sum<true, NP, kFa>(s, row, NP * h, cj2, scale2)
+                                : row_exp_sum<false, NP, kFa>(s, row, NP * h, cj2, scale2);
+        if (pingpong && ((t == 0 && j < nmin) || (t == 1 && j + 1 < nmin)))
+          named_bar_arrive(2 - t, 512);
+        PASA_STATE(j, 0, mloc);
+        PASA_STATE(j, 1, MODE == kModePasa ? (h == 0 ? __fadd_rn(sh, other.y) : 0.f) : 0.f);
+        PASA_STATE(j, 2, fnew);
+        PASA_STATE(j, 3, mnew);
+        PASA_STATE(j, 4, __half2float(__low2half(u32_as_h2(cj2))));
+        PASA_STATE(j, 5, ep);
+        PASA_STATE(j, 6, lsum);
+        if (tr) PASA_TR(t, j, 7);
+        // P packed two per column: this half's 32 pairs -> columns [32h, 32h + 32)
+        tmem_st_16cols_b32(t_s + NP * h, s);
+        tmem_st_16cols_b32(t_s + NP * h + 16, s + 16);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
+        if (tr) PASA_TR(t, j, 4);
+        l_run = (jc == 1) ? lsum : __fadd_rn(__fmul_rn(ep, l_run), lsum);
+        PASA_STATE(j, 7, l_run);
+        m_run = mnew;
+        fbar = fnew;
+        rcp_j = __frcp_rn(static_cast<float>(jc + 1));
+        // T = P V_j -> this half's D/2 output columns
+        mbar_wait(&t_full[t], j & 1);
+        if (tr) PASA_TR(t, j, 5);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) tmem_ld_32cols_pack16(t_t + (D / 2) * h + c * 32, s + c * 16);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&t_empty[t]);
+        if (tr) PASA_TR(t, j, 6);
+        if (jc == 1) {
+#pragma unroll
+          for (int i = 0; i < D / 4; ++i) o[i] = s[i];
+        } else {
+          const __half2 ep2 = __float2half2_rn(ep);
+#pragma unroll
+          for (int i = 0; i < D / 4; ++i)
+            o[i] = h2_as_u32(__hfma2(ep2, u32_as_h2(o[i]), u32_as_h2(s[i])));
+        }
       }
-      PASA_TR_IF(tr, t, j, 3);
-      constexpr bool kFa = MODE == kModeFa16;
-      const float lsum = diag ? row_exp_sum<true, NP, kFa>(s, row, NP * w, cj2, scale2)
-                              : row_exp_sum<false, NP, kFa>(s, row, NP * w, cj2, scale2);
-      PASA_TR_IF(tr, t, j, 7);
-      PASA_STATE(j, 0, mloc);
-      PASA_STATE(j, 2, fnew);
-      PASA_STATE(j, 3, mnew);
-      PASA_STATE(j, 4, __half2float(__low2half(u32_as_h2(cj2))));
-      PASA_STATE(j, 5, ep);
-      PASA_STATE(j, 6, lsum);
-      // P packed two per column: this slice's 16 pairs -> columns [16w, 16w + 16)
-      tmem_st_16cols_b32(t_s + NP * w, s);
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t]);
-      PASA_TR_IF(tr, t, j, 4);
-      l_run[t] = (jc == 1) ? lsum : __fadd_rn(__fmul_rn(ep, l_run[t]), lsum);
-      PASA_STATE(j, 7, l_run[t]);
-      m_run[t] = mnew;
-      fbar[t] = fnew;
-      ep_last[t] = ep;
-    };
-
-    // ---- T = P V_j of tile t -> this slice's D/4 output columns
-    auto oupdate = [&](const int t, const int j) {
-      const uint32_t t_t = lane_base + t * Cfg::TMEM_TILE + 128;
-      const bool tr = t == 0 && w == 0 && quad == 0 && lane == 0;
-      (void)tr;
-      mbar_wait(&t_full[t], j & 1);
-      PASA_TR_IF(tr, t, j, 5);
-      tc_fence_after();
-      if (D == 128) tmem_ld_32cols_pack16(t_t + (D / 4) * w, s);
-      else tmem_ld_16cols_pack16(t_t + (D / 4) * w, s);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&t_empty[t]);
-      PASA_TR_IF(tr, t, j, 6);
-      if (j == 0) {
-#pragma unroll
-        for (int i = 0; i < NO; ++i) o[t][i] = s[i];
-      } else {
-        const __half2 ep2 = __float2half2_rn(ep_last[t]);
-#pragma unroll
-        for (int i = 0; i < NO; ++i)
-          o[t][i] = h2_as_u32(__hfma2(ep2, u32_as_h2(o[t][i]), u32_as_h2(s[i])));
-      }
-    };
-
-    const int nmax = max(nblk[0], nblk[1]);
-    for (int j = 0; j < nmax; ++j) {
-      if (j < nblk[0]) softmax(0, j);
-      if (j >= 1 && j - 1 < nblk[1]) oupdate(1, j - 1);
-      if (j < nblk[1]) softmax(1, j);
-      if (j < nblk[0]) oupdate(0, j);
-      rcp_j = __frcp_rn(static_cast<float>(j + 2));
-    }
-    if (nblk[1] > 0 && nblk[1] == nmax) oupdate(1, nmax - 1);
-
-    // ---- epilogue: global recovering O * 2^c0 / l (pasa.cpp:184-194), fp16 store
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      if (nblk[t] == 0) continue;
-      const TileInfo ti = t == 0 ? ti0 : ti1;
-      *xslot(nblk[t] & 1, t, w) = make_float2(l_run[t], 0.f);
-      named_bar_sync(xbar, 128);
-      const float l_tot = __fadd_rn(__fadd_rn(xslot(nblk[t] & 1, t, 0)->x, xslot(nblk[t] & 1, t, 1)->x),
-                                    __fadd_rn(xslot(nblk[t] & 1, t, 2)->x, xslot(nblk[t] & 1, t, 3)->x));
+      // Epilogue: global recovering O / l (pasa.cpp:184-194), fp16 store.
+      *xslot(ti.nblk & 1, h) = make_float2(l_run, 0.f);
+      named_bar_sync(xbar, 64);
+      const float lo_other = xslot(ti.nblk & 1, 1 - h)->x;
+      const float l_tot = h == 0 ? __fadd_rn(l_run, lo_other) : __fadd_rn(lo_other, l_run);
       const float inv_l = __fmul_rn(__frcp_rn(l_tot), ldexpf(1.0f, c0));  // exact 2^c0
       uint16_t* dst = p.out + ((static_cast<size_t>(b) * p.Hq + ti.hq) * p.S1 +
-                               static_cast<size_t>(ti.i) * kTile + row) * D + (D / 4) * w;
+                               static_cast<size_t>(ti.i) * kTile + row) * D + (D / 2) * h;
 #pragma unroll
-      for (int i = 0; i < NO; i += 4) {
-        uint32_t wv[4];
+      for (int i = 0; i < D / 4; i += 4) {
+        uint32_t w[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const __half a = __float2half_rn(__fmul_rn(lo_f(o[t][i + k]), inv_l));
-          const __half c = __float2half_rn(__fmul_rn(hi_f(o[t][i + k]), inv_l));
-          wv[k] = h2_as_u32(__halves2half2(a, c));
+          const __half a = __float2half_rn(__fmul_rn(lo_f(o[i + k]), inv_l));
+          const __half c = __float2half_rn(__fmul_rn(hi_f(o[i + k]), inv_l));
+          w[k] = h2_as_u32(__halves2half2(a, c));
         }
-        *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
   }

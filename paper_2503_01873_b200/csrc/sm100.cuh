@@ -144,14 +144,6 @@ __device__ __forceinline__ void tmem_ld_32cols_pack16(uint32_t taddr, uint32_t* 
         "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
-// 32 lanes x 16 columns of 16-bit values packed two per register (8 regs).
-__device__ __forceinline__ void tmem_ld_16cols_pack16(uint32_t taddr, uint32_t* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x8.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7])
-      : "r"(taddr));
-}
 // 32 lanes x 16 columns, 32-bit each (16 regs).
 __device__ __forceinline__ void tmem_ld_16cols_b32(uint32_t taddr, uint32_t* r) {
   asm volatile(
