@@ -36,7 +36,15 @@ using namespace sm100;
 // blocks -- per softmax warpgroup (warp quadrant 0, lane 0) and for the MMA
 // issuer -- into p.trace[cta][role][iter][event].
 // Alternate the two softmax warpgroups' exp passes (named barriers 1, 2).
-constexpr bool kPingPong = true;
+#ifndef PASA_PINGPONG
+#define PASA_PINGPONG 1
+#endif
+constexpr bool kPingPong = PASA_PINGPONG != 0;
+// One exp pair in kPolyEvery on the FMA-pipe polynomial (0: MUFU only).
+#ifndef PASA_POLY_EVERY
+#define PASA_POLY_EVERY 4
+#endif
+constexpr int kPolyEvery = PASA_POLY_EVERY;
 
 constexpr int kTraceCtas = 4, kTraceIters = 32, kTraceEvents = 8, kTraceRoles = 3;
 // ... followed by a per-block row-state dump (CTA (0,0), tile 0, row kTraceRow,
@@ -162,7 +170,9 @@ __device__ __forceinline__ float row_exp_sum(uint32_t* s, int row, int pbase, ui
                           : h2_as_u32(__hsub2(u32_as_h2(s[i]), u32_as_h2(cj2)));
     // one pair in four on the FMA pipe, the rest on MUFU: balances MUFU time
     // (8 cycles / pair / SMSP) against issue slots (poly ~11 vs MUFU 3 per pair)
-    uint32_t pv = ((i & 3) == 3) ? ex2_poly_f16x2(x) : ex2_f16x2(x);
+    uint32_t pv = (kPolyEvery > 0 && (i % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1)
+                      ? ex2_poly_f16x2(x)
+                      : ex2_f16x2(x);
     if (DIAG) pv &= diag_keep(pbase + i, row);
     acc[2 * (i & 3)] = add_lo_f16(acc[2 * (i & 3)], pv);
     acc[2 * (i & 3) + 1] = add_hi_f16(acc[2 * (i & 3) + 1], pv);
