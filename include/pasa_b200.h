@@ -50,9 +50,9 @@ typedef struct pasa_b200_desc {
   int32_t seq_q;     /* S1, multiple of s1                                     */
   int32_t seq_kv;    /* S2, multiple of s2                                     */
   int32_t head_dim;  /* d in {64, 128}                                         */
-  int32_t s1;        /* query block; numerically irrelevant, multiple of 128 or a divisor of it */
-  int32_t s2;        /* KV block = shifting-matrix size; this build: 128       */
-  int32_t causal;    /* 0: reference semantics; 1: causal (requires S1 == S2) */
+  int32_t s1;        /* query block; numerically irrelevant (any divisor of S1) */
+  int32_t s2;        /* KV block = shifting-matrix size, <= 128 (128 is fastest)*/
+  int32_t causal;    /* 0: reference semantics; 1: causal (S1 == S2, s2 = 128) */
   int32_t reserved;
   double beta;       /* shift fraction in [0, 1) (pasa.cpp:98-101); 0 = FP16 FA */
   double alpha;      /* static scale, must equal sqrt(d) (pasa.cpp:206-208)     */

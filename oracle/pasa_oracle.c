@@ -624,7 +624,7 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
         const double* qr = row_ptr(q, sh->Hq, sh->S1, d, b, h, i * s1 + r);
         const size_t pos = row0 + r;
         for (size_t c = 0; c < s2; ++c) S[c] = tc_dot(qr, 1, kpj + c * d, 1, d, mp->tc_mode);
-        /* Two threads per row (columns [0, s2/2) and [s2/2, s2)); in each half
+        /* Two threads per row (tile columns [0, 64) and [64, 128)); in each half
          * eight FP32 chains: column c -> chain 2*((c/2)%4) + c%2 (the kernel's
          * pair-register order), combined ((t0+t1)+(t2+t3)), t_r = a_2r + a_2r+1;
          * the row total is half0 + half1. */
@@ -632,7 +632,7 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
         double mloc = -INFINITY;
         for (size_t c = 0; c < s2; ++c) {
           const int ch = 2 * (int)((c / 2) % 4) + (int)(c % 2);
-          sacc[c >= s2 / 2][ch] = sacc[c >= s2 / 2][ch] + (float)S[c];
+          sacc[c >= 64][ch] = sacc[c >= 64][ch] + (float)S[c];
         }
         for (size_t c = 0; c < s2; ++c) {
           const int masked = sh->causal && (j * s2 + c > pos);
@@ -643,7 +643,7 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
           shalf[hh] = ((sacc[hh][0] + sacc[hh][1]) + (sacc[hh][2] + sacc[hh][3])) +
                       ((sacc[hh][4] + sacc[hh][5]) + (sacc[hh][6] + sacc[hh][7]));
         const float ssum = shalf[0] + shalf[1];
-        const float sbar = ssum * (1.0f / (float)s2);
+        const float sbar = ssum * (float)(1.0 / (double)s2);
         const float rcp = 1.0f / (float)jc; /* the kernel multiplies by 1/j */
         float fnew = (jc == 1) ? sbar : fbar[r] + (sbar - fbar[r]) * rcp;
         const float dmc = inva * (sbar - fnew);
@@ -663,7 +663,7 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
           const double a = fl16(S[c] - cj);
           S[c] = masked ? 0.0 : fl16(log2dom ? exp2(a) : exp(a));
           const int ch = 2 * (int)((c / 2) % 4) + (int)(c % 2);
-          lacc[c >= s2 / 2][ch] = lacc[c >= s2 / 2][ch] + (float)S[c];
+          lacc[c >= 64][ch] = lacc[c >= 64][ch] + (float)S[c];
         }
         for (int hh = 0; hh < 2; ++hh) { /* each half keeps its own partial l */
           const float lloc = ((lacc[hh][0] + lacc[hh][1]) + (lacc[hh][2] + lacc[hh][3])) +
@@ -745,7 +745,7 @@ ORC_API int orc_model_fa16(const orc_shape* sh, const double* q, const double* k
           const double a = fl16(S[c] * scale_h - ms);
           S[c] = masked ? 0.0 : fl16(exp2(a));
           const int ch = 2 * (int)((c / 2) % 4) + (int)(c % 2);
-          lacc[c >= s2 / 2][ch] = lacc[c >= s2 / 2][ch] + (float)S[c];
+          lacc[c >= 64][ch] = lacc[c >= 64][ch] + (float)S[c];
         }
         for (int hh = 0; hh < 2; ++hh) {
           const float lloc = ((lacc[hh][0] + lacc[hh][1]) + (lacc[hh][2] + lacc[hh][3])) +

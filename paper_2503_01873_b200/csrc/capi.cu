@@ -64,15 +64,15 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-// 3-D view {d, seq, batch*heads} of a BHSD fp16 tensor, box {64, 128, 1}, 128B swizzle.
-int make_tmap(CUtensorMap* m, const void* base, int d, int seq, int bh) {
+// 3-D view {d, seq, batch*heads} of a BHSD fp16 tensor, box {64, rows, 1}, 128B swizzle.
+int make_tmap(CUtensorMap* m, const void* base, int d, int seq, int bh, int rows = kTile) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return fail(PASA_B200_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(seq),
                         static_cast<cuuint64_t>(bh)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(d) * 2,
                            static_cast<cuuint64_t>(d) * 2 * static_cast<cuuint64_t>(seq)};
-  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(kTile), 1};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -101,11 +101,9 @@ int check_desc(const pasa_b200_desc* d) {
   // ---- limits of this build (valid for the reference, unsupported here)
   if (d->head_dim != 64 && d->head_dim != 128)
     return fail(PASA_B200_EUNSUPPORTED, "head_dim must be 64 or 128");
-  if (d->s2 != kTile) return fail(PASA_B200_EUNSUPPORTED, "s2 must be 128");
-  if (d->seq_q % kTile != 0 || d->seq_kv % kTile != 0)
-    return fail(PASA_B200_EUNSUPPORTED, "S1 and S2 must be multiples of 128");
-  if (d->causal && d->seq_q != d->seq_kv)
-    return fail(PASA_B200_EUNSUPPORTED, "causal requires S1 == S2");
+  if (d->s2 > kTile) return fail(PASA_B200_EUNSUPPORTED, "s2 must be <= 128");
+  if (d->causal && (d->seq_q != d->seq_kv || d->s2 != kTile || d->seq_q % kTile != 0))
+    return fail(PASA_B200_EUNSUPPORTED, "causal requires S1 == S2, s2 == 128, S1 % 128 == 0");
   return PASA_B200_OK;
 }
 
@@ -155,9 +153,10 @@ static int preprocess_impl(const pasa_b200_desc* d, const void* k, const void* v
                     float lscale, __half dg, __half of, cudaStream_t st) {
   if (d->head_dim != 64 && d->head_dim != 128)
     return fail(PASA_B200_EUNSUPPORTED, "head_dim must be 64 or 128");
-  if (d->s2 != kTile || d->seq_kv % kTile != 0)
-    return fail(PASA_B200_EUNSUPPORTED, "s2 must be 128 and divide S2");
+  if (d->s2 <= 0 || d->s2 > kTile || d->seq_kv % d->s2 != 0)
+    return fail(PASA_B200_EUNSUPPORTED, "s2 must be <= 128 and divide S2");
   KprepParams p{};
+  p.s2 = d->s2;
   p.k = static_cast<const uint16_t*>(k);
   p.v = static_cast<const uint16_t*>(v ? v : k);
   p.kp = static_cast<uint16_t*>(kp);
@@ -245,16 +244,18 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
   int rc;
   CUtensorMap tq, tk, tv;
   if ((rc = make_tmap(&tq, q, d->head_dim, d->seq_q, d->batch * d->heads_q))) return rc;
-  if ((rc = make_tmap(&tk, keys, d->head_dim, d->seq_kv, d->batch * d->heads_kv))) return rc;
-  if ((rc = make_tmap(&tv, v, d->head_dim, d->seq_kv, d->batch * d->heads_kv))) return rc;
+  if ((rc = make_tmap(&tk, keys, d->head_dim, d->seq_kv, d->batch * d->heads_kv, d->s2))) return rc;
+  if ((rc = make_tmap(&tv, v, d->head_dim, d->seq_kv, d->batch * d->heads_kv, d->s2))) return rc;
   FwdParams p{};
   p.B = d->batch;
   p.Hq = d->heads_q;
   p.Hkv = d->heads_kv;
   p.S1 = d->seq_q;
   p.S2 = d->seq_kv;
-  p.nq = d->seq_q / kTile;
-  p.nkv = d->seq_kv / kTile;
+  p.nq = (d->seq_q + kTile - 1) / kTile;
+  p.nkv = d->seq_kv / d->s2;
+  p.s2 = d->s2;
+  p.inv_s2 = static_cast<float>(1.0 / d->s2);
   p.group = d->heads_q / d->heads_kv;
   p.tiles_per_kv = p.group * p.nq;
   p.inva = static_cast<float>(d->beta / (1.0 - d->beta));  // pasa.cpp:85

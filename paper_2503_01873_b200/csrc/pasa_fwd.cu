@@ -46,11 +46,12 @@ constexpr bool kPingPong = PASA_PINGPONG != 0;
 #endif
 constexpr int kPolyEvery = PASA_POLY_EVERY;
 
-constexpr int kTraceCtas = 4, kTraceIters = 32, kTraceEvents = 8, kTraceRoles = 3;
+[[maybe_unused]] constexpr int kTraceCtas = 4, kTraceIters = 32, kTraceEvents = 8, kTraceRoles = 3;
 // ... followed by a per-block row-state dump (CTA (0,0), tile 0, row kTraceRow,
 // half 0): kStateIters x 8 floats {mloc, ssum, fnew, mnew, cj, ep, lsum, l_run}.
-constexpr int kTraceRow = 2, kStateIters = 512;
-constexpr int kTraceStateOffset = kTraceCtas * kTraceRoles * kTraceIters * kTraceEvents;
+[[maybe_unused]] constexpr int kTraceRow = 2, kStateIters = 512;
+[[maybe_unused]] constexpr int kTraceStateOffset =
+    kTraceCtas * kTraceRoles * kTraceIters * kTraceEvents;
 #ifdef PASA_TRACE
 #define PASA_TR(role, it, ev)                                                                  \
   do {                                                                                        \
@@ -113,9 +114,10 @@ __device__ __forceinline__ TileInfo tile_info(const FwdParams& p, int hkv, int i
   return ti;
 }
 
-// Column mask of the diagonal block for this row: keep lo/hi of pair i?
-__device__ __forceinline__ uint32_t diag_keep(int i, int row) {
-  return (2 * i + 1 <= row) ? 0xFFFFFFFFu : (2 * i <= row ? 0x0000FFFFu : 0u);
+// Column mask: keep lo/hi of pair i when its columns are < lim (lim = row + 1
+// on the causal diagonal block, s2 for a short KV block).
+__device__ __forceinline__ uint32_t col_keep(int i, int lim) {
+  return (2 * i + 1 < lim) ? 0xFFFFFFFFu : (2 * i < lim ? 0x0000FFFFu : 0u);
 }
 
 // Pass 1 over this thread's half of an S' row (32 packed pairs, global pair
@@ -124,7 +126,7 @@ __device__ __forceinline__ uint32_t diag_keep(int i, int row) {
 // chains keep the dependency depth at 8; the reduction order is restated in
 // oracle/pasa_oracle.c (orc_model_pasa).
 template <bool DIAG, int NP, bool SUM = true>
-__device__ __forceinline__ void row_max_sum(const uint32_t* s, int row, int pbase, float& mloc,
+__device__ __forceinline__ void row_max_sum(const uint32_t* s, int lim, int pbase, float& mloc,
                                             float& ssum) {
   float acc[8];
   uint32_t mx[4];
@@ -141,7 +143,7 @@ __device__ __forceinline__ void row_max_sum(const uint32_t* s, int row, int pbas
     }
     uint32_t vm = v;
     if (DIAG) {
-      const uint32_t keep = diag_keep(pbase + i, row);
+      const uint32_t keep = col_keep(pbase + i, lim);
       vm = (v & keep) | (0xFC00FC00u & ~keep);
     }
     mx[i & 3] = h2_as_u32(__hmax2(u32_as_h2(mx[i & 3]), u32_as_h2(vm)));
@@ -158,7 +160,7 @@ __device__ __forceinline__ void row_max_sum(const uint32_t* s, int row, int pbas
 // eight-chain order as pass 1.  Three pairs in four use MUFU ex2.approx.f16x2,
 // one the FMA-pipe polynomial (sm100.cuh); both are within 1 ulp of 2^x.
 template <bool DIAG, int NP, bool FA = false>
-__device__ __forceinline__ float row_exp_sum(uint32_t* s, int row, int pbase, uint32_t cj2,
+__device__ __forceinline__ float row_exp_sum(uint32_t* s, int lim, int pbase, uint32_t cj2,
                                              uint32_t scale2 = 0) {
   float acc[8];
 #pragma unroll
@@ -173,7 +175,7 @@ __device__ __forceinline__ float row_exp_sum(uint32_t* s, int row, int pbase, ui
     uint32_t pv = (kPolyEvery > 0 && (i % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1)
                       ? ex2_poly_f16x2(x)
                       : ex2_f16x2(x);
-    if (DIAG) pv &= diag_keep(pbase + i, row);
+    if (DIAG) pv &= col_keep(pbase + i, lim);
     acc[2 * (i & 3)] = add_lo_f16(acc[2 * (i & 3)], pv);
     acc[2 * (i & 3) + 1] = add_hi_f16(acc[2 * (i & 3) + 1], pv);
     s[i] = pv;
@@ -240,6 +242,14 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     }
     fence_barrier_init();
   }
+  if (p.s2 < kTile) {
+    // Short KV blocks: TMA fills rows [0, s2) of each stage, the rest must read as
+    // zero for the whole kernel (zero K' rows give S' = 0, zero V' rows add nothing).
+    uint4* z = reinterpret_cast<uint4*>(smem + Cfg::SMEM_K);
+    for (int e = threadIdx.x; e < (KS + VS) * Cfg::TILE_BYTES / 16; e += blockDim.x)
+      z[e] = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_holder);
   tc_fence_before();
   __syncthreads();
@@ -266,15 +276,15 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       for (int j = 0; j < nmax; ++j) {
         const int ks = j % KS, vs = j % VS;
         mbar_wait(&k_empty[ks], ((j / KS) & 1) ^ 1);
-        mbar_expect_tx(&k_full[ks], Cfg::TILE_BYTES);
+        mbar_expect_tx(&k_full[ks], Cfg::NBOX * 128 * p.s2);
         for (int bx = 0; bx < Cfg::NBOX; ++bx)
           tma_load_3d(smem + Cfg::SMEM_K + ks * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_kp,
-                      &k_full[ks], bx * 64, j * kTile, b * p.Hkv + hkv);
+                      &k_full[ks], bx * 64, j * p.s2, b * p.Hkv + hkv);
         mbar_wait(&v_empty[vs], ((j / VS) & 1) ^ 1);
-        mbar_expect_tx(&v_full[vs], Cfg::TILE_BYTES);
+        mbar_expect_tx(&v_full[vs], Cfg::NBOX * 128 * p.s2);
         for (int bx = 0; bx < Cfg::NBOX; ++bx)
           tma_load_3d(smem + Cfg::SMEM_V + vs * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_v,
-                      &v_full[vs], bx * 64, j * kTile, b * p.Hkv + hkv);
+                      &v_full[vs], bx * 64, j * p.s2, b * p.Hkv + hkv);
       }
     }
   } else if (warp == 1) {
@@ -388,11 +398,14 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         tmem_ld_32cols_pack16(t_s + 64 * h + 32, s + 16);
         tmem_wait_ld();
         if (tr) PASA_TR(t, j, 2);
-        const bool diag = CAUSAL && (j == ti.nblk - 1);
+        // masked columns: causal diagonal block (c > row) or a short KV block (c >= s2)
+        const bool cdiag = CAUSAL && (j == ti.nblk - 1);
+        const bool diag = cdiag || p.s2 < kTile;
+        const int lim = cdiag ? row + 1 : p.s2;
         constexpr bool kSum = MODE == kModePasa;
         float mh, sh = 0.f;
-        if (diag) row_max_sum<true, NP, kSum>(s, row, NP * h, mh, sh);
-        else row_max_sum<false, NP, kSum>(s, row, NP * h, mh, sh);
+        if (diag) row_max_sum<true, NP, kSum>(s, lim, NP * h, mh, sh);
+        else row_max_sum<false, NP, kSum>(s, lim, NP * h, mh, sh);
         *xslot(j & 1, h) = make_float2(mh, sh);
         named_bar_sync(xbar, 64);
         const float2 other = *xslot(j & 1, 1 - h);
@@ -402,7 +415,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         uint32_t cj2, scale2 = 0;
         if (MODE == kModePasa) {
           const float ssum = h == 0 ? __fadd_rn(sh, other.y) : __fadd_rn(other.y, sh);
-          const float sbar = __fmul_rn(ssum, 1.0f / 128.0f);
+          const float sbar = __fmul_rn(ssum, p.inv_s2);
           fnew = (jc == 1) ? sbar : __fadd_rn(fbar, __fmul_rn(__fsub_rn(sbar, fbar), rcp_j));
           const float dmc = __fmul_rn(p.inva, __fsub_rn(sbar, fnew));
           const float dmp = (jc == 1) ? 0.f : __fmul_rn(p.inva, __fsub_rn(fbar, fnew));
@@ -426,8 +439,8 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         // turns go T0(0), T1(0), T0(1), T1(1), ... while both tiles have blocks.
         if (pingpong && j < nmin && (t == 1 || j > 0)) named_bar_sync(1 + t, 512);
         constexpr bool kFa = MODE == kModeFa16;
-        const float lsum = diag ? row_exp_sum<true, NP, kFa>(s, row, NP * h, cj2, scale2)
-                                : row_exp_sum<false, NP, kFa>(s, row, NP * h, cj2, scale2);
+        const float lsum = diag ? row_exp_sum<true, NP, kFa>(s, lim, NP * h, cj2, scale2)
+                                : row_exp_sum<false, NP, kFa>(s, lim, NP * h, cj2, scale2);
         if (pingpong && ((t == 0 && j < nmin) || (t == 1 && j + 1 < nmin)))
           named_bar_arrive(2 - t, 512);
         PASA_STATE(j, 0, mloc);
@@ -478,6 +491,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       const float lo_other = xslot(ti.nblk & 1, 1 - h)->x;
       const float l_tot = h == 0 ? __fadd_rn(l_run, lo_other) : __fadd_rn(lo_other, l_run);
       const float inv_l = __fmul_rn(__frcp_rn(l_tot), ldexpf(1.0f, c0));  // exact 2^c0
+      const bool row_ok = ti.i * kTile + row < p.S1;  // ragged last query tile
       uint16_t* dst = p.out + ((static_cast<size_t>(b) * p.Hq + ti.hq) * p.S1 +
                                static_cast<size_t>(ti.i) * kTile + row) * D + (D / 2) * h;
 #pragma unroll
@@ -489,7 +503,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
           const __half c = __float2half_rn(__fmul_rn(hi_f(o[i + k]), inv_l));
           w[k] = h2_as_u32(__halves2half2(a, c));
         }
-        *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(w[0], w[1], w[2], w[3]);
+        if (row_ok) *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
   }

@@ -9,6 +9,7 @@ constexpr int kTile = 128;  // query tile rows (s1 on the device) and the KV blo
 // Key pre-pass: K'_j = K_j^T * M (reference pasa.cpp:53-56) in the kernel's
 // K-major layout kp[(b, h, j*s2 + c), t] = K'_j[t][c], plus max|V| per (b, h).
 struct KprepParams {
+  int s2;              // KV block size (128 on the fast path)
   const uint16_t* k;   // (B, Hkv, S2, D) fp16
   const uint16_t* v;   // (B, Hkv, S2, D) fp16 (only read for vmax)
   uint16_t* kp;        // (B, Hkv, S2, D) fp16
@@ -48,7 +49,9 @@ struct VscaleParams {
 enum FwdMode : int { kModePasa = 0, kModeFa16 = 1 };
 struct FwdParams {
   int B, Hq, Hkv, S1, S2;
-  int nq, nkv, group;     // S1/128, S2/128, Hq/Hkv
+  int nq, nkv, group;     // ceil(S1/128), S2/s2, Hq/Hkv
+  int s2;                 // KV block (shifting-matrix size), <= 128; < 128 masks columns
+  float inv_s2;           // fl32(1/s2): the block mean S'bar = sum * inv_s2
   int tiles_per_kv;       // group * nq
   float inva;             // beta / (1 - beta)       (pasa.cpp:85)
   float qk_scale;         // FA16 mode only: log2(e) / alpha applied after the FP16 store

@@ -113,6 +113,40 @@ __global__ void __launch_bounds__(D * 4) pasa_kprep_kernel(const KprepParams p) 
   }
 }
 
+// The same chains for a KV block of s2 < 128 keys (ragged / short sequences,
+// e.g. temporal attention with S2 = 25): one thread per head-dim index, the
+// block read straight from global memory (L1-resident), no column groups.
+__global__ void __launch_bounds__(128) pasa_kprep_small_kernel(const KprepParams p) {
+  const int j = blockIdx.x, bh = blockIdx.y, t = threadIdx.x, s2 = p.s2, D = p.D;
+  const size_t base = (static_cast<size_t>(bh) * p.S2 + static_cast<size_t>(j) * s2) * D;
+  const __half* kg = reinterpret_cast<const __half*>(p.k) + base;
+  __half* out = reinterpret_cast<__half*>(p.kp) + base;
+  __shared__ float red[4];
+  float vm = 0.f;
+  if (p.v) {
+    const __half* vg = reinterpret_cast<const __half*>(p.v) + base;
+    for (int e = t; e < s2 * D; e += blockDim.x) vm = fmaxf(vm, fabsf(__half2float(vg[e])));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) vm = fmaxf(vm, __shfl_xor_sync(0xffffffffu, vm, o));
+  if ((t & 31) == 0) red[t / 32] = vm;
+  __syncthreads();
+  if (t == 0) {
+    for (int w = 1; w < blockDim.x / 32; ++w) vm = fmaxf(vm, red[w]);
+    atomicMax(reinterpret_cast<int*>(p.vmax) + bh, __float_as_int(vm));
+  }
+  if (t >= D) return;
+  float prefix = 0.f;
+  for (int c = 0; c < s2; ++c) {
+    const float kc = __half2float(kg[c * D + t]);
+    float acc = __fmaf_rn(kc, p.diag, prefix);
+    for (int q = c + 1; q < s2; ++q) acc = __fmaf_rn(__half2float(kg[q * D + t]), p.off, acc);
+    if (p.lscale != 1.0f) acc = __fmul_rn(acc, p.lscale);
+    out[c * D + t] = __float2half_rn(acc);
+    prefix = __fmaf_rn(kc, p.off, prefix);
+  }
+}
+
 // V' = V * 2^-c0 (exact power-of-two scaling; RNE only where V' is subnormal).
 __global__ void __launch_bounds__(256) pasa_vscale_kernel(const VscaleParams p) {
   const long long n8 = p.total / 8;
@@ -139,6 +173,10 @@ cudaError_t launch_vscale(const VscaleParams& p, cudaStream_t stream) {
 }
 
 cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stream) {
+  if (p.s2 != kTile) {
+    pasa_kprep_small_kernel<<<dim3(p.S2 / p.s2, B * Hkv), 128, 0, stream>>>(p);
+    return cudaGetLastError();
+  }
   dim3 grid(p.S2 / kTile, B * Hkv);
   if (p.D == 128) {
     pasa_kprep_kernel<128><<<grid, dim3(128, 4), 0, stream>>>(p);

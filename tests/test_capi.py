@@ -52,6 +52,9 @@ def _check(lib, **kw):
 def test_check_accepts_config1_and_qwen(lib):
     assert _check(lib)[0] == 0
     assert _check(lib, beta=0.0)[0] == 0  # beta == 0: the FP16 FA mode (pasa.cpp:212-221)
+    # ragged: short KV block (SVD temporal N = 25) and S1 not a multiple of 128
+    assert _check(lib, seq_q=25, seq_kv=25, s1=25, s2=25, head_dim=64, alpha=8.0)[0] == 0
+    assert _check(lib, seq_q=200, seq_kv=256, s1=200, s2=64)[0] == 0
     assert _check(lib, heads_q=28, heads_kv=4, seq_q=16384, seq_kv=16384, causal=1)[0] == 0
     assert _check(lib, head_dim=64, alpha=8.0)[0] == 0
 
@@ -64,8 +67,9 @@ def test_check_accepts_config1_and_qwen(lib):
     (dict(beta=-0.1), _lib.EINVAL, "beta must lie in [0, 1)"),
     (dict(batch=0), _lib.EINVAL, "empty query tensor"),
     (dict(head_dim=96, alpha=math.sqrt(96.0)), _lib.EUNSUPPORTED, "head_dim"),
-    (dict(s2=64), _lib.EUNSUPPORTED, "s2 must be 128"),
+    (dict(s2=256, s1=256), _lib.EUNSUPPORTED, "s2 must be <= 128"),
     (dict(causal=1, seq_q=512), _lib.EUNSUPPORTED, "causal requires S1 == S2"),
+    (dict(causal=1, s2=64), _lib.EUNSUPPORTED, "causal requires S1 == S2"),
 ])
 def test_check_rejects(lib, kw, code, msg):
     rc, err = _check(lib, **kw)
@@ -76,7 +80,7 @@ def test_errors_map_to_reference_exception_types(lib):
     with pytest.raises(ValueError, match="alpha does not match"):
         _lib.check(lib.pasa_b200_check(C.byref(_desc(alpha=2.0))))
     with pytest.raises(_lib.PasaError):
-        _lib.check(lib.pasa_b200_check(C.byref(_desc(s2=64))))
+        _lib.check(lib.pasa_b200_check(C.byref(_desc(s2=256, s1=256))))
 
 
 def test_workspace_size(lib):

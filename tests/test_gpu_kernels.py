@@ -327,3 +327,45 @@ def test_fwd_long_n_sampled_rows(dev, orc):
     assert orc.nan_pct(on) == 0.0
     assert orc.rmse(on, gold) <= 1.25 * r_ref + 1e-3
     assert orc.rmse(on, refo) <= 2.0 * r_ref + 1e-3
+
+
+# ----------------------------------------------------------------- ragged shapes
+
+RAGGED = [
+    # kind, x0, am, seed, B, H, S1, S2, d, s1, s2
+    ("hybrid", 5.0, 10.0, 11, 4, 5, 25, 25, 64, 25, 25),       # SVD temporal: one 25-key block
+    ("uniform", 20.0, 2.0, 12, 1, 2, 200, 256, 128, 200, 64),  # S1 % 128 != 0, s2 = 64
+    ("hybrid", 0.0, 10.0, 13, 2, 2, 96, 384, 64, 96, 128),     # short query block only
+]
+
+
+@pytest.mark.parametrize("case", RAGGED, ids=["svd_temporal_25", "s1_200_s2_64", "s1_96"])
+def test_fwd_ragged_vs_model_and_reference(dev, orc, case):
+    from paper_2503_01873_b200 import pasa_attention_fwd
+    kind, x0, am, seed, B, H, S1, S2, D, s1, s2 = case
+    q = orc.generate(kind, x0, am, seed, B, H, S1, D, tensor_ids=(0,))[0]
+    k, v = orc.generate(kind, x0, am, seed + 100, B, H, S2, D, tensor_ids=(1, 2))
+    qt, kt, vt = (torch.from_numpy(x).half().to(dev) for x in (q, k, v))
+    o = pasa_attention_fwd(qt, kt, vt, s1=s1, s2=s2)
+    torch.cuda.synchronize()
+    pb = Problem(q, k, v, s1=s1, s2=s2)
+    on = o.double().cpu().numpy()
+    gold, model, refo = orc.golden(pb), orc.model_pasa(pb), orc.pasa_ref(pb)
+    r_model, r_ref = orc.rmse(model, gold), orc.rmse(refo, gold)
+    assert orc.nan_pct(on) == 0.0
+    assert orc.rmse(on, gold) <= 1.25 * r_model + 2e-4, (orc.rmse(on, gold), r_model)
+    assert orc.rmse(on, model) <= 0.75 * r_model + 2e-4
+    assert orc.rmse(on, gold) <= 1.25 * r_ref + 1e-3  # Tier 1 vs the reference
+
+
+def test_fa16_ragged(dev, orc):
+    from paper_2503_01873_b200 import flash_fp16_fwd
+    q, k, v = orc.generate("hybrid", 0.0, 10.0, 14, 1, 2, 160, 64)
+    k2, v2 = orc.generate("hybrid", 0.0, 10.0, 15, 1, 2, 96, 64, tensor_ids=(1, 2))
+    qt, kt, vt = (torch.from_numpy(x).half().to(dev) for x in (q, k2, v2))
+    o = flash_fp16_fwd(qt, kt, vt, s1=160, s2=32)
+    torch.cuda.synchronize()
+    pb = Problem(q, k2, v2, s1=160, s2=32)
+    gold, model = orc.golden(pb), orc.model_fa16(pb)
+    on = o.double().cpu().numpy()
+    assert orc.rmse(on, gold) <= 1.25 * orc.rmse(model, gold) + 2e-4
