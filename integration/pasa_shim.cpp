@@ -117,18 +117,19 @@ Matrix2D preprocess_keys(const Matrix2D& k_block, const Matrix2D& m,
 Tensor4D pasa_attention(const AttentionProblem& problem, const PasaParams& params,
                         const PrecisionPolicy& policy, const AttnOptions& opts,
                         RunDiagnostics* diag) {
-  (void)opts;  // threads/m0 are CPU-loop knobs; diagnose has no FP64 side channel here
+  // opts.threads is a CPU-loop knob; diagnose has no FP64 side channel here
   if (params.s2 != problem.s2) throw std::invalid_argument("pasa: params.s2 does not match the problem");
   if (params.m.rows != params.s2 || params.m.cols != params.s2)
     throw std::invalid_argument("pasa: shifting matrix has the wrong shape");
   if (params.alpha != problem.alpha)
     throw std::invalid_argument("pasa: params.alpha does not match sqrt(d)");
   if (params.beta == 1.0) throw std::invalid_argument("pasa: beta == 1 has no recovery");
-  if (params.beta == 0.0)
-    throw std::invalid_argument(
-        "pasa_b200: beta == 0 routes to flash_attention (pasa.cpp:212-221), not offloaded");
-  if (!is_pasa_fp16(policy))
+  if (!is_pasa_fp16(policy))  // PASA_FP16 and, for beta == 0, FA_PARTIAL_FP16 share these precisions
     throw std::invalid_argument("pasa_b200 offloads the PASA_FP16 policy only");
+  // beta == 0 degrades to the blocked FP16 attention (pasa.cpp:212-221); the device runs it
+  // as the FA16 mode of the same kernel, which implements the -inf initial max only.
+  if (params.beta == 0.0 && opts.m0 != M0Mode::NegInf)
+    throw std::invalid_argument("pasa_b200: beta == 0 offloads the m0 = -inf flash_attention only");
   const Tensor4D& q = problem.q;
   pasa_b200_desc desc{static_cast<int32_t>(q.batch), static_cast<int32_t>(q.heads),
                       static_cast<int32_t>(problem.k.heads), static_cast<int32_t>(q.seq),
