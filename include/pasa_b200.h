@@ -90,7 +90,7 @@ PASA_B200_API size_t pasa_b200_workspace_size(const pasa_b200_desc* desc);
  * loop at :231-240), device pointers, stream-ordered.  Output layout is
  * K-major: kp[(b, h, j*s2 + c), t] = K'_j[t][c].  lscale = 1 gives the
  * reference's bits exactly (FP32 sequential accumulate, one FP16 rounding);
- * the fused path uses lscale = log2(e).  vmax (nullable, B*Hkv floats) gets
+ * the fused path uses lscale = log2(e)/2.  vmax (nullable, B*Hkv floats) gets
  * max|V| per head when v is non-NULL. */
 PASA_B200_API int pasa_b200_preprocess_keys(const pasa_b200_desc* desc, const void* k, const void* v,
                               void* kp, float* vmax, float lscale, void* stream);
@@ -113,7 +113,7 @@ PASA_B200_API int pasa_b200_attention_fwd(const pasa_b200_desc* desc, const void
                             pasa_b200_diag* diag, void* stream);
 
 /* The full pre-pass of the fused kernel, device pointers, stream-ordered:
- * kp = K'^T blocks with lscale = log2(e) (as pasa_b200_preprocess_keys),
+ * kp = K'^T blocks with lscale = log2(e)/2 (as pasa_b200_preprocess_keys),
  * vmax = max|V| per (b, kv head), and vp = V * 2^-c0 per head with
  * c0 = max(0, ceil(log2(S2 * vmax / 2^14))) -- the exact power-of-two scale
  * that keeps the FP16 O accumulator bounded. */
@@ -143,6 +143,26 @@ PASA_B200_API int pasa_b200_flash_fp16_fwd(const pasa_b200_desc* desc, const voi
  * speed, pageable ones through the driver's staging path. */
 PASA_B200_API int pasa_b200_attention_host(const pasa_b200_desc* desc, const uint16_t* q, const uint16_t* k,
                              const uint16_t* v, uint16_t* o);
+
+/* Device-side input generator: elements [start,
+ * start + n) of tensor `tensor_id` (0 = Q, 1 = K, 2 = V) of the reference's
+ * generate() (bench.cpp:28-72, rng.hpp:14-40) as binary16 into device memory:
+ * kind 0 = uniform x0 - am + 2 am u, kind 1 = hybrid x0 + N(0,1) plus a
+ * Bernoulli(p)-gated am * N(0,1) outlier.  Uniform is bit-identical to the
+ * reference; hybrid agrees except within an ulp of an FP16 rounding boundary
+ * (device log/cos).  Errors: p outside (0, 1) for hybrid -> EINVAL with the
+ * reference's message.  Stream-ordered. */
+PASA_B200_API int pasa_b200_generate(int32_t kind, double x0, double am, double p, uint64_t seed,
+                                     uint64_t tensor_id, uint64_t start, uint64_t n, void* out,
+                                     void* stream);
+
+/* Resonance inputs (the SVD d = 64 case): BHSD tensor
+ * `tensor_id` with Q = qa cos(2 pi 3c/d + 0.3h) + U(-1,1),
+ * K = -ka (1 + 0.1 sin(2 pi s/512)) cos(...) + U(-1,1), V = U(-1,1).  Matches
+ * the oracle's orc_generate_resonance.  Stream-ordered. */
+PASA_B200_API int pasa_b200_generate_resonance(uint64_t seed, int32_t tensor_id, int32_t batch,
+                                               int32_t heads, int32_t seq, int32_t head_dim,
+                                               double qa, double ka, void* out, void* stream);
 
 #ifdef __cplusplus
 }  /* extern "C" */

@@ -60,6 +60,7 @@ class ModelParams(C.Structure):
     _fields_ = [
         ("beta", C.c_double), ("diag", C.c_double), ("off", C.c_double),
         ("lscale", C.c_double), ("tc_mode", C.c_int), ("c0", C.c_double),
+        ("xscale", C.c_double),
     ]
 
 
@@ -229,11 +230,17 @@ class Oracle:
     def model_inflation(self, vmax: float, S2: int, lscale: float = LOG2E) -> float:
         return self.lib.orc_model_inflation(vmax, S2, lscale)
 
-    def model_pasa(self, pb: Problem, beta: float = BETA_STAR, lscale: float = LOG2E,
-                   tc_mode: int = 1, c0: float = -1.0, threads: int = 0) -> np.ndarray:
+    def model_pasa(self, pb: Problem, beta: float = BETA_STAR, lscale: float = LOG2E / 2,
+                   tc_mode: int = 1, c0: float = -1.0, threads: int = 0,
+                   xscale: float | None = None) -> np.ndarray:
+        """The kernel's numerics: scores stored in units of lscale
+        (log2(e)/2 on the device), exp argument xscale*fl16(S' - c_j) with
+        xscale = log2(e)/lscale rounded to the power of two (2 by default)."""
         d = pb.q.shape[-1]
         diag, off = self.shift_entries(pb.s2, beta, float(np.sqrt(d)), P16)
-        mp = ModelParams(beta, diag, off, lscale, tc_mode, c0)
+        if xscale is None:
+            xscale = 2.0 if lscale == LOG2E / 2 else 1.0
+        mp = ModelParams(beta, diag, off, lscale, tc_mode, c0, xscale)
         o = np.empty(pb.q.shape)
         sh = pb.shape()
         rc = self.lib.orc_model_pasa(C.byref(sh), _f64(pb.q), _f64(pb.k), _f64(pb.v), o,

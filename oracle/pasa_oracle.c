@@ -562,7 +562,11 @@ static inline double tc_dot(const double* a, size_t as, const double* b,
 typedef struct {
   double beta, diag, off, lscale;
   int tc_mode;
-  double c0; /* inflation in L units; < 0 selects the kernel's automatic rule */
+  double c0;     /* inflation in L units; < 0 selects the kernel's automatic rule */
+  double xscale; /* exact power of two applied after the store: the exp argument is
+                    xscale*fl16(S' - c_j) (the kernel: lscale = log2(e)/2,
+                    xscale = 2, so the FP16 S' store holds 1/ln 2 / 2 = 0.72 x the
+                    reference's scores and overflows later than the reference) */
 } orc_model_params;
 
 /* The kernel's O-bounding exponent (pasa_kernels.cuh: pasa_inflation): the
@@ -588,6 +592,7 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
   const float inva = (float)(mp->beta / (1.0 - mp->beta));
   const double L = mp->lscale;
   const int log2dom = (L != 1.0);
+  const double xs = mp->xscale > 0.0 ? mp->xscale : 1.0;
   const int nt = resolve_threads(threads);
   double* kp = malloc(sizeof(double) * sh->B * sh->Hkv * sh->S2 * d);
   orc_preprocess_keys(k, sh->B, sh->Hkv, sh->S2, d, s2, mp->diag, mp->off, P32,
@@ -654,13 +659,17 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
         const double cj = fl16((double)cjf);
         double ep = 0.0;
         if (jc > 1) {
-          const float earg = (m[r] + dmp) - mnew;
+          const float earg = ((m[r] + dmp) - mnew) * (float)xs;
           ep = fl16(log2dom ? exp2((double)earg) : exp((double)earg));
         }
         float lacc[2][8] = {{0.f}}; /* same chains, per half row */
         for (size_t c = 0; c < s2; ++c) {
           const int masked = sh->causal && (j * s2 + c > pos);
-          const double a = fl16(S[c] - cj);
+          /* the kernel's one-HFMA2 form fl16(xs S' - xs c_j) while xs c_j fits FP16,
+           * else xs fl16(S' - c_j) (both exact scalings of the same rounding
+           * except in the subnormal range) */
+          const double a = (fabs(xs * cj) <= 65504.0) ? fl16(xs * S[c] - xs * cj)
+                                                      : xs * fl16(S[c] - cj);
           S[c] = masked ? 0.0 : fl16(log2dom ? exp2(a) : exp(a));
           const int ch = 2 * (int)((c / 2) % 4) + (int)(c % 2);
           lacc[c >= 64][ch] = lacc[c >= 64][ch] + (float)S[c];

@@ -64,6 +64,9 @@ def load(path: str = SO) -> C.CDLL:
     L.pasa_b200_attention_host.argtypes = [dp, vp, vp, vp, vp]
     L.pasa_b200_flash_fp16_fwd.argtypes = [dp, vp, vp, vp, vp, vp]
     L.pasa_b200_preprocess_keys_host.argtypes = [dp, vp, vp, C.c_double, C.c_double]
+    u64, i32, f64 = C.c_uint64, C.c_int32, C.c_double
+    L.pasa_b200_generate.argtypes = [i32, f64, f64, f64, u64, u64, u64, u64, vp, vp]
+    L.pasa_b200_generate_resonance.argtypes = [u64, i32, i32, i32, i32, i32, f64, f64, vp, vp]
     _LIB = L
     return L
 

@@ -22,6 +22,8 @@ cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stre
 cudaError_t launch_vscale(const VscaleParams& p, cudaStream_t stream);
 cudaError_t launch_fwd(int D, bool causal, int mode, const CUtensorMap& tq, const CUtensorMap& tk,
                        const CUtensorMap& tv, const FwdParams& p, cudaStream_t stream);
+cudaError_t launch_generate(const GenParams& p, void* out, cudaStream_t stream);
+cudaError_t launch_generate_resonance(const ResonanceParams& p, void* out, cudaStream_t stream);
 }  // namespace pasa_b200
 
 using namespace pasa_b200;
@@ -222,7 +224,8 @@ int pasa_b200_preprocess(const pasa_b200_desc* d, const void* k, const void* v, 
   __half dg, of;
   shift_scalars(d->s2, d->beta, d->alpha, &dg, &of);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int rc = preprocess_impl(d, k, v, kp, vmax, static_cast<float>(kLog2e), dg, of, st);
+  // K' carries log2(e)/2: the kernel's exp argument is 2 fl16(S' - c_j)
+  int rc = preprocess_impl(d, k, v, kp, vmax, static_cast<float>(0.5 * kLog2e), dg, of, st);
   if (rc) return rc;
   VscaleParams vs{};
   vs.v = static_cast<const uint16_t*>(v);
@@ -372,3 +375,29 @@ __attribute__((visibility("default"))) int pasa_b200_debug_set_trace(void* devic
 #endif
 
 }  // extern "C"
+
+int pasa_b200_generate(int32_t kind, double x0, double am, double p, uint64_t seed,
+                       uint64_t tensor_id, uint64_t start, uint64_t n, void* out, void* stream) {
+  g_last_error.clear();
+  if (kind != 0 && kind != 1) return fail(PASA_B200_EINVAL, "generate: kind must be 0 or 1");
+  if (kind == 1 && !(p > 0.0 && p < 1.0))
+    return fail(PASA_B200_EINVAL, "generate: p must lie in (0, 1)");  // bench.cpp:59-61
+  if (n && !out) return fail(PASA_B200_EINVAL, "generate: NULL output");
+  GenParams gp{kind, x0, am, p, seed, tensor_id, start, n};
+  const cudaError_t e = launch_generate(gp, out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "generate");
+}
+
+int pasa_b200_generate_resonance(uint64_t seed, int32_t tensor_id, int32_t batch, int32_t heads,
+                                 int32_t seq, int32_t head_dim, double qa, double ka, void* out,
+                                 void* stream) {
+  g_last_error.clear();
+  if (tensor_id < 0 || tensor_id > 2)
+    return fail(PASA_B200_EINVAL, "generate_resonance: tensor_id must be 0, 1 or 2");
+  if (batch < 0 || heads < 0 || seq < 0 || head_dim <= 0)
+    return fail(PASA_B200_EINVAL, "generate_resonance: negative or zero extent");
+  if (!out && batch && heads && seq) return fail(PASA_B200_EINVAL, "generate_resonance: NULL output");
+  ResonanceParams rp{seed, tensor_id, batch, heads, seq, head_dim, qa, ka};
+  const cudaError_t e = launch_generate_resonance(rp, out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? 0 : cuda_fail(e, "generate_resonance");
+}

@@ -14,7 +14,8 @@
 // Per KV block j and tile t (reference pasa.cpp:256-278, Algorithm 1):
 //   S'_t  = Q_t K'_j^T      tcgen05.mma kind::f16, SS, F16 accumulator in TMEM
 //   softmax WG: tcgen05.ld S' (packed half2), row max / FP32 row mean,
-//   pseudo-average recursion, corrected max, P = 2^(S' - c_j) (f16x2 MUFU),
+//   pseudo-average recursion, corrected max, P = 2^(2(S' - c_j)) (f16x2 MUFU;
+//   S' is stored in units of log2(e)/2),
 //   tcgen05.st P back over the S' columns (packed 2 x f16 per column)
 //   T_t   = P V_j           tcgen05.mma kind::f16, TS (P from TMEM), F16 acc
 //   softmax WG: O <- e_prev * O + T in half2 registers (HFMA2)
@@ -159,7 +160,7 @@ __device__ __forceinline__ void row_max_sum(const uint32_t* s, int lim, int pbas
 // Pass 2: P = 2^(S' - c_j) in place (masked -> 0) and its FP32 sum, same
 // eight-chain order as pass 1.  Three pairs in four use MUFU ex2.approx.f16x2,
 // one the FMA-pipe polynomial (sm100.cuh); both are within 1 ulp of 2^x.
-template <bool DIAG, int NP, bool FA = false>
+template <bool DIAG, int NP, bool FMA>
 __device__ __forceinline__ float row_exp_sum(uint32_t* s, int lim, int pbase, uint32_t cj2,
                                              uint32_t scale2 = 0) {
   float acc[8];
@@ -167,9 +168,17 @@ __device__ __forceinline__ float row_exp_sum(uint32_t* s, int lim, int pbase, ui
   for (int k = 0; k < 8; ++k) acc[k] = 0.f;
 #pragma unroll
   for (int i = 0; i < NP; ++i) {
-    // PASA: x = S' - c_j.  FA16: x = S*(log2e/alpha) - m*(log2e/alpha) in one HFMA2.
-    const uint32_t x = FA ? h2_as_u32(__hfma2(u32_as_h2(s[i]), u32_as_h2(scale2), u32_as_h2(cj2)))
-                          : h2_as_u32(__hsub2(u32_as_h2(s[i]), u32_as_h2(cj2)));
+    // FMA form: x = fl16(S * scale - c) in one HFMA2 -- FA16: scale = log2e/alpha,
+    // c = m*scale; PASA: scale = 2, c = 2 c_j (scores are stored in units of
+    // log2(e)/2, so the FP16 store holds 0.72x the reference's scores).
+    // Split form (PASA rows with |c_j| > 32752): x = 2 fl16(S' - c_j), exact doubling.
+    uint32_t x;
+    if (FMA) {
+      x = h2_as_u32(__hfma2(u32_as_h2(s[i]), u32_as_h2(scale2), u32_as_h2(cj2)));
+    } else {
+      const __half2 d = __hsub2(u32_as_h2(s[i]), u32_as_h2(cj2));
+      x = h2_as_u32(__hadd2(d, d));
+    }
     // one pair in four on the FMA pipe, the rest on MUFU: balances MUFU time
     // (8 cycles / pair / SMSP) against issue slots (poly ~11 vs MUFU 3 per pair)
     uint32_t pv = (kPolyEvery > 0 && (i % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1)
@@ -413,6 +422,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         const int jc = j + 1;
         float mnew, ep, fnew = 0.f;
         uint32_t cj2, scale2 = 0;
+        bool fast2 = true;  // PASA: the exp argument is one HFMA2 (see below)
         if (MODE == kModePasa) {
           const float ssum = h == 0 ? __fadd_rn(sh, other.y) : __fadd_rn(other.y, sh);
           const float sbar = __fmul_rn(ssum, p.inv_s2);
@@ -423,8 +433,14 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
           const float mprev = __fadd_rn(m_run, dmp);
           mnew = (jc == 1) ? cand : fmaxf(mprev, cand);
           const __half cj = __float2half_rn(__fsub_rn(mnew, dmc));
-          ep = (jc == 1) ? 0.f : __half2float(__float2half_rn(ex2_f32(__fsub_rn(mprev, mnew))));
-          cj2 = h2_as_u32(__half2half2(cj));
+          ep = (jc == 1) ? 0.f
+                         : __half2float(__float2half_rn(ex2_f32(__fmul_rn(2.f, __fsub_rn(mprev, mnew)))));
+          // x = fl16(2 S' - 2 c_j) in one HFMA2 while -2 c_j is representable (every
+          // row of the warp: |c_j| <= 32752); otherwise 2 fl16(S' - c_j) in two ops.
+          fast2 = __all_sync(0xFFFFFFFFu, __habs(cj) <= __float2half_rn(32752.f));
+          cj2 = fast2 ? h2_as_u32(__half2half2(__hmul(cj, __float2half_rn(-2.f))))
+                      : h2_as_u32(__half2half2(cj));
+          scale2 = h2_as_u32(__float2half2_rn(2.f));
         } else {
           // naive FP16 FA (attention.cpp:92-180): running max of the FP16-stored
           // scores, P = 2^(S*s - m*s) with s = log2(e)/alpha applied after the store
@@ -438,9 +454,13 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         // Ping-pong the MUFU-heavy exp pass between the two tiles:
         // turns go T0(0), T1(0), T0(1), T1(1), ... while both tiles have blocks.
         if (pingpong && j < nmin && (t == 1 || j > 0)) named_bar_sync(1 + t, 512);
-        constexpr bool kFa = MODE == kModeFa16;
-        const float lsum = diag ? row_exp_sum<true, NP, kFa>(s, lim, NP * h, cj2, scale2)
-                                : row_exp_sum<false, NP, kFa>(s, lim, NP * h, cj2, scale2);
+        float lsum;
+        if (MODE == kModeFa16 || fast2)
+          lsum = diag ? row_exp_sum<true, NP, true>(s, lim, NP * h, cj2, scale2)
+                      : row_exp_sum<false, NP, true>(s, lim, NP * h, cj2, scale2);
+        else
+          lsum = diag ? row_exp_sum<true, NP, false>(s, lim, NP * h, cj2, scale2)
+                      : row_exp_sum<false, NP, false>(s, lim, NP * h, cj2, scale2);
         if (pingpong && ((t == 0 && j < nmin) || (t == 1 && j + 1 < nmin)))
           named_bar_arrive(2 - t, 512);
         PASA_STATE(j, 0, mloc);

@@ -60,4 +60,16 @@ struct FwdParams {
   long long* trace;       // PASA_TRACE builds only: clock64 timeline (see pasa_fwd.cu)
 };
 
+// Device generators (pasa_gen.cu; bench.cpp:28-56, rng.hpp).
+struct GenParams {
+  int kind;            // 0 = uniform(x0 +- am), 1 = hybrid normal + Bernoulli(p) outlier
+  double x0, am, p;
+  uint64_t seed, tensor_id, start, n;  // flat indices [start, start + n) of tensor `tensor_id`
+};
+struct ResonanceParams {
+  uint64_t seed;
+  int tensor_id, B, H, S, d;
+  double qa, ka;
+};
+
 }  // namespace pasa_b200

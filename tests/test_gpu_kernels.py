@@ -369,3 +369,27 @@ def test_fa16_ragged(dev, orc):
     gold, model = orc.golden(pb), orc.model_fa16(pb)
     on = o.double().cpu().numpy()
     assert orc.rmse(on, gold) <= 1.25 * orc.rmse(model, gold) + 2e-4
+
+
+def test_fwd_store_headroom_beyond_reference(dev, orc):
+    """One key whose shifted score is ~5.05e4 (inside FP16, 1.17 % of the reference's
+    PASA rows still overflow elsewhere in its pipeline).  The kernel stores S' in units
+    of log2(e)/2 (0.72x the reference's scores), so it stays finite and exact; a
+    log2(e)-scaled store would overflow at 4.5e4."""
+    from paper_2503_01873_b200 import pasa_attention_fwd
+    rng = np.random.default_rng(21)
+    S, D = 256, 128
+    q = orc.f16(100.0 + rng.uniform(-1, 1, (1, 1, S, D)))
+    k = orc.f16(rng.uniform(-1, 1, (1, 1, S, D)))
+    k[:, :, 0, :] += 45.0
+    k = orc.f16(k)
+    v = orc.f16(rng.uniform(-1, 1, (1, 1, S, D)))
+    pb = Problem(q, k, v)
+    gold = orc.golden(pb)
+    assert orc.nan_pct(orc.model_pasa(pb, lscale=LOG2E)) == 100.0  # the log2(e) store overflows
+    assert orc.nan_pct(orc.flash_ref(pb)) == 100.0                 # and so does naive FP16 FA
+    qt, kt, vt = (torch.from_numpy(x).half().to(dev) for x in (q, k, v))
+    o = pasa_attention_fwd(qt, kt, vt).double().cpu().numpy()
+    assert orc.nan_pct(o) == 0.0
+    assert orc.rmse(o, gold) <= 1e-3
+    assert orc.rmse(o, orc.model_pasa(pb)) <= 1e-3

@@ -24,7 +24,7 @@ st = tr[4 * 3 * 32 * 8:].cpu().numpy().view(np.float32).reshape(512, 8)
 # ---- NumPy mirror of orc_model_pasa for one row (float32 scalars, fp16 elements)
 f16 = lambda x: np.float16(x).astype(np.float64)
 diag, off = orc.shift_entries(128, BETA_STAR, math.sqrt(128.0))
-kp = orc.preprocess_keys(k, 128, diag, off, lscale=1.4426950408889634)[0, 0]   # (S, 128)
+kp = orc.preprocess_keys(k, 128, diag, off, lscale=1.4426950408889634 / 2)[0, 0]   # (S, 128)
 qr = qs[0, 0, ROW]
 vh = v[0, 0]
 vmax = np.abs(v).max(); c0 = orc.model_inflation(vmax, S)
