@@ -280,6 +280,11 @@ class RefLib:
         L.ref_rmse.restype = C.c_double
         L.ref_rmse.argtypes = [sz, _dp, _dp]
         L.ref_nan_stats.restype = C.c_double
+        L.ref_report.restype = C.c_long
+        L.ref_report.argtypes = [C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_char_p),
+                                 C.POINTER(C.c_char_p), _dp,
+                                 np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS"), C.c_int,
+                                 C.c_char_p, sz]
         L.ref_nan_stats.argtypes = [sz, _dp]
         L.ref_shift_entries.argtypes = [sz, C.c_double, C.c_double, C.c_int,
                                         C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -329,6 +334,24 @@ class RefLib:
     def rmse(self, x, g):
         x, g = _f64(x).reshape(-1), _f64(g).reshape(-1)
         return self.lib.ref_rmse(x.size, x, g)
+
+    def report(self, rows, json: bool = False) -> str:
+        """The reference's report_csv / report_json_rows text for RunReport-like rows."""
+        n = len(rows)
+        enc = lambda xs: (C.c_char_p * max(n, 1))(*[x.encode() for x in xs])  # noqa: E731
+        nums = np.zeros((max(n, 1), 14))
+        ints = np.zeros((max(n, 1), 6), dtype=np.int64)
+        for i, r in enumerate(rows):
+            nums[i, :11] = [r.x0, r.am, r.p, r.beta, r.rmse, r.nan_pct, r.s_min_before,
+                            r.s_max_before, r.s_min_after, r.s_max_after, r.wall_s]
+            ints[i] = [r.seed, r.batch, r.heads, r.seq, r.dim, int(r.has_ranges)]
+        cap = 4096 + 1024 * n
+        buf = C.create_string_buffer(cap)
+        m = self.lib.ref_report(n, enc([r.policy for r in rows]), enc([r.kind for r in rows]),
+                                enc([r.error for r in rows]), nums, ints, int(json), buf, cap)
+        if m < 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return buf.value.decode()
 
     def nan_stats(self, x):
         x = _f64(x).reshape(-1)

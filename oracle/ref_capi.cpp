@@ -13,6 +13,7 @@
 #include <cstring>
 #include <exception>
 #include <string>
+#include <vector>
 
 #include "pasa/attention.hpp"
 #include "pasa/bench.hpp"
@@ -180,6 +181,40 @@ int ref_invariance(double beta, size_t n, double* out5) {
     out5[3] = r.inva_actual;
     out5[4] = r.rel_err;
   });
+}
+
+// The reference's report text (bench.cpp:249-316) for n rows given field by
+// field: nums[i*14 + ...] = {x0, am, p, beta, rmse, nan_pct, s_min_before,
+// s_max_before, s_min_after, s_max_after, wall_s, -, -, -}, ints[i*6 + ...] =
+// {seed, B, N, S, d, has_ranges}; json = 0 -> report_csv, 1 -> report_json_rows.
+// Returns the byte count written (truncated to cap - 1), or -1.
+long ref_report(int n, const char* const* policy, const char* const* kind,
+                const char* const* error, const double* nums, const long long* ints,
+                int json, char* out, size_t cap) {
+  std::string text;
+  const int rc = guarded([&] {
+    std::vector<pasa::RunReport> rows(n);
+    for (int i = 0; i < n; ++i) {
+      pasa::RunReport& r = rows[i];
+      const double* f = nums + 14 * i;
+      const long long* z = ints + 6 * i;
+      r.policy = policy[i];
+      r.kind = kind[i];
+      r.error = error[i];
+      r.x0 = f[0]; r.am = f[1]; r.p = f[2]; r.beta = f[3]; r.rmse = f[4]; r.nan_pct = f[5];
+      r.s_min_before = f[6]; r.s_max_before = f[7]; r.s_min_after = f[8]; r.s_max_after = f[9];
+      r.wall_s = f[10];
+      r.seed = static_cast<uint64_t>(z[0]);
+      r.batch = z[1]; r.heads = z[2]; r.seq = z[3]; r.dim = z[4];
+      r.has_ranges = z[5] != 0;
+    }
+    text = json ? pasa::report_json_rows(rows) : pasa::report_csv(rows);
+  });
+  if (rc) return -1;
+  const size_t m = text.size() < cap ? text.size() : cap - 1;
+  std::memcpy(out, text.data(), m);
+  out[m] = 0;
+  return static_cast<long>(m);
 }
 
 }  // extern "C"
