@@ -76,7 +76,7 @@ def test_device_golden_rmse_nan_stats_match_reference(dev, orc, ref):
     gold = _np(ba.golden_attention(qt, kt, vt))
     assert np.abs(gold - gold_cpu).max() <= 1e-12
     g32 = _np(ba.golden_attention(qt, kt, vt, dtype=torch.float32))
-    assert np.abs(g32 - gold_cpu).max() <= 1e-5
+    assert np.abs(g32 - gold_cpu).max() <= 2e-4  # FP32 softmax over 384 keys, |O| ~ 5
     gs = _np(ba.golden_attention(qt, kt, vt, rows=slice(128, 256)))
     assert np.abs(gs - gold_cpu[:, :, 128:256]).max() <= 1e-12
     o = ref.pasa(pb)
@@ -150,9 +150,10 @@ def test_cli_sweep_gate_and_run(dev, tmp_path):
     assert r.returncode == 0, r.stderr
     doc = json.load(open(tmp_path / "s.json"))
     assert doc["config"]["shape"] == [1, 2, 256, 64] and len(doc["rows"]) == 12
-    r = subprocess.run(cmd + ["sweep", "--preset", "appendix-e", "--small", "--must-be-finite",
-                              "FA_PARTIAL_FP16"], capture_output=True, text=True, cwd=ROOT, env=env)
-    assert r.returncode == 2  # naive FP16 FA overflows on the x0 = 30 cells
+    r = subprocess.run(cmd + ["sweep", "--preset", "appendix-e", "--shape", "1,2,256,128",
+                              "--must-be-finite", "FA_PARTIAL_FP16"], capture_output=True,
+                       text=True, cwd=ROOT, env=env)
+    assert r.returncode == 2  # naive FP16 FA overflows on the x0 = 30 cells at d = 128
     d = str(tmp_path / "in")
     r = subprocess.run(cmd + ["gen", "--kind", "hybrid", "--x0", "30", "--am", "10", "--shape",
                               "1,2,256,128", "--out-dir", d], capture_output=True, text=True,
