@@ -12,9 +12,12 @@ plus the fused PASA forward kernel (pasa.cpp:196-293).  FLOPs follow the FA
 convention, 4 * B * Hq * S1 * S2 * d, halved for causal.
 
 Inputs are synthetic: the reference's hybrid distribution (x0 = 0, Am = 10,
-p = 0.001; bench.cpp:28-40) with a Qwen-like K/Q channel bias that pushes
-pre-scale scores past the FP16 range, generated on the
-device.  Inputs (Q + K + V + O ~ 300 MB) exceed L2 and L2 is also flushed
+p = 0.001; bench.cpp:28-40), generated on the device with the reference's own
+counter-based generator (identical values), with a Qwen-like K/Q channel bias
+that pushes pre-scale scores past the FP16 range.
+Accuracy is also reported on uniform(30, 0.5) at the same shape (non-degenerate
+softmax, overflows naive FP16 FA) and on a parity sample shared with the CPU
+reference.  Inputs (Q + K + V + O ~ 300 MB) exceed L2 and L2 is also flushed
 (256 MiB write) between timed steps, outside the timed events.
 
 ``--impl reference`` times the reference's own CPU implementation
@@ -120,46 +123,45 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- inputs
+CHANS = (7, 23, 71, 101)                  # Qwen-like outlier channels
+KBIAS = (400.0, -250.0, 300.0, -150.0)
+QBIAS = (-140.0, 150.0, -160.0, 120.0)
+SEED = 1234
+
+
 def make_inputs(torch, dev, B, S, seed):
-    """Hybrid(0, 10, p=0.001) + Qwen-like channel bias, FP16, on the device."""
-    g = torch.Generator(device=dev)
-    g.manual_seed(seed)
-
-    def hybrid(shape):
-        core = torch.randn(shape, device=dev, generator=g)
-        gate = torch.rand(shape, device=dev, generator=g) < 0.001
-        return core + gate * (10.0 * torch.randn(shape, device=dev, generator=g))
-
-    q = hybrid((B, HQ, S, D))
-    k = hybrid((B, HKV, S, D))
-    v = hybrid((B, HKV, S, D))
-    chans = torch.tensor([7, 23, 71, 101], device=dev)
-    kbias = torch.tensor([400.0, -250.0, 300.0, -150.0], device=dev)
-    qbias = torch.tensor([-140.0, 150.0, -160.0, 120.0], device=dev)
-    k[..., chans] += kbias
-    q[..., chans] += qbias
-    return q.half(), k.half(), v.half()
-
-
-def torch_attention_fp32(torch, q, k, v, row0):
-    """FP32 reference rows [row0, row0 + q.shape[2]) under the causal mask."""
-    q, k, v = q.float(), k.float(), v.float()
-    s = (q @ k.transpose(-1, -2)) / math.sqrt(q.shape[-1])
-    rows = torch.arange(row0, row0 + q.shape[2], device=q.device)[:, None]
-    cols = torch.arange(k.shape[2], device=q.device)[None, :]
-    s = s.masked_fill(cols > rows, float("-inf"))
-    return torch.softmax(s, dim=-1) @ v
+    """The reference's hybrid(0, 10, p=0.001) tensors (bench.cpp:28-72, device generator:
+    identical values) + the Qwen-like channel bias, FP16, on the device."""
+    from paper_2503_01873_b200 import bench_api as ba
+    gi = ba.generate(ba.DistributionSpec(ba.DistKind.HYBRID, 0.0, 10.0, 0.001, seed, B, HQ, S, D,
+                                         HKV), dev)
+    q, k = gi.q.float(), gi.k.float()
+    for c, kb, qb in zip(CHANS, KBIAS, QBIAS):
+        k[..., c] += kb
+        q[..., c] += qb
+    return q.half(), k.half(), gi.v
 
 
 # ----------------------------------------------------------------------------- reference arm
-def reference_sample(threads_hint: int, S: int, seed: int = 0):
-    """Inputs for one bounded sample: nb query blocks of one head against all S keys."""
+def reference_sample(threads_hint: int, S: int, seed: int = SEED):
+    """One bounded sample of the bench workload for the CPU reference: the last nb query
+    blocks of query head 0 against all S keys of KV head 0 -- the same values the B200
+    arm generates (flat indices [0, S*d) of tensors 0/1/2, plus the channel bias)."""
     import numpy as np
 
     from oracle.oracle import Oracle
     orc = Oracle()
     nb = min(max(1, threads_hint), S // 128)
-    q, k, v = orc.generate("hybrid", 0.0, 10.0, seed, 1, 1, S, D)
+    outs = []
+    for tid in range(3):
+        a = np.empty(S * D)
+        orc.lib.orc_generate(1, 0.0, 10.0, 0.001, seed, tid, 0, a.size, a)
+        outs.append(a.reshape(1, 1, S, D))
+    q, k, v = outs
+    for c, kb, qb in zip(CHANS, KBIAS, QBIAS):
+        k[..., c] += kb
+        q[..., c] += qb
+    q, k = orc.f16(q), orc.f16(k)
     return np.ascontiguousarray(q[:, :, S - nb * 128:]), k, v, nb
 
 
@@ -206,7 +208,8 @@ def run_reference_arm(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f16 (emulated on f64 carriers)",
-            "data": "synthetic hybrid(0,10,p=0.001) via the reference generator",
+            "data": "synthetic hybrid(0,10,p=0.001) via the reference generator + Qwen-like "
+                    "channel bias (the B200 arm's values for head 0)",
             "config": cfg,
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "reference",
                              "sample": sample},
@@ -301,17 +304,37 @@ def run_b200(args):
     # ---------------- numerics on the measured output: RMSE vs FP32, non-finite count
     q, k, v, kp, vp, vmax, o, desc = bufs
     nonfinite = int((~torch.isfinite(o)).sum().item())
+    from paper_2503_01873_b200 import bench_api as ba
     rows = 256
     r0 = SEQ - rows
     hs = [0, 1, 7, 27]  # heads in different KV groups
     errs, norms = 0.0, 0.0
     for h in hs:
-        ref = torch_attention_fp32(torch, q[:, h:h + 1, r0:], k[:, h // 7:h // 7 + 1],
-                                   v[:, h // 7:h // 7 + 1], r0)
-        got = o[:, h:h + 1, r0:].float()
-        errs += float(((got - ref) ** 2).sum())
-        norms += float((ref ** 2).sum())
+        g = ba.golden_attention(q[:, h:h + 1], k[:, h // 7:h // 7 + 1], v[:, h // 7:h // 7 + 1],
+                                causal=True, rows=slice(r0, SEQ))
+        got = o[:, h:h + 1, r0:].double()
+        errs += float(((got - g) ** 2).sum())
+        norms += float((g ** 2).sum())
     rmse_fp32 = math.sqrt(errs / norms)
+
+    # The biased headline data is nearly one-hot (outlier keys on the bias channels win every
+    # row by ~235 in S/alpha), so also measure a non-degenerate overflow case on the same
+    # shape: Appendix E's uniform(30, 0.5) (|QK^T| ~ 1.2e5 > 65504 overflows naive FP16 FA).
+    gu = ba.generate(ba.DistributionSpec(ba.DistKind.UNIFORM, 30.0, 0.5, 0.001, SEED, 1, HQ, SEQ, D,
+                                         HKV), dev)
+    from paper_2503_01873_b200 import flash_fp16_fwd, pasa_attention_fwd
+    ou = pasa_attention_fwd(gu.q, gu.k, gu.v, BETA, causal=True)
+    ou_fa = flash_fp16_fwd(gu.q, gu.k, gu.v, causal=True)
+    eu = nu = 0.0
+    for h in hs:
+        g = ba.golden_attention(gu.q[:, h:h + 1], gu.k[:, h // 7:h // 7 + 1],
+                                gu.v[:, h // 7:h // 7 + 1], causal=True, rows=slice(r0, SEQ))
+        eu += float(((ou[:, h:h + 1, r0:].double() - g) ** 2).sum())
+        nu += float((g ** 2).sum())
+    uniform30 = {"rmse_vs_fp64": math.sqrt(eu / nu), "nonfinite": int((~torch.isfinite(ou)).sum()),
+                 "fa16_nonfinite_pct": ba.nan_stats(ou_fa),
+                 "data": "uniform(30, 0.5) (PAPER.md:596-601), same shape, causal"}
+    del gu, ou, ou_fa
 
     # ---------------- seqlen sweep (same config, other N)
     sweep = {}
@@ -369,16 +392,31 @@ def run_b200(args):
 
     # ---------------- CPU baseline (rank 0, N = 1 only)
     cpu_base = None
+    parity = None
     if world == 1 and rank == 0 and not os.environ.get("PASA_BENCH_NO_CPU"):
         from oracle.oracle import ref_available, RefLib
         if ref_available():
             cores = cpu_cores()
             qs, ks, vs, nb = reference_sample(8 * cores, SEQ)  # ~10 s of reference work
-            dt, _ = time_reference_step(RefLib(), qs, ks, vs)
+            dt, o_ref = time_reference_step(RefLib(), qs, ks, vs)
             cpu_base = {"value": 4.0 * nb * 128 * SEQ * D / dt / 1e12, "unit": UNIT,
                         "cores": cores, "kind": "reference",
                         "sample": f"pasa::pasa_attention (oracle/_ref) 1 head x {nb} query blocks "
                                   f"x {SEQ} keys, non-causal rows, {dt:.1f} s"}
+            # parity on the identical sample: the B200 kernel (non-causal, like the
+            # reference), the reference and the FP64 golden on the same rows
+            from paper_2503_01873_b200 import pasa_attention_fwd
+            qt, kt, vt = (torch.from_numpy(x).half().to(dev) for x in (qs, ks, vs))
+            o_new = pasa_attention_fwd(qt, kt, vt, BETA).double()
+            gold = ba.golden_attention(qt, kt, vt)
+            o_rt = torch.from_numpy(o_ref).to(dev)
+            parity = {"rows": nb * 128, "keys": SEQ, "head": 0,
+                      "rmse_b200_vs_fp64": ba.rmse(o_new, gold),
+                      "rmse_reference_vs_fp64": ba.rmse(o_rt, gold),
+                      "rmse_b200_vs_reference": ba.rmse(o_new, o_rt),
+                      "nan_pct_b200": ba.nan_stats(o_new), "nan_pct_reference": ba.nan_stats(o_rt),
+                      "note": "FP16 scores of this biased data carry |S'| ~ 3e2 after the shift, "
+                              "so every FP16 pipeline loses accuracy; the reference loses more"}
 
     traffic = None
     prof = os.path.join(ROOT, "profiles", "roofline_traffic.json")
@@ -411,7 +449,8 @@ def run_b200(args):
                 "api": "pasa_b200_attention_host (C-ABI, pinned host buffers)"},
         "gpu_launches": 3 * args.steps,  # key pre-pass, V scale, fused forward
         "clocks": clocks,
-        "rmse_vs_fp32": rmse_fp32, "nonfinite_outputs": nonfinite,
+        "rmse_vs_fp32": rmse_fp32, "rmse_golden": "FP64 golden_attention on device, 4 heads x 256 rows",
+        "nonfinite_outputs": nonfinite, "parity_sample": parity, "accuracy_uniform30": uniform30,
         "fa16_baseline": fa16,
         "sweep": sweep,
     }

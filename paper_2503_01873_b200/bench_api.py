@@ -153,6 +153,33 @@ def golden_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: 
     return out
 
 
+def golden_rmse(computed: torch.Tensor, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                causal: bool = False, dtype: torch.dtype = torch.float32,
+                max_chunk_bytes: int = 1 << 30) -> float:
+    """rmse(computed, golden_attention(q, k, v)) streamed over (b, h, row chunks) so the
+    golden is never materialised: full-output RMSE at N = 128K."""
+    B, Hq, S1, d = q.shape
+    S2 = k.shape[2]
+    if not bool(torch.isfinite(computed).all()):
+        return math.nan
+    elt = torch.finfo(dtype).bits // 8
+    chunk = max(1, min(S1, max_chunk_bytes // (3 * S2 * elt)))
+    err = nrm = 0.0
+    for b in range(B):
+        for h in range(Hq):
+            for i in range(0, S1, chunk):
+                j = min(S1, i + chunk)
+                g = golden_attention(q[b:b + 1, h:h + 1], k[b:b + 1, h // (Hq // k.shape[1]):][:, :1],
+                                     v[b:b + 1, h // (Hq // k.shape[1]):][:, :1], causal, dtype,
+                                     max_chunk_bytes, slice(i, j)).to(torch.float64)
+                c = computed[b, h, i:j].to(torch.float64)
+                err += float(((c - g[0, 0]) ** 2).sum())
+                nrm += float((g * g).sum())
+    if nrm == 0.0:
+        raise ZeroNormError("rmse: golden norm is zero, metric undefined")
+    return math.sqrt(err) / math.sqrt(nrm)
+
+
 def rmse(computed: torch.Tensor, golden: torch.Tensor) -> float:
     """bench.cpp:74-90: ||c - g||_2 / ||g||_2 in FP64; NaN if ``computed`` holds a NaN/INF;
     ZeroNormError if the golden norm is zero."""

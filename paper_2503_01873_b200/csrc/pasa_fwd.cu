@@ -46,8 +46,20 @@ constexpr bool kPingPong = PASA_PINGPONG != 0;
 #define PASA_POLY_EVERY 4
 #endif
 constexpr int kPolyEvery = PASA_POLY_EVERY;
+// setmaxnreg split of the per-CTA register pool (640 x 96 = 61440 at launch):
+// warpgroup 0 (TMA, MMA, 2 idle warps) drops to PASA_WG0_REGS, the four softmax
+// warpgroups rise to PASA_SM_REGS; 128 * WG0 + 512 * SM <= 61440.
+#ifndef PASA_WG0_REGS
+#define PASA_WG0_REGS 56
+#endif
+#ifndef PASA_SM_REGS
+#define PASA_SM_REGS 104
+#endif
+static_assert(128 * PASA_WG0_REGS + 512 * PASA_SM_REGS <= 61440, "register pool");
+#define PASA_STR2(x) #x
+#define PASA_STR(x) PASA_STR2(x)
 
-[[maybe_unused]] constexpr int kTraceCtas = 4, kTraceIters = 32, kTraceEvents = 8, kTraceRoles = 3;
+[[maybe_unused]] constexpr int kTraceCtas = 4, kTraceIters = 32, kTraceEvents = 10, kTraceRoles = 3;
 // ... followed by a per-block row-state dump (CTA (0,0), tile 0, row kTraceRow,
 // half 0): kStateIters x 8 floats {mloc, ssum, fnew, mnew, cj, ep, lsum, l_run}.
 [[maybe_unused]] constexpr int kTraceRow = 2, kStateIters = 512;
@@ -268,7 +280,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
   // Register budget: 640 threads x 96 at launch = 61440 per CTA; setmaxnreg
   // moves registers only within the CTA: 128 x 56 + 512 x 104 = 60416.
   if (warp < 4) {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 " PASA_STR(PASA_WG0_REGS) ";");
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
@@ -365,7 +377,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     }
   }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 " PASA_STR(PASA_SM_REGS) ";");
     // ------------------------------------------------------------ softmax WGs
     // Two threads per row: warps 4-7 / 8-11 hold columns 0-63 / 64-127 of
     // tile 0's rows, warps 12-15 / 16-19 those of tile 1.  Row max and sum are
@@ -390,6 +402,8 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       const int c0 = MODE == kModePasa ? pasa_inflation(p.S2, p.vmax[b * p.Hkv + hkv]) : 0;
       constexpr int NP = 32;  // pairs per thread
       uint32_t o[D / 4];
+#pragma unroll
+      for (int i = 0; i < D / 4; ++i) o[i] = 0u;
       uint32_t s[NP];
       float m_run = 0.f, l_run = 0.f, fbar = 0.f;
       float rcp_j = 1.0f;  // 1/(j+1), computed off the critical path
@@ -454,6 +468,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         // Ping-pong the MUFU-heavy exp pass between the two tiles:
         // turns go T0(0), T1(0), T0(1), T1(1), ... while both tiles have blocks.
         if (pingpong && j < nmin && (t == 1 || j > 0)) named_bar_sync(1 + t, 512);
+        if (tr) PASA_TR(t, j, 8);
         float lsum;
         if (MODE == kModeFa16 || fast2)
           lsum = diag ? row_exp_sum<true, NP, true>(s, lim, NP * h, cj2, scale2)
@@ -495,10 +510,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&t_empty[t]);
         if (tr) PASA_TR(t, j, 6);
-        if (jc == 1) {
-#pragma unroll
-          for (int i = 0; i < D / 4; ++i) o[i] = s[i];
-        } else {
+        {  // O <- e_prev O + T; block 1 has e_prev = 0 and O = 0 (no branch, no copies)
           const __half2 ep2 = __float2half2_rn(ep);
 #pragma unroll
           for (int i = 0; i < D / 4; ++i)

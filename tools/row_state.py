@@ -16,11 +16,11 @@ qt, kt, vt = (torch.from_numpy(x).half().to(dev) for x in (qs, k, v))
 o = torch.empty_like(qt)
 d = _lib.Desc(1, 1, 1, 128, S, 128, 128, 128, 0, 0, BETA_STAR, math.sqrt(128.0))
 ws = torch.empty(L.pasa_b200_workspace_size(C.byref(d)), dtype=torch.uint8, device=dev)
-tr = torch.zeros(4 * 3 * 32 * 8 + 512 * 4, dtype=torch.int64, device=dev)
+tr = torch.zeros(4 * 3 * 32 * 10 + 512 * 4, dtype=torch.int64, device=dev)
 L.pasa_b200_debug_set_trace(tr.data_ptr())
 _lib.check(L.pasa_b200_attention_fwd(C.byref(d), qt.data_ptr(), kt.data_ptr(), vt.data_ptr(), o.data_ptr(), ws.data_ptr(), ws.numel(), None, None))
 torch.cuda.synchronize()
-st = tr[4 * 3 * 32 * 8:].cpu().numpy().view(np.float32).reshape(512, 8)
+st = tr[4 * 3 * 32 * 10:].cpu().numpy().view(np.float32).reshape(512, 8)
 # ---- NumPy mirror of orc_model_pasa for one row (float32 scalars, fp16 elements)
 f16 = lambda x: np.float16(x).astype(np.float64)
 diag, off = orc.shift_entries(128, BETA_STAR, math.sqrt(128.0))

@@ -3,8 +3,10 @@
     python tools/sweep.py [--out profiles/r01_sweep.json] [--quick]
 
 For each configuration: fused-kernel TFLOP/s (CUDA events, L2 flushed between
-launches), step TFLOP/s (pre-pass + fused), RMSE of sampled rows against a
-torch FP32 attention and the non-finite count of the whole output.
+launches), step TFLOP/s (pre-pass + fused), RMSE of the WHOLE output against the
+device FP32 golden (bench_api.golden_rmse, streamed), RMSE of sampled rows against
+the FP64 golden, and the non-finite count.  Inputs come from the device
+generators, identical to the reference's generate().
 Configs (BASELINE.json):
   configs[1] Qwen2-7B attn 28/4 GQA d=128 causal, N in {8K, 16K, 32K}
   configs[2] SVD spatial d=64 (50 x 5 heads, N = 9216) with resonance Q/K
@@ -23,7 +25,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from paper_2503_01873_b200 import _lib  # noqa: E402
-from paper_2503_01873_b200.api import LOG2E  # noqa: E402
+from paper_2503_01873_b200 import bench_api as ba  # noqa: E402
 
 BETA = 0.984497
 
@@ -36,36 +38,16 @@ def peak():
 
 
 def gen(kind, B, Hq, Hkv, S, d, dev, seed):
-    g = torch.Generator(device=dev)
-    g.manual_seed(seed)
+    """Reference-identical inputs from the device generators (bench.cpp:28-72)."""
     if kind == "resonance":  # SURVEY 8d config 3
-        c = torch.arange(d, device=dev, dtype=torch.float32)
-        h = torch.arange(Hq, device=dev, dtype=torch.float32)[:, None, None]
-        s = torch.arange(S, device=dev, dtype=torch.float32)[None, :, None]
-        wave = torch.cos(2 * math.pi * 3 * c / d + 0.3 * h)
-        q = 70 * wave + (2 * torch.rand(B, Hq, S, d, device=dev, generator=g) - 1)
-        k = -34 * (1 + 0.1 * torch.sin(2 * math.pi * s / 512)) * wave[:Hkv] + (
-            2 * torch.rand(B, Hkv, S, d, device=dev, generator=g) - 1)
-        v = 2 * torch.rand(B, Hkv, S, d, device=dev, generator=g) - 1
-        return q.half(), k.half(), v.half()
-
-    def hybrid(shape):
-        core = torch.randn(shape, device=dev, generator=g)
-        gate = torch.rand(shape, device=dev, generator=g) < 0.001
-        return core + gate * (10.0 * torch.randn(shape, device=dev, generator=g))
-    return hybrid((B, Hq, S, d)).half(), hybrid((B, Hkv, S, d)).half(), hybrid((B, Hkv, S, d)).half()
+        gi = ba.generate_resonance(seed, B, Hq, S, d, device=dev)
+        return gi.q, gi.k[:, :Hkv].contiguous(), gi.v[:, :Hkv].contiguous()
+    gi = ba.generate(ba.DistributionSpec(ba.DistKind.HYBRID, 0.0, 10.0, 0.001, seed, B, Hq, S, d,
+                                         Hkv), dev)
+    return gi.q, gi.k, gi.v
 
 
-def ref_rows(q, k, v, r0, causal):
-    qf, kf, vf = q.float(), k.float(), v.float()
-    s = (qf @ kf.transpose(-1, -2)) / math.sqrt(q.shape[-1])
-    if causal:
-        rows = torch.arange(r0, r0 + q.shape[2], device=q.device)[:, None]
-        s = s.masked_fill(torch.arange(k.shape[2], device=q.device)[None] > rows, float("-inf"))
-    return torch.softmax(s, -1) @ vf
-
-
-def run(L, name, kind, B, Hq, Hkv, S, d, causal, iters, dev):
+def run(L, name, kind, B, Hq, Hkv, S, d, causal, iters, dev, full_rmse=True):
     q, k, v = gen(kind, B, Hq, Hkv, S, d, dev, 7)
     desc = _lib.Desc(B, Hq, Hkv, S, S, d, 128, 128, int(causal), 0, BETA, math.sqrt(d))
     _lib.check(L.pasa_b200_check(C.byref(desc)))
@@ -97,22 +79,24 @@ def run(L, name, kind, B, Hq, Hkv, S, d, causal, iters, dev):
     step = sum(e[0].elapsed_time(e[2]) for e in evs) / iters
     fwd = sum(e[1].elapsed_time(e[2]) for e in evs) / iters
     flops = 4.0 * B * Hq * S * S * d * (0.5 if causal else 1.0)
-    # accuracy: last 256 rows of a few heads vs torch FP32
-    g = Hq // Hkv
-    r0 = S - 256
+    # accuracy: every row vs the device FP32 golden (streamed), and the last 256 rows of a
+    # few heads vs the FP64 golden (the reference's golden_attention precision)
+    full = ba.golden_rmse(o, q, k, v, causal, torch.float32) if full_rmse else None
     err = nrm = 0.0
+    r0 = S - 256
     for b in range(min(B, 2)):
         for h in sorted({0, Hq // 2, Hq - 1}):
-            ref = ref_rows(q[b:b + 1, h:h + 1, r0:], k[b:b + 1, h // g:h // g + 1],
-                           v[b:b + 1, h // g:h // g + 1], r0, causal)
-            got = o[b:b + 1, h:h + 1, r0:].float()
-            err += float(((got - ref) ** 2).sum())
-            nrm += float((ref ** 2).sum())
+            g = ba.golden_attention(q[b:b + 1, h:h + 1], k[b:b + 1, h // (Hq // Hkv):][:, :1],
+                                    v[b:b + 1, h // (Hq // Hkv):][:, :1], causal,
+                                    rows=slice(r0, S))
+            got = o[b:b + 1, h:h + 1, r0:].double()
+            err += float(((got - g) ** 2).sum())
+            nrm += float((g ** 2).sum())
     res = {"config": name, "B": B, "Hq": Hq, "Hkv": Hkv, "N": S, "d": d, "causal": causal,
            "data": kind, "fwd_ms": fwd, "step_ms": step,
            "fwd_tflops": flops / fwd / 1e9, "step_tflops": flops / step / 1e9,
            "fwd_frac_of_measured_peak": flops / fwd / 1e9 / peak(),
-           "rmse_vs_fp32_sampled": math.sqrt(err / nrm),
+           "rmse_vs_fp32_full": full, "rmse_vs_fp64_sampled": math.sqrt(err / nrm),
            "nonfinite": int((~torch.isfinite(o)).sum().item())}
     print(json.dumps(res), flush=True)
     del q, k, v, kp, vp, o, flush

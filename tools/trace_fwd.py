@@ -20,7 +20,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-CTAS, ROLES, ITERS, EVENTS = 4, 3, 32, 8
+CTAS, ROLES, ITERS, EVENTS = 4, 3, 32, 10
 
 
 def main():
@@ -57,17 +57,17 @@ def main():
         rel = np.where(t[c] > 0, t[c] - base, -1)
         res[c] = rel.tolist()
         print(f"=== CTA y={c}")
-        print(" j | WG0: waitS  ldS  p1+sc  p2  stP  waitT  ldT  O   | WG1: waitS  ldS  p1+sc  p2  stP  waitT  ldT  O | period0 period1")
+        print(" j | WG0: waitS  ldS p1+sc ppwait exp  stP  waitT  ldT  O   | WG1: waitS  ldS p1+sc ppwait exp  stP  waitT  ldT  O | period0 period1")
         for j in range(1, ITERS - 1):
             row = []
             for w in range(2):
                 e = rel[w, j]
                 if e[0] < 0:
-                    row.append("   -" * 7)
+                    row.append("   -" * 9)
                     continue
                 nxt = rel[w, j + 1][0]
                 row.append(" ".join(f"{x:5d}" for x in [e[1] - e[0], e[2] - e[1], e[3] - e[2],
-                                                         e[7] - e[3], e[4] - e[7], e[5] - e[4],
+                                                         e[8] - e[3], e[7] - e[8], e[4] - e[7], e[5] - e[4],
                                                          e[6] - e[5], (nxt - e[6]) if nxt > 0 else -1]))
             per = [rel[w, j + 1][0] - rel[w, j][0] if rel[w, j + 1][0] > 0 else -1 for w in range(2)]
             print(f"{j:2d} | {row[0]} | {row[1]} | {per[0]:6d} {per[1]:6d}")
