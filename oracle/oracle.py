@@ -23,6 +23,7 @@ OWN_SO = os.path.join(HERE, "_build", "libpasa_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libpasa_ref_capi.so")
 
 P64, P32, P16 = 0, 1, 2
+PR1 = 3  # accumulation mode of the fused path's rank-1 pre-pass (orc_preprocess_keys)
 # reference PolicyId (precision.hpp:41-47)
 GOLDEN_FP64, FA_FP32, FA_PARTIAL_FP16, FA_FULL_FP16, PASA_FP16 = range(5)
 POLICY_PRECS = {  # (accum, store, vec) -- precision.cpp:23-38

@@ -38,7 +38,7 @@
 /* Precision helpers (reference precision.hpp:20-32, half.hpp:28-46)         */
 /* ------------------------------------------------------------------------ */
 
-enum { P64 = 0, P32 = 1, P16 = 2 };
+enum { P64 = 0, P32 = 1, P16 = 2, PR1 = 3 /* rank-1 pre-pass, accumulation mode only */ };
 
 static inline double fl16(double x) { return (double)(_Float16)x; }
 static inline double fl32(double x) { return (double)(float)x; }
@@ -394,6 +394,23 @@ ORC_API int orc_flash_ref(const orc_shape* sh, const double* q,
 static void prepass_block(const double* kb, size_t s2, size_t d, double diag,
                           double off, int p_acc, int p_store, double lscale,
                           double* kp) {
+  if (p_acc == PR1) {
+    /* The fused path's rank-1 pre-pass (pasa_kprep_rank1_kernel): M = (diag-off) I
+     * + off J, so K'[t][c] = fl16(fl32(fma(diag - off, K[c][t], fl32(off * colsum[t])))
+     * * lscale) with colsum the FP32 sum over p ascending. */
+    const double dm = (double)((float)diag - (float)off);
+    for (size_t t = 0; t < d; ++t) {
+      float cs = 0.f;
+      for (size_t p = 0; p < s2; ++p) cs = cs + (float)kb[p * d + t];
+      const double os = fl32(off * (double)cs);
+      for (size_t c = 0; c < s2; ++c) {
+        double a = fl32(fma(dm, kb[c * d + t], os));
+        a = fl32(a * (double)(float)lscale);
+        kp[c * d + t] = rnd(p_store, a);
+      }
+    }
+    return;
+  }
   for (size_t t = 0; t < d; ++t) {
     for (size_t c = 0; c < s2; ++c) {
       double acc = 0.0;
@@ -595,8 +612,9 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
   const double xs = mp->xscale > 0.0 ? mp->xscale : 1.0;
   const int nt = resolve_threads(threads);
   double* kp = malloc(sizeof(double) * sh->B * sh->Hkv * sh->S2 * d);
-  orc_preprocess_keys(k, sh->B, sh->Hkv, sh->S2, d, s2, mp->diag, mp->off, P32,
-                      P16, L, kp, nt);
+  /* the kernel's pre-pass: rank-1 form for full blocks, FP32 chains for s2 < 128 */
+  orc_preprocess_keys(k, sh->B, sh->Hkv, sh->S2, d, s2, mp->diag, mp->off,
+                      (L != 1.0 && s2 == 128) ? PR1 : P32, P16, L, kp, nt);
 #pragma omp parallel for num_threads(nt) schedule(dynamic)
   for (long long x = 0; x < (long long)(sh->B * sh->Hq * nq); ++x) {
     const size_t i = (size_t)x % nq;

@@ -152,7 +152,7 @@ size_t pasa_b200_workspace_size(const pasa_b200_desc* d) {
 }
 
 static int preprocess_impl(const pasa_b200_desc* d, const void* k, const void* v, void* kp, float* vmax,
-                    float lscale, __half dg, __half of, cudaStream_t st) {
+                    float lscale, __half dg, __half of, cudaStream_t st, bool rank1 = false) {
   if (d->head_dim != 64 && d->head_dim != 128)
     return fail(PASA_B200_EUNSUPPORTED, "head_dim must be 64 or 128");
   if (d->s2 <= 0 || d->s2 > kTile || d->seq_kv % d->s2 != 0)
@@ -174,6 +174,7 @@ static int preprocess_impl(const pasa_b200_desc* d, const void* k, const void* v
   p.diag = __half2float(dg);
   p.off = __half2float(of);
   p.lscale = lscale;
+  p.rank1 = rank1 && d->s2 == kTile;
   cudaError_t e = cudaMemsetAsync(p.vmax, 0, static_cast<size_t>(d->batch) * d->heads_kv * 4, st);
   if (e == cudaSuccess) e = launch_kprep(p, d->batch, d->heads_kv, st);
   if (scratch) cudaFreeAsync(scratch, st);
@@ -225,7 +226,8 @@ int pasa_b200_preprocess(const pasa_b200_desc* d, const void* k, const void* v, 
   shift_scalars(d->s2, d->beta, d->alpha, &dg, &of);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // K' carries log2(e)/2: the kernel's exp argument is 2 fl16(S' - c_j)
-  int rc = preprocess_impl(d, k, v, kp, vmax, static_cast<float>(0.5 * kLog2e), dg, of, st);
+  int rc = preprocess_impl(d, k, v, kp, vmax, static_cast<float>(0.5 * kLog2e), dg, of, st,
+                           /*rank1=*/true);
   if (rc) return rc;
   VscaleParams vs{};
   vs.v = static_cast<const uint16_t*>(v);

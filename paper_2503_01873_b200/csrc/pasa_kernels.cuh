@@ -18,7 +18,8 @@ struct KprepParams {
   int D;
   float diag;          // fl16((1 - beta/s2)/alpha)     (pasa.cpp:26)
   float off;           // fl16(-beta/(alpha*s2))        (pasa.cpp:27)
-  float lscale;        // 1 reproduces the reference; log2(e) for the fused kernel
+  float lscale;        // 1 reproduces the reference; log2(e)/2 for the fused kernel
+  int rank1;           // fused path: K' = (diag-off) K + off colsum (pasa_kprep_rank1_kernel)
 };
 
 // O-bounding exponent c0 >= 0: the smallest integer with

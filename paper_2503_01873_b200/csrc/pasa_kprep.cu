@@ -113,6 +113,65 @@ __global__ void __launch_bounds__(D * 4) pasa_kprep_kernel(const KprepParams p) 
   }
 }
 
+// The fused path's pre-pass (lscale != 1, no bit-parity with the reference's
+// chains required): M = (diag - off) I + off J is a rank-1 update of a scaled
+// identity, so K'_j[t][c] = (diag - off) K[c][t] + off * colsum_j[t] -- one FMA
+// per element after an FP32 column sum, three FP32 roundings instead of the
+// chain's 128, and a memory-bound kernel (the chain kernel above is kept for the
+// bit-exact reference pre-pass, lscale = 1).  Also reduces max|V| per head.
+//   colsum = sum_p K[p][t] (FP32, p ascending); os = fl32(off * colsum);
+//   K' = fl16(fl32(fma(diag - off, K[c][t], os)) * lscale)
+// restated in oracle/pasa_oracle.c (orc_preprocess_keys, p_acc = PR1).
+template <int D>
+__global__ void __launch_bounds__(256) pasa_kprep_rank1_kernel(const KprepParams p) {
+  constexpr int S2 = kTile, NT = 256;
+  __shared__ __align__(16) __half kb[S2 * D];
+  __shared__ float os[D];
+  __shared__ float red[NT / 32];
+  const int j = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
+  const size_t base = (static_cast<size_t>(bh) * p.S2 + static_cast<size_t>(j) * S2) * D;
+  const uint4* kg = reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(p.k) + base);
+  const uint4* vg = reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(p.v) + base);
+  float vm = 0.f;
+#pragma unroll 4
+  for (int e = tid; e < S2 * D / 8; e += NT) {
+    reinterpret_cast<uint4*>(kb)[e] = kg[e];
+    const uint4 w = vg[e];
+    const __half2* h = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __half22float2(__habs2(h[k]));
+      vm = fmaxf(vm, fmaxf(f.x, f.y));  // NaN ignored
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) vm = fmaxf(vm, __shfl_xor_sync(0xffffffffu, vm, o));
+  if ((tid & 31) == 0) red[tid / 32] = vm;
+  __syncthreads();
+  if (tid < D) {
+    float cs = 0.f;
+    for (int r = 0; r < S2; ++r) cs = __fadd_rn(cs, __half2float(kb[r * D + tid]));
+    os[tid] = __fmul_rn(p.off, cs);
+  }
+  if (tid == 0) {
+    float m = 0.f;
+    for (int w = 0; w < NT / 32; ++w) m = fmaxf(m, red[w]);
+    atomicMax(reinterpret_cast<int*>(p.vmax) + bh, __float_as_int(m));  // m >= 0
+  }
+  __syncthreads();
+  const float dm = p.diag - p.off;  // exact: both are FP16 values
+  __half2* out = reinterpret_cast<__half2*>(reinterpret_cast<__half*>(p.kp) + base);
+  const __half2* kin = reinterpret_cast<const __half2*>(kb);
+#pragma unroll 4
+  for (int e = tid; e < S2 * D / 2; e += NT) {
+    const int t = (2 * e) % D;
+    const float2 kv = __half22float2(kin[e]);
+    const float a = __fmul_rn(__fmaf_rn(dm, kv.x, os[t]), p.lscale);
+    const float b = __fmul_rn(__fmaf_rn(dm, kv.y, os[t + 1]), p.lscale);
+    out[e] = __floats2half2_rn(a, b);
+  }
+}
+
 // The same chains for a KV block of s2 < 128 keys (ragged / short sequences,
 // e.g. temporal attention with S2 = 25): one thread per head-dim index, the
 // block read straight from global memory (L1-resident), no column groups.
@@ -178,6 +237,12 @@ cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stre
     return cudaGetLastError();
   }
   dim3 grid(p.S2 / kTile, B * Hkv);
+  if (p.rank1) {  // the fused path's pre-pass: rank-1 form, memory-bound
+    if (p.D == 128) pasa_kprep_rank1_kernel<128><<<grid, 256, 0, stream>>>(p);
+    else if (p.D == 64) pasa_kprep_rank1_kernel<64><<<grid, 256, 0, stream>>>(p);
+    else return cudaErrorInvalidValue;
+    return cudaGetLastError();
+  }
   if (p.D == 128) {
     pasa_kprep_kernel<128><<<grid, dim3(128, 4), 0, stream>>>(p);
   } else if (p.D == 64) {

@@ -393,3 +393,29 @@ def test_fwd_store_headroom_beyond_reference(dev, orc):
     assert orc.nan_pct(o) == 0.0
     assert orc.rmse(o, gold) <= 1e-3
     assert orc.rmse(o, orc.model_pasa(pb)) <= 1e-3
+
+
+@pytest.mark.parametrize("D", [64, 128])
+def test_fused_prepass_rank1_bitexact(dev, orc, D):
+    """pasa_b200_preprocess (the fused path's pre-pass): K' in the rank-1 form is
+    bit-exact with the oracle's restatement (PR1), max|V| and V' = V 2^-c0 exact."""
+    from oracle.oracle import PR1
+    from paper_2503_01873_b200 import _lib
+    L = _lib.load()
+    q, k, v = orc.generate("hybrid", 20.0, 50.0, 41, 1, 2, 512, D)
+    kt, vt = (torch.from_numpy(x).half().to(dev) for x in (k, v))
+    desc = _lib.Desc(1, 2, 2, 512, 512, D, 128, 128, 0, 0, BETA_STAR, math.sqrt(D))
+    kp, vp = torch.empty_like(kt), torch.empty_like(vt)
+    vmax = torch.zeros(2, dtype=torch.float32, device=dev)
+    _lib.check(L.pasa_b200_preprocess(C.byref(desc), kt.data_ptr(), vt.data_ptr(), kp.data_ptr(),
+                                      vp.data_ptr(), vmax.data_ptr(),
+                                      torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    diag, off = orc.shift_entries(128, BETA_STAR, math.sqrt(D), P16)
+    want = orc.preprocess_keys(k, 128, diag, off, lscale=LOG2E / 2, p_acc=PR1)
+    assert np.array_equal(kp.double().cpu().numpy(), want)
+    vm = np.abs(v).reshape(2, -1).max(axis=1)
+    assert np.array_equal(vmax.cpu().numpy(), vm.astype(np.float32))
+    for h in range(2):
+        c0 = int(orc.model_inflation(float(vm[h]), 512))
+        assert np.array_equal(vp[0, h].double().cpu().numpy(), orc.f16(v[0, h] * 2.0 ** -c0))
