@@ -41,11 +41,18 @@ using namespace sm100;
 #define PASA_PINGPONG 1
 #endif
 constexpr bool kPingPong = PASA_PINGPONG != 0;
-// One exp pair in kPolyEvery on the FMA-pipe polynomial (0: MUFU only).
+// One exp pair in kPolyEvery on the FMA-pipe polynomial (0: MUFU only).  d = 128
+// balances MUFU against issue slots at 4; at d = 64 the FMA pipe and the issue
+// slots are shared with twice the softmax work per FLOP and MUFU-only wins
+// (measured: tools/variants.py, +6 % at d = 64, -2 % at d = 128).
 #ifndef PASA_POLY_EVERY
 #define PASA_POLY_EVERY 4
 #endif
-constexpr int kPolyEvery = PASA_POLY_EVERY;
+#ifndef PASA_POLY_EVERY_D64
+#define PASA_POLY_EVERY_D64 0
+#endif
+template <int D>
+constexpr int kPolyEvery = D == 64 ? PASA_POLY_EVERY_D64 : PASA_POLY_EVERY;
 // setmaxnreg split of the per-CTA register pool (640 x 96 = 61440 at launch):
 // warpgroup 0 (TMA, MMA, 2 idle warps) drops to PASA_WG0_REGS, the four softmax
 // warpgroups rise to PASA_SM_REGS; 128 * WG0 + 512 * SM <= 61440.
@@ -172,7 +179,7 @@ __device__ __forceinline__ void row_max_sum(const uint32_t* s, int lim, int pbas
 // Pass 2: P = 2^(S' - c_j) in place (masked -> 0) and its FP32 sum, same
 // eight-chain order as pass 1.  Three pairs in four use MUFU ex2.approx.f16x2,
 // one the FMA-pipe polynomial (sm100.cuh); both are within 1 ulp of 2^x.
-template <bool DIAG, int NP, bool FMA>
+template <int D, bool DIAG, int NP, bool FMA>
 __device__ __forceinline__ float row_exp_sum(uint32_t* s, int lim, int pbase, uint32_t cj2,
                                              uint32_t scale2 = 0) {
   float acc[8];
@@ -193,7 +200,8 @@ __device__ __forceinline__ float row_exp_sum(uint32_t* s, int lim, int pbase, ui
     }
     // one pair in four on the FMA pipe, the rest on MUFU: balances MUFU time
     // (8 cycles / pair / SMSP) against issue slots (poly ~11 vs MUFU 3 per pair)
-    uint32_t pv = (kPolyEvery > 0 && (i % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1)
+    constexpr int PE = kPolyEvery<D>;
+    uint32_t pv = (PE > 0 && (i % (PE > 0 ? PE : 1)) == PE - 1)
                       ? ex2_poly_f16x2(x)
                       : ex2_f16x2(x);
     if (DIAG) pv &= col_keep(pbase + i, lim);
@@ -471,11 +479,11 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         if (tr) PASA_TR(t, j, 8);
         float lsum;
         if (MODE == kModeFa16 || fast2)
-          lsum = diag ? row_exp_sum<true, NP, true>(s, lim, NP * h, cj2, scale2)
-                      : row_exp_sum<false, NP, true>(s, lim, NP * h, cj2, scale2);
+          lsum = diag ? row_exp_sum<D, true, NP, true>(s, lim, NP * h, cj2, scale2)
+                      : row_exp_sum<D, false, NP, true>(s, lim, NP * h, cj2, scale2);
         else
-          lsum = diag ? row_exp_sum<true, NP, false>(s, lim, NP * h, cj2, scale2)
-                      : row_exp_sum<false, NP, false>(s, lim, NP * h, cj2, scale2);
+          lsum = diag ? row_exp_sum<D, true, NP, false>(s, lim, NP * h, cj2, scale2)
+                      : row_exp_sum<D, false, NP, false>(s, lim, NP * h, cj2, scale2);
         if (pingpong && ((t == 0 && j < nmin) || (t == 1 && j + 1 < nmin)))
           named_bar_arrive(2 - t, 512);
         PASA_STATE(j, 0, mloc);
