@@ -58,11 +58,20 @@ typedef struct pasa_b200_desc {
   double alpha;      /* static scale, must equal sqrt(d) (pasa.cpp:206-208)     */
 } pasa_b200_desc;
 
-/* Optional device-side counters, accumulated atomically (RunDiagnostics,
- * attention.hpp:30-48).  Pass NULL to skip. */
+/* RunDiagnostics (attention.hpp:30-48) accumulated on the device: the scores the
+ * tensor core stored (S' in PASA mode, S in the FP16 FA mode; masked entries
+ * excluded) -- finite min/max in the reference's units (S'/alpha-scaled, i.e. the
+ * kernel's log2(e)/2-scaled store divided back) and inf/NaN counts -- and the
+ * output counters.  A DEVICE pointer, reset with pasa_b200_diag_reset; pass NULL
+ * to skip (no cost).  Accumulates (merge semantics) across calls. */
 typedef struct pasa_b200_diag {
   unsigned long long out_nonfinite;
   unsigned long long out_total;
+  unsigned long long store_pos_inf;
+  unsigned long long store_neg_inf;
+  unsigned long long store_nan;
+  float store_finite_min; /* +inf when nothing finite was stored */
+  float store_finite_max; /* -inf when nothing finite was stored */
 } pasa_b200_diag;
 
 /* Library version (major*10000 + minor*100 + patch). */
@@ -136,6 +145,9 @@ PASA_B200_API int pasa_b200_attention_fwd_prepped(const pasa_b200_desc* desc, co
 PASA_B200_API int pasa_b200_flash_fp16_fwd(const pasa_b200_desc* desc, const void* q,
                                            const void* k, const void* v, void* o, void* stream);
 
+/* Reset a device pasa_b200_diag (counters 0, min +inf, max -inf), stream-ordered. */
+PASA_B200_API int pasa_b200_diag_reset(pasa_b200_diag* diag, void* stream);
+
 /* pasa_b200_attention_fwd from HOST buffers (binary16 bit patterns): copies
  * Q, K, V in, runs, copies O back and synchronizes.  The drop-in for a CPU
  * caller of pasa_attention (the reference's `sweep`, bench.cpp:224).  Device
@@ -143,6 +155,12 @@ PASA_B200_API int pasa_b200_flash_fp16_fwd(const pasa_b200_desc* desc, const voi
  * speed, pageable ones through the driver's staging path. */
 PASA_B200_API int pasa_b200_attention_host(const pasa_b200_desc* desc, const uint16_t* q, const uint16_t* k,
                              const uint16_t* v, uint16_t* o);
+
+/* pasa_b200_attention_host that also fills a HOST pasa_b200_diag (overwritten):
+ * the drop-in for pasa_attention(..., RunDiagnostics* diag) (pasa.cpp:244-291). */
+PASA_B200_API int pasa_b200_attention_host_diag(const pasa_b200_desc* desc, const uint16_t* q,
+                                                const uint16_t* k, const uint16_t* v, uint16_t* o,
+                                                pasa_b200_diag* diag);
 
 /* Device-side input generator: elements [start,
  * start + n) of tensor `tensor_id` (0 = Q, 1 = K, 2 = V) of the reference's

@@ -117,7 +117,7 @@ Matrix2D preprocess_keys(const Matrix2D& k_block, const Matrix2D& m,
 Tensor4D pasa_attention(const AttentionProblem& problem, const PasaParams& params,
                         const PrecisionPolicy& policy, const AttnOptions& opts,
                         RunDiagnostics* diag) {
-  // opts.threads is a CPU-loop knob; diagnose has no FP64 side channel here
+  // opts.threads is a CPU-loop knob; opts.diagnose's FP64 side channel is not offloaded
   if (params.s2 != problem.s2) throw std::invalid_argument("pasa: params.s2 does not match the problem");
   if (params.m.rows != params.s2 || params.m.cols != params.s2)
     throw std::invalid_argument("pasa: shifting matrix has the wrong shape");
@@ -138,18 +138,22 @@ Tensor4D pasa_attention(const AttentionProblem& problem, const PasaParams& param
                       params.beta, problem.alpha};
   std::vector<uint16_t> qh = to_half_bits(q), kh = to_half_bits(problem.k),
                         vh = to_half_bits(problem.v), oh(q.size());
-  const int rc = pasa_b200_attention_host(&desc, qh.data(), kh.data(), vh.data(), oh.data());
+  pasa_b200_diag dd{};
+  const int rc = diag ? pasa_b200_attention_host_diag(&desc, qh.data(), kh.data(), vh.data(),
+                                                      oh.data(), &dd)
+                      : pasa_b200_attention_host(&desc, qh.data(), kh.data(), vh.data(), oh.data());
   if (rc) rethrow_status(rc);
   Tensor4D out(q.batch, q.heads, q.seq, q.dim, policy.vector_prec);
-  uint64_t nonfinite = 0;
-  for (size_t i = 0; i < out.size(); ++i) {
-    out.data[i] = half_bits_to_double(oh[i]);
-    nonfinite += !std::isfinite(out.data[i]);
-  }
-  if (diag) {
+  for (size_t i = 0; i < out.size(); ++i) out.data[i] = half_bits_to_double(oh[i]);
+  if (diag) {  // the device's RunDiagnostics (store statistics + output counters)
     RunDiagnostics d;
-    d.out_total = out.size();
-    d.out_nonfinite = nonfinite;
+    d.store_finite_min = dd.store_finite_min;
+    d.store_finite_max = dd.store_finite_max;
+    d.store_pos_inf = dd.store_pos_inf;
+    d.store_neg_inf = dd.store_neg_inf;
+    d.store_nan = dd.store_nan;
+    d.out_total = dd.out_total;
+    d.out_nonfinite = dd.out_nonfinite;
     diag->merge(d);
   }
   return out;

@@ -272,9 +272,9 @@ class RefLib:
         L.ref_last_error.restype = C.c_char_p
         sz = C.c_size_t
         L.ref_pasa_attention.argtypes = [sz] * 7 + [_dp, _dp, _dp, C.c_double, C.c_int,
-                                                    C.c_int, C.c_int, _dp]
+                                                    C.c_int, C.c_int, _dp, C.c_void_p]
         L.ref_flash_attention.argtypes = [sz] * 7 + [_dp, _dp, _dp, C.c_int, C.c_int,
-                                                     C.c_int, _dp]
+                                                     C.c_int, _dp, C.c_void_p]
         L.ref_golden.argtypes = [sz] * 7 + [_dp, _dp, _dp, C.c_int, _dp]
         L.ref_generate.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, C.c_uint64,
                                    sz, sz, sz, sz, _dp, _dp, _dp]
@@ -306,18 +306,30 @@ class RefLib:
             raise ValueError("reference requires equal Q/K heads (tensor.cpp:24-26)")
         return B, H, S1, S2, d, pb.s1, pb.s2
 
-    def pasa(self, pb: Problem, beta: float = BETA_STAR, policy: int = PASA_FP16,
-             m_prec: int = P16, threads: int = 0):
-        o = np.empty(pb.q.shape)
-        self._check(self.lib.ref_pasa_attention(*self._dims(pb), _f64(pb.q), _f64(pb.k),
-                                                _f64(pb.v), beta, m_prec, policy, threads, o))
-        return o
+    DIAG_FIELDS = ("store_finite_min", "store_finite_max", "store_pos_inf", "store_neg_inf",
+                   "store_nan", "out_nonfinite", "out_total")
 
-    def flash(self, pb: Problem, policy: int = FA_PARTIAL_FP16, m0_zero=False, threads: int = 0):
+    def _diag(self, want):
+        return np.zeros(7) if want else None
+
+    def pasa(self, pb: Problem, beta: float = BETA_STAR, policy: int = PASA_FP16,
+             m_prec: int = P16, threads: int = 0, diag: bool = False):
+        """The reference's pasa_attention; with diag=True returns (O, RunDiagnostics dict)."""
         o = np.empty(pb.q.shape)
+        dg = self._diag(diag)
+        self._check(self.lib.ref_pasa_attention(*self._dims(pb), _f64(pb.q), _f64(pb.k),
+                                                _f64(pb.v), beta, m_prec, policy, threads, o,
+                                                dg.ctypes.data if diag else None))
+        return (o, dict(zip(self.DIAG_FIELDS, dg))) if diag else o
+
+    def flash(self, pb: Problem, policy: int = FA_PARTIAL_FP16, m0_zero=False, threads: int = 0,
+              diag: bool = False):
+        o = np.empty(pb.q.shape)
+        dg = self._diag(diag)
         self._check(self.lib.ref_flash_attention(*self._dims(pb), _f64(pb.q), _f64(pb.k),
-                                                 _f64(pb.v), policy, int(m0_zero), threads, o))
-        return o
+                                                 _f64(pb.v), policy, int(m0_zero), threads, o,
+                                                 dg.ctypes.data if diag else None))
+        return (o, dict(zip(self.DIAG_FIELDS, dg))) if diag else o
 
     def golden(self, pb: Problem, threads: int = 0):
         o = np.empty(pb.q.shape)

@@ -45,6 +45,19 @@ int guarded(F&& f) {
 
 pasa::PolicyId policy_from(int id) { return static_cast<pasa::PolicyId>(id); }
 
+// RunDiagnostics -> {store_finite_min, store_finite_max, store_pos_inf,
+// store_neg_inf, store_nan, out_nonfinite, out_total} (nullable destination).
+void put_diag(const pasa::RunDiagnostics& d, double* out7) {
+  if (!out7) return;
+  out7[0] = d.store_finite_min;
+  out7[1] = d.store_finite_max;
+  out7[2] = static_cast<double>(d.store_pos_inf);
+  out7[3] = static_cast<double>(d.store_neg_inf);
+  out7[4] = static_cast<double>(d.store_nan);
+  out7[5] = static_cast<double>(d.out_nonfinite);
+  out7[6] = static_cast<double>(d.out_total);
+}
+
 }  // namespace
 
 extern "C" {
@@ -56,7 +69,7 @@ const char* ref_last_error() { return g_err.c_str(); }
 int ref_pasa_attention(size_t B, size_t H, size_t S1, size_t S2, size_t d,
                        size_t s1, size_t s2, const double* q, const double* k,
                        const double* v, double beta, int m_prec, int policy,
-                       int threads, double* out) {
+                       int threads, double* out, double* diag7) {
   return guarded([&] {
     auto prob = pasa::make_problem(to_tensor(q, B, H, S1, d),
                                    to_tensor(k, B, H, S2, d),
@@ -65,16 +78,18 @@ int ref_pasa_attention(size_t B, size_t H, size_t S1, size_t S2, size_t d,
                                          static_cast<pasa::Prec>(m_prec));
     pasa::AttnOptions opts;
     opts.threads = threads;
-    auto o = pasa::pasa_attention(prob, params,
-                                  pasa::policy_for(policy_from(policy)), opts);
+    pasa::RunDiagnostics diag;
+    auto o = pasa::pasa_attention(prob, params, pasa::policy_for(policy_from(policy)), opts,
+                                  diag7 ? &diag : nullptr);
     std::memcpy(out, o.data.data(), o.size() * sizeof(double));
+    put_diag(diag, diag7);
   });
 }
 
 int ref_flash_attention(size_t B, size_t H, size_t S1, size_t S2, size_t d,
                         size_t s1, size_t s2, const double* q, const double* k,
                         const double* v, int policy, int m0_zero, int threads,
-                        double* out) {
+                        double* out, double* diag7) {
   return guarded([&] {
     auto prob = pasa::make_problem(to_tensor(q, B, H, S1, d),
                                    to_tensor(k, B, H, S2, d),
@@ -82,9 +97,11 @@ int ref_flash_attention(size_t B, size_t H, size_t S1, size_t S2, size_t d,
     pasa::AttnOptions opts;
     opts.threads = threads;
     opts.m0 = m0_zero ? pasa::M0Mode::Zero : pasa::M0Mode::NegInf;
-    auto o = pasa::flash_attention(prob, pasa::policy_for(policy_from(policy)),
-                                   opts);
+    pasa::RunDiagnostics diag;
+    auto o = pasa::flash_attention(prob, pasa::policy_for(policy_from(policy)), opts,
+                                   diag7 ? &diag : nullptr);
     std::memcpy(out, o.data.data(), o.size() * sizeof(double));
+    put_diag(diag, diag7);
   });
 }
 

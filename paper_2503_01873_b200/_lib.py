@@ -34,6 +34,17 @@ class Diag(C.Structure):
 _LIB = None
 
 
+class Diag(C.Structure):
+    """Mirror of ``pasa_b200_diag`` (device-side RunDiagnostics)."""
+
+    _fields_ = [
+        ("out_nonfinite", C.c_ulonglong), ("out_total", C.c_ulonglong),
+        ("store_pos_inf", C.c_ulonglong), ("store_neg_inf", C.c_ulonglong),
+        ("store_nan", C.c_ulonglong), ("store_finite_min", C.c_float),
+        ("store_finite_max", C.c_float),
+    ]
+
+
 def exported_symbols_from_header() -> list[str]:
     """Every function the public header declares."""
     text = open(HEADER).read()
@@ -64,6 +75,8 @@ def load(path: str = SO) -> C.CDLL:
     L.pasa_b200_attention_host.argtypes = [dp, vp, vp, vp, vp]
     L.pasa_b200_flash_fp16_fwd.argtypes = [dp, vp, vp, vp, vp, vp]
     L.pasa_b200_preprocess_keys_host.argtypes = [dp, vp, vp, C.c_double, C.c_double]
+    L.pasa_b200_diag_reset.argtypes = [vp, vp]
+    L.pasa_b200_attention_host_diag.argtypes = [dp, vp, vp, vp, vp, C.POINTER(Diag)]
     u64, i32, f64 = C.c_uint64, C.c_int32, C.c_double
     L.pasa_b200_generate.argtypes = [i32, f64, f64, f64, u64, u64, u64, u64, vp, vp]
     L.pasa_b200_generate_resonance.argtypes = [u64, i32, i32, i32, i32, i32, f64, f64, vp, vp]

@@ -89,7 +89,8 @@ class AttnOptions:
 
 @dataclass
 class RunDiagnostics:
-    """attention.hpp:30-48 (the output counters are filled)."""
+    """attention.hpp:30-48: store statistics (the scores the tensor core stored, in the
+    reference's units) and output counters, filled by the device; no FP64 side channel."""
 
     store_finite_min: float = math.inf
     store_finite_max: float = -math.inf
@@ -99,6 +100,13 @@ class RunDiagnostics:
     out_nonfinite: int = 0
     out_total: int = 0
     has_fp64_ranges: bool = False
+
+    @staticmethod
+    def from_c(d: "_lib.Diag") -> "RunDiagnostics":
+        """From the C-ABI's pasa_b200_diag (device RunDiagnostics, copied to the host)."""
+        return RunDiagnostics(float(d.store_finite_min), float(d.store_finite_max),
+                              int(d.store_pos_inf), int(d.store_neg_inf), int(d.store_nan),
+                              int(d.out_nonfinite), int(d.out_total))
 
     def merge(self, o: "RunDiagnostics") -> None:
         self.store_finite_min = min(self.store_finite_min, o.store_finite_min)
@@ -235,8 +243,11 @@ def workspace_for(desc: _lib.Desc, device: torch.device) -> torch.Tensor:
 def pasa_attention_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, beta: float = BETA_STAR,
                        causal: bool = False, s1: int = 128, s2: int = 128,
                        out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
-                       stream: torch.cuda.Stream | None = None) -> torch.Tensor:
-    """Device entry point: fp16 CUDA tensors (BHSD), asynchronous on ``stream``."""
+                       stream: torch.cuda.Stream | None = None,
+                       diag: "RunDiagnostics | None" = None) -> torch.Tensor:
+    """Device entry point: fp16 CUDA tensors (BHSD), asynchronous on ``stream``.
+    ``diag`` (optional) is merged with the device RunDiagnostics of this call (the
+    diagnostic kernel instantiation; synchronises the stream)."""
     L = _lib.load()
     if not (q.is_cuda and k.is_cuda and v.is_cuda):
         raise ValueError("pasa_attention_fwd expects CUDA tensors; use pasa_attention for host data")
@@ -248,9 +259,17 @@ def pasa_attention_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, beta: 
     if workspace is None:
         workspace = workspace_for(desc, q.device)
     st = (stream or torch.cuda.current_stream(q.device)).cuda_stream
+    dbuf = None
+    if diag is not None:
+        dbuf = torch.empty(C.sizeof(_lib.Diag), dtype=torch.uint8, device=q.device)
+        _lib.check(L.pasa_b200_diag_reset(dbuf.data_ptr(), st))
     _lib.check(L.pasa_b200_attention_fwd(C.byref(desc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                          out.data_ptr(), workspace.data_ptr(), workspace.numel(),
-                                         None, st))
+                                         dbuf.data_ptr() if dbuf is not None else None, st))
+    if dbuf is not None:
+        torch.cuda.current_stream(q.device).synchronize() if stream is None else stream.synchronize()
+        host = _lib.Diag.from_buffer_copy(bytes(dbuf.cpu().numpy()))
+        diag.merge(RunDiagnostics.from_c(host))
     return out
 
 
@@ -273,9 +292,11 @@ def flash_fp16_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: bo
 
 
 def flash_attention(problem: AttentionProblem, policy: PrecisionPolicy | PolicyId,
-                    opts: AttnOptions | None = None) -> torch.Tensor:
+                    opts: AttnOptions | None = None,
+                    diag: RunDiagnostics | None = None) -> torch.Tensor:
     """attention.hpp:57-60 on the B200: the FA_PARTIAL_FP16 policy only (the
-    reference's partial-FP16 FlashAttention); FP64/FP32 policies are CPU-oracle features."""
+    reference's partial-FP16 FlashAttention); FP64/FP32 policies are CPU-oracle features.
+    ``diag`` gets the stored-score statistics and output counters (attention.cpp:125)."""
     opts = opts or AttnOptions()
     pol = policy if isinstance(policy, PrecisionPolicy) else policy_for(policy)
     if (pol.gemm_accum, pol.gemm_store, pol.vector_prec) != (Prec.FP32, Prec.FP16, Prec.FP16):
@@ -285,6 +306,8 @@ def flash_attention(problem: AttentionProblem, policy: PrecisionPolicy | PolicyI
     q, k, v = problem.q, problem.k, problem.v
     if not q.is_cuda:
         raise ValueError("flash_attention on B200 expects CUDA tensors")
+    if diag is not None:  # beta = 0 through the diagnostic instantiation
+        return pasa_attention_fwd(q, k, v, 0.0, opts.causal, problem.s1, problem.s2, diag=diag)
     return flash_fp16_fwd(q, k, v, opts.causal, problem.s1, problem.s2)
 
 
@@ -321,21 +344,26 @@ def pasa_attention(problem: AttentionProblem, params: PasaParams,
     if params.beta == 1.0:
         raise ValueError("pasa: beta == 1 has no recovery")
     if params.beta == 0.0:  # degrades to the blocked FP16 attention (pasa.cpp:212-221)
-        return flash_attention(problem, pol, opts)
+        return flash_attention(problem, pol, opts, diag)
     if pol.id != PolicyId.PASA_FP16:
         raise ValueError(f"pasa_attention on B200 implements PASA_FP16 only, got {pol.id.name}")
     q, k, v = problem.q, problem.k, problem.v
     if q.is_cuda:
-        out = pasa_attention_fwd(q, k, v, params.beta, opts.causal, problem.s1, problem.s2)
+        out = pasa_attention_fwd(q, k, v, params.beta, opts.causal, problem.s1, problem.s2,
+                                 diag=diag)
     else:
         L = _lib.load()
         desc = _desc(q, k, problem.s1, problem.s2, params.beta, problem.alpha, opts.causal)
         out = torch.empty_like(q)
         qn, kn, vn = (t.contiguous().view(torch.int16) for t in (q, k, v))
-        _lib.check(L.pasa_b200_attention_host(C.byref(desc), qn.data_ptr(), kn.data_ptr(),
-                                              vn.data_ptr(), out.view(torch.int16).data_ptr()))
-    if diag is not None:
-        d = RunDiagnostics(out_total=out.numel(),
-                           out_nonfinite=int((~torch.isfinite(out)).sum().item()))
-        diag.merge(d)
+        if diag is None:
+            _lib.check(L.pasa_b200_attention_host(C.byref(desc), qn.data_ptr(), kn.data_ptr(),
+                                                  vn.data_ptr(), out.view(torch.int16).data_ptr()))
+        else:
+            hd = _lib.Diag()
+            _lib.check(L.pasa_b200_attention_host_diag(C.byref(desc), qn.data_ptr(), kn.data_ptr(),
+                                                       vn.data_ptr(),
+                                                       out.view(torch.int16).data_ptr(),
+                                                       C.byref(hd)))
+            diag.merge(RunDiagnostics.from_c(hd))
     return out

@@ -242,7 +242,8 @@ int pasa_b200_preprocess(const pasa_b200_desc* d, const void* k, const void* v, 
 }
 
 static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, const void* keys,
-                          const void* v, const float* vmax, void* o, void* stream) {
+                          const void* v, const float* vmax, void* o, void* stream,
+                          pasa_b200_diag* diag = nullptr) {
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(keys) |
        reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(o)) & 15)
     return fail(PASA_B200_EINVAL, "attention_fwd: tensors must be 16-byte aligned");
@@ -268,6 +269,8 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
   p.vmax = vmax;
   p.out = static_cast<uint16_t*>(o);
   p.trace = g_trace;
+  p.diag = diag;
+  p.diag_scale = mode == kModePasa ? static_cast<float>(2.0 / kLog2e) : 1.0f;
   cudaError_t e = launch_fwd(d->head_dim, d->causal != 0, mode, tq, tk, tv, p,
                              static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "pasa_fwd launch");
@@ -305,20 +308,50 @@ int pasa_b200_attention_fwd(const pasa_b200_desc* d, const void* q, const void* 
     return fail(PASA_B200_EINVAL, "attention_fwd: NULL tensor or workspace");
   if (workspace_bytes < pasa_b200_workspace_size(d))
     return fail(PASA_B200_EINVAL, "attention_fwd: workspace too small");
-  (void)diag;
   // beta == 0 degrades to the blocked FP16 attention (pasa.cpp:212-221)
-  if (d->beta == 0.0) return launch_forward(d, kModeFa16, q, k, v, nullptr, o, stream);
+  if (d->beta == 0.0) return launch_forward(d, kModeFa16, q, k, v, nullptr, o, stream, diag);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   void* kp = ws;
   void* vp = ws + align_up(kp_bytes(d), 256);
   float* vmax = reinterpret_cast<float*>(ws + 2 * align_up(kp_bytes(d), 256));
   rc = pasa_b200_preprocess(d, k, v, kp, vp, vmax, stream);
   if (rc) return rc;
-  return pasa_b200_attention_fwd_prepped(d, q, kp, vp, vmax, o, stream);
+  if (!diag) return pasa_b200_attention_fwd_prepped(d, q, kp, vp, vmax, o, stream);
+  return launch_forward(d, kModePasa, q, kp, vp, vmax, o, stream, diag);
 }
+
+__global__ void diag_reset_kernel(pasa_b200_diag* g) {
+  *g = pasa_b200_diag{0ull, 0ull, 0ull, 0ull, 0ull, __int_as_float(0x7f800000),
+                      __int_as_float(0xff800000)};
+}
+
+int pasa_b200_diag_reset(pasa_b200_diag* diag, void* stream) {
+  g_last_error.clear();
+  if (!diag) return fail(PASA_B200_EINVAL, "diag_reset: NULL");
+  diag_reset_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(diag);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : cuda_fail(e, "diag_reset");
+}
+
+static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const uint16_t* k,
+                               const uint16_t* v, uint16_t* o, pasa_b200_diag* hdiag);
 
 int pasa_b200_attention_host(const pasa_b200_desc* d, const uint16_t* q, const uint16_t* k,
                              const uint16_t* v, uint16_t* o) {
+  return attention_host_impl(d, q, k, v, o, nullptr);
+}
+
+int pasa_b200_attention_host_diag(const pasa_b200_desc* d, const uint16_t* q, const uint16_t* k,
+                                  const uint16_t* v, uint16_t* o, pasa_b200_diag* diag) {
+  if (!diag) {
+    g_last_error.clear();
+    return fail(PASA_B200_EINVAL, "attention_host_diag: NULL diag");
+  }
+  return attention_host_impl(d, q, k, v, o, diag);
+}
+
+static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const uint16_t* k,
+                               const uint16_t* v, uint16_t* o, pasa_b200_diag* hdiag) {
   g_last_error.clear();
   int rc = check_desc(d);
   if (rc) return rc;
@@ -336,7 +369,7 @@ int pasa_b200_attention_host(const pasa_b200_desc* d, const uint16_t* q, const u
   const size_t nq = static_cast<size_t>(d->batch) * d->heads_q * d->seq_q * d->head_dim * 2;
   const size_t nk = kp_bytes(d);
   const size_t ws = pasa_b200_workspace_size(d);
-  const size_t total = 2 * align_up(nq, 256) + 2 * align_up(nk, 256) + ws;
+  const size_t total = 2 * align_up(nq, 256) + 2 * align_up(nk, 256) + ws + 256;
   cudaError_t e = cudaSuccess;
   if (cache.dev != dev || cache.bytes < total) {
     if (cache.buf) cudaFree(cache.buf);
@@ -354,14 +387,18 @@ int pasa_b200_attention_host(const pasa_b200_desc* d, const uint16_t* q, const u
   uint8_t* dv = dk + align_up(nk, 256);
   uint8_t* dout = dv + align_up(nk, 256);
   uint8_t* dws = dout + align_up(nq, 256);
+  pasa_b200_diag* ddiag = reinterpret_cast<pasa_b200_diag*>(dws + align_up(ws, 256));
   cudaStream_t st = cache.stream;
   e = cudaMemcpyAsync(dq, q, nq, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(dk, k, nk, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(dv, v, nk, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-  rc = pasa_b200_attention_fwd(d, dq, dk, dv, dout, dws, ws, nullptr, st);
+  if (hdiag && (rc = pasa_b200_diag_reset(ddiag, st))) return rc;
+  rc = pasa_b200_attention_fwd(d, dq, dk, dv, dout, dws, ws, hdiag ? ddiag : nullptr, st);
   if (rc) return rc;
   e = cudaMemcpyAsync(o, dout, nq, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess && hdiag)
+    e = cudaMemcpyAsync(hdiag, ddiag, sizeof(pasa_b200_diag), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "D2H copy / kernel");
   return PASA_B200_OK;

@@ -110,7 +110,9 @@ struct FwdCfg {
   static constexpr int HALVES = 2;  // threads per row: each owns 64 S' columns, D/2 outputs
   static constexpr int SMEM_XCH = SMEM_BAR + NUM_BARS * 8 + 16;  // row max/sum exchange
   static constexpr int XCH_BYTES = 2 * NT * HALVES * kTile * 8;  // [j&1][t][half][row] float2
-  static constexpr int SMEM_BYTES = SMEM_XCH + XCH_BYTES + 1024;
+  static constexpr int SMEM_DIAG = SMEM_XCH + XCH_BYTES;  // RunDiagnostics: 5 words / thread
+  static constexpr int DIAG_BYTES = NT * HALVES * 128 * 5 * 4;
+  static constexpr int SMEM_BYTES = SMEM_DIAG + DIAG_BYTES + 1024;
   static constexpr int THREADS = 128 + NT * HALVES * 128;  // WG0: TMA, MMA, 2 idle; 4 softmax WGs
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t TMEM_TILE = 256;               // S/P at +0, T at +128
@@ -213,9 +215,48 @@ __device__ __forceinline__ float row_exp_sum(uint32_t* s, int lim, int pbase, ui
                    __fadd_rn(__fadd_rn(acc[4], acc[5]), __fadd_rn(acc[6], acc[7])));
 }
 
+// RunDiagnostics (attention.cpp:25-36, track_store) over this thread's stored
+// scores of one block (masked columns excluded), merged into its shared-memory slot
+// {finite min, finite max, +inf, -inf, NaN}.  Diagnostic mode only.
+template <int NP>
+__device__ __forceinline__ void track_store_block(const uint32_t* s, int lim, int pbase, bool masked,
+                                               float* slot) {
+  float mn = slot[0], mx = slot[1];
+  uint32_t pinf = __float_as_uint(slot[2]), ninf = __float_as_uint(slot[3]),
+           nan = __float_as_uint(slot[4]);
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      if (masked && 2 * (pbase + i) + half >= lim) continue;
+      const float v = half ? hi_f(s[i]) : lo_f(s[i]);
+      if (isnan(v)) ++nan;
+      else if (isinf(v)) (v > 0.f ? ++pinf : ++ninf);
+      else { mn = fminf(mn, v); mx = fmaxf(mx, v); }
+    }
+  }
+  slot[0] = mn; slot[1] = mx;
+  slot[2] = __uint_as_float(pinf); slot[3] = __uint_as_float(ninf); slot[4] = __uint_as_float(nan);
+}
+
+__device__ __forceinline__ void atomic_min_f(float* a, float v) {
+  if (v >= 0.f) atomicMin(reinterpret_cast<int*>(a), __float_as_int(v));
+  else atomicMax(reinterpret_cast<unsigned*>(a), __float_as_uint(v));
+}
+__device__ __forceinline__ void atomic_max_f(float* a, float v) {
+  if (v >= 0.f) atomicMax(reinterpret_cast<int*>(a), __float_as_int(v));
+  else atomicMin(reinterpret_cast<unsigned*>(a), __float_as_uint(v));
+}
+
+// Device-side RunDiagnostics accumulator (the layout of pasa_b200_diag).
+struct DiagAccum {
+  unsigned long long out_nonfinite, out_total, store_pos_inf, store_neg_inf, store_nan;
+  float store_finite_min, store_finite_max;
+};
+
 }  // namespace
 
-template <int D, bool CAUSAL, int MODE>
+template <int D, bool CAUSAL, int MODE, bool DIAGNOSE>
 __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     pasa_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_kp,
@@ -404,6 +445,12 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       return xch + ((parity * NT + t) * Cfg::HALVES + half) * kTile + row;
     };
     const uint32_t xbar = 3 + t * 4 + quad;  // named barrier of this row quadrant's two warps
+    float* dslot = reinterpret_cast<float*>(smem + Cfg::SMEM_DIAG) + (threadIdx.x - 128) * 5;
+    if (DIAGNOSE) {
+      dslot[0] = __int_as_float(0x7f800000);  // +inf
+      dslot[1] = __int_as_float(0xff800000);  // -inf
+      dslot[2] = dslot[3] = dslot[4] = 0.f;
+    }
     if (ti.nblk > 0) {
       // O-bounding exponent: V arrives pre-scaled by 2^-c0; the
       // epilogue multiplies by 2^c0.
@@ -433,6 +480,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         const bool cdiag = CAUSAL && (j == ti.nblk - 1);
         const bool diag = cdiag || p.s2 < kTile;
         const int lim = cdiag ? row + 1 : p.s2;
+        if (DIAGNOSE) track_store_block<NP>(s, lim, NP * h, diag, dslot);
         constexpr bool kSum = MODE == kModePasa;
         float mh, sh = 0.f;
         if (diag) row_max_sum<true, NP, kSum>(s, lim, NP * h, mh, sh);
@@ -545,6 +593,36 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         }
         if (row_ok) *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(w[0], w[1], w[2], w[3]);
       }
+      if (DIAGNOSE) {  // out_nonfinite / out_total (pasa.cpp:275-286) and the store stats
+        DiagAccum* g = static_cast<DiagAccum*>(p.diag);
+        unsigned nf = 0;
+#pragma unroll
+        for (int i = 0; i < D / 4; ++i) {
+          const float a = __fmul_rn(lo_f(o[i]), inv_l), c = __fmul_rn(hi_f(o[i]), inv_l);
+          nf += !isfinite(__half2float(__float2half_rn(a))) + !isfinite(__half2float(__float2half_rn(c)));
+        }
+        unsigned long long cnt[5] = {row_ok ? nf : 0u, row_ok ? unsigned(D / 2) : 0u,
+                                     __float_as_uint(dslot[2]), __float_as_uint(dslot[3]),
+                                     __float_as_uint(dslot[4])};
+        float mn = __fmul_rn(dslot[0], p.diag_scale), mx = __fmul_rn(dslot[1], p.diag_scale);
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) {
+#pragma unroll
+          for (int k = 0; k < 5; ++k) cnt[k] += __shfl_xor_sync(0xffffffffu, cnt[k], o2);
+          mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o2));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o2));
+        }
+        if (lane == 0) {
+          unsigned long long* c = &g->out_nonfinite;
+#pragma unroll
+          for (int k = 0; k < 5; ++k)
+            if (cnt[k]) atomicAdd(c + k, cnt[k]);
+          if (mn <= mx) {
+            atomic_min_f(&g->store_finite_min, mn);
+            atomic_max_f(&g->store_finite_max, mx);
+          }
+        }
+      }
     }
   }
   tc_fence_before();
@@ -558,7 +636,9 @@ template <int D, bool CAUSAL, int MODE>
 cudaError_t launch_fwd_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                          const FwdParams& p, cudaStream_t stream) {
   using Cfg = FwdCfg<D>;
-  auto kern = pasa_fwd_kernel<D, CAUSAL, MODE>;
+  // RunDiagnostics is a separate instantiation so the production kernel's schedule is
+  // untouched by the diagnostic code.
+  auto kern = p.diag ? pasa_fwd_kernel<D, CAUSAL, MODE, true> : pasa_fwd_kernel<D, CAUSAL, MODE, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        Cfg::SMEM_BYTES);
   if (e != cudaSuccess) return e;

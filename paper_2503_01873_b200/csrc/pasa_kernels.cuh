@@ -58,6 +58,8 @@ struct FwdParams {
   float qk_scale;         // FA16 mode only: log2(e) / alpha applied after the FP16 store
   const float* vmax;      // per (b, kv head), from the pre-pass (PASA mode: V is pre-scaled)
   uint16_t* out;          // (B, Hq, S1, D) fp16
+  void* diag;             // optional device pasa_b200_diag (RunDiagnostics); nullptr = off
+  float diag_scale;       // stored score -> reference units (PASA: 2/log2(e); FA16: 1)
   long long* trace;       // PASA_TRACE builds only: clock64 timeline (see pasa_fwd.cu)
 };
 
