@@ -106,7 +106,7 @@ struct FwdCfg {
   static constexpr int SMEM_K = SMEM_Q + NT * TILE_BYTES;
   static constexpr int SMEM_V = SMEM_K + KS * TILE_BYTES;
   static constexpr int SMEM_BAR = SMEM_V + VS * TILE_BYTES;
-  static constexpr int NUM_BARS = NT + 2 * KS + 2 * VS + 4 * NT;
+  static constexpr int NUM_BARS = NT + 2 * KS + 2 * VS + 5 * NT;
   static constexpr int HALVES = 2;  // threads per row: each owns 64 S' columns, D/2 outputs
   static constexpr int SMEM_XCH = SMEM_BAR + NUM_BARS * 8 + 16;  // row max/sum exchange
   static constexpr int XCH_BYTES = 2 * NT * HALVES * kTile * 8;  // [j&1][t][half][row] float2
@@ -181,14 +181,11 @@ __device__ __forceinline__ void row_max_sum(const uint32_t* s, int lim, int pbas
 // Pass 2: P = 2^(S' - c_j) in place (masked -> 0) and its FP32 sum, same
 // eight-chain order as pass 1.  Three pairs in four use MUFU ex2.approx.f16x2,
 // one the FMA-pipe polynomial (sm100.cuh); both are within 1 ulp of 2^x.
-template <int D, bool DIAG, int NP, bool FMA>
-__device__ __forceinline__ float row_exp_sum(uint32_t* s, int lim, int pbase, uint32_t cj2,
-                                             uint32_t scale2 = 0) {
-  float acc[8];
+template <int D, bool DIAG, int I0, int I1, bool FMA>
+__device__ __forceinline__ void row_exp_range(uint32_t* s, int lim, int pbase, uint32_t cj2,
+                                              uint32_t scale2, float* acc) {
 #pragma unroll
-  for (int k = 0; k < 8; ++k) acc[k] = 0.f;
-#pragma unroll
-  for (int i = 0; i < NP; ++i) {
+  for (int i = I0; i < I1; ++i) {
     // FMA form: x = fl16(S * scale - c) in one HFMA2 -- FA16: scale = log2e/alpha,
     // c = m*scale; PASA: scale = 2, c = 2 c_j (scores are stored in units of
     // log2(e)/2, so the FP16 store holds 0.72x the reference's scores).
@@ -211,6 +208,19 @@ __device__ __forceinline__ float row_exp_sum(uint32_t* s, int lim, int pbase, ui
     acc[2 * (i & 3) + 1] = add_hi_f16(acc[2 * (i & 3) + 1], pv);
     s[i] = pv;
   }
+}
+
+// Pass 2 over a half row in two halves: mid() runs after pairs [0, NP/2) are done
+// (the caller stores them to TMEM so the PV MMA can start on those keys).
+template <int D, bool DIAG, int NP, bool FMA, class Mid>
+__device__ __forceinline__ float row_exp_sum(uint32_t* s, int lim, int pbase, uint32_t cj2,
+                                             uint32_t scale2, Mid&& mid) {
+  float acc[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+  row_exp_range<D, DIAG, 0, NP / 2, FMA>(s, lim, pbase, cj2, scale2, acc);
+  mid();
+  row_exp_range<D, DIAG, NP / 2, NP, FMA>(s, lim, pbase, cj2, scale2, acc);
   return __fadd_rn(__fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3])),
                    __fadd_rn(__fadd_rn(acc[4], acc[5]), __fadd_rn(acc[6], acc[7])));
 }
@@ -276,6 +286,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
   uint64_t* p_full = s_full + NT;
   uint64_t* t_full = p_full + NT;
   uint64_t* t_empty = t_full + NT;
+  uint64_t* p_half = t_empty + NT;  // P of keys {0-31, 64-95} stored (first half of pass 2)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
 
   const int warp = static_cast<int>(warp_id());
@@ -299,6 +310,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       mbar_init(&q_full[t], 1);
       mbar_init(&s_full[t], 1);
       mbar_init(&p_full[t], 4 * Cfg::HALVES);
+      mbar_init(&p_half[t], 4 * Cfg::HALVES);
       mbar_init(&t_full[t], 1);
       mbar_init(&t_empty[t], 4 * Cfg::HALVES);
     }
@@ -373,14 +385,18 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
                   kIdS, s > 0);
         }
       };
-      auto issue_pv = [&](int t, int vs) {
+      // PV in two parts: K-steps {0,1,4,5} (keys whose P the first half of pass 2 stored)
+      // as soon as p_half arrives, {2,3,6,7} after p_full.
+      auto issue_pv = [&](int t, int vs, int part) {
         const uint32_t d_tmem = tmem_base + t * Cfg::TMEM_TILE + 128;
         const uint32_t a_tmem = tmem_base + t * Cfg::TMEM_TILE;
         const uint32_t va = smem_u32(smem + Cfg::SMEM_V + vs * Cfg::TILE_BYTES);
 #pragma unroll
-        for (int s = 0; s < kTile / 16; ++s)
+        for (int k = 0; k < 4; ++k) {
+          const int s = (k & 1) + 4 * (k >> 1) + 2 * part;
           umma_ts(d_tmem, a_tmem + s * 8, smem_desc_sw128(va + s * 2048, Cfg::BOX_BYTES, 1024),
-                  kIdPV, s > 0);
+                  kIdPV, part > 0 || k > 0);
+        }
       };
       for (int t = 0; t < NT; ++t)
         if (tl[t].valid) mbar_wait(&q_full[t], 0);
@@ -401,11 +417,14 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         for (int t = 0; t < NT; ++t) {
           if (j >= tl[t].nblk) continue;
           PASA_TR(2, j, 4 * t + 0);
-          mbar_wait(&p_full[t], j & 1);
+          mbar_wait(&p_half[t], j & 1);
           PASA_TR(2, j, 4 * t + 1);
           mbar_wait(&t_empty[t], (j & 1) ^ 1);
           tc_fence_after();
-          issue_pv(t, vs);
+          issue_pv(t, vs, 0);
+          mbar_wait(&p_full[t], j & 1);
+          tc_fence_after();
+          issue_pv(t, vs, 1);
           PASA_TR(2, j, 4 * t + 2);
           tc_commit(&t_full[t]);
           if (j + 1 < tl[t].nblk) {
@@ -525,13 +544,22 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         // turns go T0(0), T1(0), T0(1), T1(1), ... while both tiles have blocks.
         if (pingpong && j < nmin && (t == 1 || j > 0)) named_bar_sync(1 + t, 512);
         if (tr) PASA_TR(t, j, 8);
+        // P packed two per column: this half's 32 pairs -> columns [32h, 32h + 32); the
+        // first 16 pairs are stored mid-pass so the PV MMA starts on them (p_half).
+        auto mid = [&]() {
+          tmem_st_16cols_b32(t_s + NP * h, s);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_half[t]);
+        };
         float lsum;
         if (MODE == kModeFa16 || fast2)
-          lsum = diag ? row_exp_sum<D, true, NP, true>(s, lim, NP * h, cj2, scale2)
-                      : row_exp_sum<D, false, NP, true>(s, lim, NP * h, cj2, scale2);
+          lsum = diag ? row_exp_sum<D, true, NP, true>(s, lim, NP * h, cj2, scale2, mid)
+                      : row_exp_sum<D, false, NP, true>(s, lim, NP * h, cj2, scale2, mid);
         else
-          lsum = diag ? row_exp_sum<D, true, NP, false>(s, lim, NP * h, cj2, scale2)
-                      : row_exp_sum<D, false, NP, false>(s, lim, NP * h, cj2, scale2);
+          lsum = diag ? row_exp_sum<D, true, NP, false>(s, lim, NP * h, cj2, scale2, mid)
+                      : row_exp_sum<D, false, NP, false>(s, lim, NP * h, cj2, scale2, mid);
         if (pingpong && ((t == 0 && j < nmin) || (t == 1 && j + 1 < nmin)))
           named_bar_arrive(2 - t, 512);
         PASA_STATE(j, 0, mloc);
@@ -542,8 +570,6 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         PASA_STATE(j, 5, ep);
         PASA_STATE(j, 6, lsum);
         if (tr) PASA_TR(t, j, 7);
-        // P packed two per column: this half's 32 pairs -> columns [32h, 32h + 32)
-        tmem_st_16cols_b32(t_s + NP * h, s);
         tmem_st_16cols_b32(t_s + NP * h + 16, s + 16);
         tmem_wait_st();
         tc_fence_before();
