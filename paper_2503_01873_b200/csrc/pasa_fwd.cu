@@ -53,6 +53,19 @@ constexpr bool kPingPong = PASA_PINGPONG != 0;
 #endif
 template <int D>
 constexpr int kPolyEvery = D == 64 ? PASA_POLY_EVERY_D64 : PASA_POLY_EVERY;
+// Pass 2 stores P in kPParts parts, each released to the PV MMA on its own mbarrier,
+// so the tensor core starts PV on a part while the exp of the next part runs
+// (measured, tools/variants.py: d = 128 best at 4 parts, d = 64 at 2).
+#ifndef PASA_PPARTS
+#define PASA_PPARTS 4
+#endif
+#ifndef PASA_PPARTS_D64
+#define PASA_PPARTS_D64 2
+#endif
+template <int D>
+constexpr int kPParts = D == 64 ? PASA_PPARTS_D64 : PASA_PPARTS;
+static_assert(PASA_PPARTS == 1 || PASA_PPARTS == 2 || PASA_PPARTS == 4, "P parts");
+static_assert(PASA_PPARTS_D64 == 1 || PASA_PPARTS_D64 == 2 || PASA_PPARTS_D64 == 4, "P parts");
 // setmaxnreg split of the per-CTA register pool (640 x 96 = 61440 at launch):
 // warpgroup 0 (TMA, MMA, 2 idle warps) drops to PASA_WG0_REGS, the four softmax
 // warpgroups rise to PASA_SM_REGS; 128 * WG0 + 512 * SM <= 61440.
@@ -106,7 +119,7 @@ struct FwdCfg {
   static constexpr int SMEM_K = SMEM_Q + NT * TILE_BYTES;
   static constexpr int SMEM_V = SMEM_K + KS * TILE_BYTES;
   static constexpr int SMEM_BAR = SMEM_V + VS * TILE_BYTES;
-  static constexpr int NUM_BARS = NT + 2 * KS + 2 * VS + 5 * NT;
+  static constexpr int NUM_BARS = NT + 2 * KS + 2 * VS + (3 + kPParts<D>) * NT;
   static constexpr int HALVES = 2;  // threads per row: each owns 64 S' columns, D/2 outputs
   static constexpr int SMEM_XCH = SMEM_BAR + NUM_BARS * 8 + 16;  // row max/sum exchange
   static constexpr int XCH_BYTES = 2 * NT * HALVES * kTile * 8;  // [j&1][t][half][row] float2
@@ -210,17 +223,25 @@ __device__ __forceinline__ void row_exp_range(uint32_t* s, int lim, int pbase, u
   }
 }
 
-// Pass 2 over a half row in two halves: mid() runs after pairs [0, NP/2) are done
-// (the caller stores them to TMEM so the PV MMA can start on those keys).
-template <int D, bool DIAG, int NP, bool FMA, class Mid>
+// Pass 2 over a half row in kPParts parts: part(q) runs after pairs [q NP/kPParts,
+// (q+1) NP/kPParts) are done -- the caller stores them to TMEM so the PV MMA can
+// start on those keys while the exp continues.
+template <int D, bool DIAG, int NP, bool FMA, int Q = 0, class Part>
+__device__ __forceinline__ void row_exp_parts(uint32_t* s, int lim, int pbase, uint32_t cj2,
+                                              uint32_t scale2, float* acc, Part&& part) {
+  constexpr int W = NP / kPParts<D>;
+  row_exp_range<D, DIAG, Q * W, (Q + 1) * W, FMA>(s, lim, pbase, cj2, scale2, acc);
+  part(Q);
+  if constexpr (Q + 1 < kPParts<D>)
+    row_exp_parts<D, DIAG, NP, FMA, Q + 1>(s, lim, pbase, cj2, scale2, acc, part);
+}
+template <int D, bool DIAG, int NP, bool FMA, class Part>
 __device__ __forceinline__ float row_exp_sum(uint32_t* s, int lim, int pbase, uint32_t cj2,
-                                             uint32_t scale2, Mid&& mid) {
+                                             uint32_t scale2, Part&& part) {
   float acc[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc[k] = 0.f;
-  row_exp_range<D, DIAG, 0, NP / 2, FMA>(s, lim, pbase, cj2, scale2, acc);
-  mid();
-  row_exp_range<D, DIAG, NP / 2, NP, FMA>(s, lim, pbase, cj2, scale2, acc);
+  row_exp_parts<D, DIAG, NP, FMA>(s, lim, pbase, cj2, scale2, acc, part);
   return __fadd_rn(__fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3])),
                    __fadd_rn(__fadd_rn(acc[4], acc[5]), __fadd_rn(acc[6], acc[7])));
 }
@@ -283,10 +304,9 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
   uint64_t* v_full = k_empty + KS;
   uint64_t* v_empty = v_full + VS;
   uint64_t* s_full = v_empty + VS;
-  uint64_t* p_full = s_full + NT;
-  uint64_t* t_full = p_full + NT;
+  uint64_t* t_full = s_full + NT;
   uint64_t* t_empty = t_full + NT;
-  uint64_t* p_half = t_empty + NT;  // P of keys {0-31, 64-95} stored (first half of pass 2)
+  uint64_t* p_part = t_empty + NT;  // [q][t]: P of part q stored (pass 2 in kPParts parts)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
 
   const int warp = static_cast<int>(warp_id());
@@ -309,8 +329,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     for (int t = 0; t < NT; ++t) {
       mbar_init(&q_full[t], 1);
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], 4 * Cfg::HALVES);
-      mbar_init(&p_half[t], 4 * Cfg::HALVES);
+      for (int q = 0; q < kPParts<D>; ++q) mbar_init(&p_part[q * NT + t], 4 * Cfg::HALVES);
       mbar_init(&t_full[t], 1);
       mbar_init(&t_empty[t], 4 * Cfg::HALVES);
     }
@@ -385,15 +404,16 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
                   kIdS, s > 0);
         }
       };
-      // PV in two parts: K-steps {0,1,4,5} (keys whose P the first half of pass 2 stored)
-      // as soon as p_half arrives, {2,3,6,7} after p_full.
+      // PV in kPParts parts: part q covers the K-steps whose keys pass 2 stored in its
+      // part q (half h's pairs -> K-steps 4h + [q, q + 4/kPParts)), issued on p_part[q].
       auto issue_pv = [&](int t, int vs, int part) {
         const uint32_t d_tmem = tmem_base + t * Cfg::TMEM_TILE + 128;
         const uint32_t a_tmem = tmem_base + t * Cfg::TMEM_TILE;
         const uint32_t va = smem_u32(smem + Cfg::SMEM_V + vs * Cfg::TILE_BYTES);
+        constexpr int SP = 4 / kPParts<D>;  // K-steps per half per part
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int s = (k & 1) + 4 * (k >> 1) + 2 * part;
+        for (int k = 0; k < 2 * SP; ++k) {
+          const int s = 4 * (k / SP) + part * SP + k % SP;
           umma_ts(d_tmem, a_tmem + s * 8, smem_desc_sw128(va + s * 2048, Cfg::BOX_BYTES, 1024),
                   kIdPV, part > 0 || k > 0);
         }
@@ -417,14 +437,16 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         for (int t = 0; t < NT; ++t) {
           if (j >= tl[t].nblk) continue;
           PASA_TR(2, j, 4 * t + 0);
-          mbar_wait(&p_half[t], j & 1);
+          mbar_wait(&p_part[t], j & 1);
           PASA_TR(2, j, 4 * t + 1);
           mbar_wait(&t_empty[t], (j & 1) ^ 1);
           tc_fence_after();
           issue_pv(t, vs, 0);
-          mbar_wait(&p_full[t], j & 1);
-          tc_fence_after();
-          issue_pv(t, vs, 1);
+          for (int q = 1; q < kPParts<D>; ++q) {
+            mbar_wait(&p_part[q * NT + t], j & 1);
+            tc_fence_after();
+            issue_pv(t, vs, q);
+          }
           PASA_TR(2, j, 4 * t + 2);
           tc_commit(&t_full[t]);
           if (j + 1 < tl[t].nblk) {
@@ -544,14 +566,22 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         // turns go T0(0), T1(0), T0(1), T1(1), ... while both tiles have blocks.
         if (pingpong && j < nmin && (t == 1 || j > 0)) named_bar_sync(1 + t, 512);
         if (tr) PASA_TR(t, j, 8);
-        // P packed two per column: this half's 32 pairs -> columns [32h, 32h + 32); the
-        // first 16 pairs are stored mid-pass so the PV MMA starts on them (p_half).
-        auto mid = [&]() {
-          tmem_st_16cols_b32(t_s + NP * h, s);
+        // P packed two per column: this half's 32 pairs -> columns [32h, 32h + 32), stored
+        // part by part so the PV MMA starts on each part while the exp continues.
+        auto mid = [&](int q) {
+          constexpr int W = NP / kPParts<D>;
+          if (W == 16) {
+            tmem_st_16cols_b32(t_s + NP * h + q * W, s + q * W);
+          } else if (W == 8) {
+            tmem_st_8cols_b32(t_s + NP * h + q * W, s + q * W);
+          } else {
+            tmem_st_16cols_b32(t_s + NP * h, s);
+            tmem_st_16cols_b32(t_s + NP * h + 16, s + 16);
+          }
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&p_half[t]);
+          if (lane == 0) mbar_arrive(&p_part[q * NT + t]);
         };
         float lsum;
         if (MODE == kModeFa16 || fast2)
@@ -570,11 +600,6 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         PASA_STATE(j, 5, ep);
         PASA_STATE(j, 6, lsum);
         if (tr) PASA_TR(t, j, 7);
-        tmem_st_16cols_b32(t_s + NP * h + 16, s + 16);
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[t]);
         if (tr) PASA_TR(t, j, 4);
         l_run = (jc == 1) ? lsum : __fadd_rn(__fmul_rn(ep, l_run), lsum);
         PASA_STATE(j, 7, l_run);

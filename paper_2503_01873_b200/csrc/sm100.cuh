@@ -154,6 +154,13 @@ __device__ __forceinline__ void tmem_ld_16cols_b32(uint32_t taddr, uint32_t* r) 
         "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+// 32 lanes x 8 columns of 32-bit registers.
+__device__ __forceinline__ void tmem_st_8cols_b32(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+               "r"(r[7])
+               : "memory");
+}
 // 32 lanes x 16 columns of 32-bit registers.
 __device__ __forceinline__ void tmem_st_16cols_b32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
