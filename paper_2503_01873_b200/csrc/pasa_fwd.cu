@@ -36,11 +36,17 @@ using namespace sm100;
 // < kTraceCtas record clock64() at fixed points of the first kTraceIters
 // blocks -- per softmax warpgroup (warp quadrant 0, lane 0) and for the MMA
 // issuer -- into p.trace[cta][role][iter][event].
-// Alternate the two softmax warpgroups' exp passes (named barriers 1, 2).
+// Alternate the two softmax warpgroups' exp passes (named barriers 1, 2).  Pays at
+// d = 64 (+12 %: the exp passes dominate); at d = 128, with P released to the PV MMA in
+// parts, letting both tiles' exp passes overlap is faster (+2-3 %, tools/variants.py).
 #ifndef PASA_PINGPONG
-#define PASA_PINGPONG 1
+#define PASA_PINGPONG 0
 #endif
-constexpr bool kPingPong = PASA_PINGPONG != 0;
+#ifndef PASA_PINGPONG_D64
+#define PASA_PINGPONG_D64 1
+#endif
+template <int D>
+constexpr bool kPingPong = (D == 64 ? PASA_PINGPONG_D64 : PASA_PINGPONG) != 0;
 // One exp pair in kPolyEvery on the FMA-pipe polynomial (0: MUFU only).  d = 128
 // balances MUFU against issue slots at 4; at d = 64 the FMA pipe and the issue
 // slots are shared with twice the softmax work per FLOP and MUFU-only wins
@@ -506,7 +512,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       // both tiles' block counts (identical in every thread of the CTA)
       const int nmin = min(tile_info(p, hkv, unit * NT, CAUSAL).nblk,
                            tile_info(p, hkv, unit * NT + 1, CAUSAL).nblk);
-      const bool pingpong = kPingPong;
+      const bool pingpong = kPingPong<D>;
       for (int j = 0; j < ti.nblk; ++j) {
         const bool tr = h == 0 && quad == 0 && lane == 0;
         if (tr) PASA_TR(t, j, 0);
