@@ -47,6 +47,9 @@ using namespace sm100;
 #endif
 template <int D>
 constexpr bool kPingPong = (D == 64 ? PASA_PINGPONG_D64 : PASA_PINGPONG) != 0;
+#ifndef PASA_DYN_ORDER
+#define PASA_DYN_ORDER 1
+#endif
 // One exp pair in kPolyEvery on the FMA-pipe polynomial (0: MUFU only).  d = 128
 // balances MUFU against issue slots at 4; at d = 64 the FMA pipe and the issue
 // slots are shared with twice the softmax work per FLOP and MUFU-only wins
@@ -440,7 +443,14 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         const int vs = j % VS;
         mbar_wait(&v_full[vs], (j / VS) & 1);
         bool k_next = false;
-        for (int t = 0; t < NT; ++t) {
+        // Serve the tile whose first P part is ready first (no head-of-line blocking
+        // when the two tiles' exp passes overlap).
+        int first = 0;
+        if (PASA_DYN_ORDER && j < tl[0].nblk && j < tl[1].nblk &&
+            !mbar_test_wait(&p_part[0], j & 1) && mbar_test_wait(&p_part[1], j & 1))
+          first = 1;
+        for (int tt = 0; tt < NT; ++tt) {
+          const int t = tt ^ first;
           if (j >= tl[t].nblk) continue;
           PASA_TR(2, j, 4 * t + 0);
           mbar_wait(&p_part[t], j & 1);
