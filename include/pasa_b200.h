@@ -150,9 +150,11 @@ PASA_B200_API int pasa_b200_diag_reset(pasa_b200_diag* diag, void* stream);
 
 /* pasa_b200_attention_fwd from HOST buffers (binary16 bit patterns): copies
  * Q, K, V in, runs, copies O back and synchronizes.  The drop-in for a CPU
- * caller of pasa_attention (the reference's `sweep`, bench.cpp:224).  Device
+ * caller of pasa_attention (the reference's `sweep`, bench.cpp:224).  Pipelined
+ * over chunks of (batch, kv head) units on three streams: the copy-in of chunk
+ * c+1 and the copy-out of chunk c-1 overlap the compute of chunk c.  Device
  * buffers are cached per thread and device; pinned host buffers copy at DMA
- * speed, pageable ones through the driver's staging path. */
+ * speed (and overlap), pageable ones through the driver's staging path. */
 PASA_B200_API int pasa_b200_attention_host(const pasa_b200_desc* desc, const uint16_t* q, const uint16_t* k,
                              const uint16_t* v, uint16_t* o);
 

@@ -358,48 +358,97 @@ static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const
   if (!q || !k || !v || !o) return fail(PASA_B200_EINVAL, "attention_host: NULL buffer");
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(PASA_B200_ENODEV, "no CUDA device");
-  // Per-thread, per-device cache of the device copies and a private stream.
+  // The problem is pipelined over chunks of (batch, kv head) units -- the Q/O rows of a
+  // unit's query heads and its K/V are contiguous in BHSD -- so the host-to-device copy of
+  // chunk c+1 and the device-to-host copy of chunk c-1 overlap the compute of chunk c
+  // (three streams; PCIe is full duplex).  Per-thread, per-device cache of the device
+  // buffers, streams and events.
+  constexpr int kMaxChunks = 8;
   struct Cache {
     int dev = -1;
     uint8_t* buf = nullptr;
     size_t bytes = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t st[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev_in[kMaxChunks] = {}, ev_done[kMaxChunks] = {};
   };
   thread_local Cache cache;
-  const size_t nq = static_cast<size_t>(d->batch) * d->heads_q * d->seq_q * d->head_dim * 2;
-  const size_t nk = kp_bytes(d);
-  const size_t ws = pasa_b200_workspace_size(d);
-  const size_t total = 2 * align_up(nq, 256) + 2 * align_up(nk, 256) + ws + 256;
+  const int group = d->heads_q / d->heads_kv;
+  const int units = d->batch * d->heads_kv;
+  const size_t q_unit = static_cast<size_t>(group) * d->seq_q * d->head_dim * 2;
+  const size_t k_unit = static_cast<size_t>(d->seq_kv) * d->head_dim * 2;
+  const size_t nq = q_unit * units, nk = k_unit * units;
+  // chunking: up to kMaxChunks, but only when each chunk still moves >= 4 MiB
+  int nch = units < kMaxChunks ? units : kMaxChunks;
+  while (nch > 1 && (nq + 2 * nk) / nch < (4u << 20)) --nch;
+  const int per = (units + nch - 1) / nch;
+  nch = (units + per - 1) / per;
+  pasa_b200_desc cd = *d;  // the largest chunk
+  cd.batch = 1;
+  cd.heads_kv = per;
+  cd.heads_q = per * group;
+  const size_t ws = pasa_b200_workspace_size(&cd);
+  const size_t total = 2 * align_up(nq, 256) + 2 * align_up(nk, 256) + align_up(ws, 256) + 256;
   cudaError_t e = cudaSuccess;
   if (cache.dev != dev || cache.bytes < total) {
     if (cache.buf) cudaFree(cache.buf);
-    if (cache.stream && cache.dev != dev) cudaStreamDestroy(cache.stream), cache.stream = nullptr;
+    if (cache.dev != dev) {
+      for (auto& s : cache.st)
+        if (s) cudaStreamDestroy(s), s = nullptr;
+      for (int c = 0; c < kMaxChunks; ++c) {
+        if (cache.ev_in[c]) cudaEventDestroy(cache.ev_in[c]), cache.ev_in[c] = nullptr;
+        if (cache.ev_done[c]) cudaEventDestroy(cache.ev_done[c]), cache.ev_done[c] = nullptr;
+      }
+    }
     cache.buf = nullptr;
     cache.bytes = 0;
     if ((e = cudaMalloc(&cache.buf, total)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
     cache.bytes = total;
     cache.dev = dev;
   }
-  if (!cache.stream && (e = cudaStreamCreateWithFlags(&cache.stream, cudaStreamNonBlocking)) != cudaSuccess)
-    return cuda_fail(e, "cudaStreamCreate");
+  for (auto& s : cache.st)
+    if (!s && (e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "cudaStreamCreate");
+  for (int c = 0; c < kMaxChunks; ++c) {
+    if (!cache.ev_in[c] && (e = cudaEventCreateWithFlags(&cache.ev_in[c], cudaEventDisableTiming)))
+      return cuda_fail(e, "cudaEventCreate");
+    if (!cache.ev_done[c] && (e = cudaEventCreateWithFlags(&cache.ev_done[c], cudaEventDisableTiming)))
+      return cuda_fail(e, "cudaEventCreate");
+  }
   uint8_t* dq = cache.buf;
   uint8_t* dk = dq + align_up(nq, 256);
   uint8_t* dv = dk + align_up(nk, 256);
   uint8_t* dout = dv + align_up(nk, 256);
   uint8_t* dws = dout + align_up(nq, 256);
   pasa_b200_diag* ddiag = reinterpret_cast<pasa_b200_diag*>(dws + align_up(ws, 256));
-  cudaStream_t st = cache.stream;
-  e = cudaMemcpyAsync(dq, q, nq, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(dk, k, nk, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(dv, v, nk, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-  if (hdiag && (rc = pasa_b200_diag_reset(ddiag, st))) return rc;
-  rc = pasa_b200_attention_fwd(d, dq, dk, dv, dout, dws, ws, hdiag ? ddiag : nullptr, st);
-  if (rc) return rc;
-  e = cudaMemcpyAsync(o, dout, nq, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess && hdiag)
-    e = cudaMemcpyAsync(hdiag, ddiag, sizeof(pasa_b200_diag), cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaStream_t s_in = cache.st[0], s_comp = cache.st[1], s_out = cache.st[2];
+  if (hdiag && (rc = pasa_b200_diag_reset(ddiag, s_comp))) return rc;
+  const uint8_t* hq = reinterpret_cast<const uint8_t*>(q);
+  const uint8_t* hk = reinterpret_cast<const uint8_t*>(k);
+  const uint8_t* hv = reinterpret_cast<const uint8_t*>(v);
+  uint8_t* ho = reinterpret_cast<uint8_t*>(o);
+  for (int c = 0; c < nch; ++c) {
+    const int u0 = c * per, nu = (u0 + per <= units ? per : units - u0);
+    const size_t oq = q_unit * u0, ok = k_unit * u0, bq = q_unit * nu, bk = k_unit * nu;
+    e = cudaMemcpyAsync(dq + oq, hq + oq, bq, cudaMemcpyHostToDevice, s_in);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dk + ok, hk + ok, bk, cudaMemcpyHostToDevice, s_in);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dv + ok, hv + ok, bk, cudaMemcpyHostToDevice, s_in);
+    if (e == cudaSuccess) e = cudaEventRecord(cache.ev_in[c], s_in);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s_comp, cache.ev_in[c], 0);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+    pasa_b200_desc ud = cd;
+    ud.heads_kv = nu;
+    ud.heads_q = nu * group;
+    rc = pasa_b200_attention_fwd(&ud, dq + oq, dk + ok, dv + ok, dout + oq, dws, ws,
+                                 hdiag ? ddiag : nullptr, s_comp);
+    if (rc) return rc;
+    e = cudaEventRecord(cache.ev_done[c], s_comp);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, cache.ev_done[c], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ho + oq, dout + oq, bq, cudaMemcpyDeviceToHost, s_out);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+  }
+  if (hdiag)
+    e = cudaMemcpyAsync(hdiag, ddiag, sizeof(pasa_b200_diag), cudaMemcpyDeviceToHost, s_out);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s_out);
   if (e != cudaSuccess) return cuda_fail(e, "D2H copy / kernel");
   return PASA_B200_OK;
 }
