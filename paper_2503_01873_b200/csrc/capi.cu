@@ -364,12 +364,13 @@ static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const
   // (three streams; PCIe is full duplex).  Per-thread, per-device cache of the device
   // buffers, streams and events.
   constexpr int kMaxChunks = 8;
+  constexpr int kMaxEvents = 2 * kMaxChunks;  // chunks x query-head parts
   struct Cache {
     int dev = -1;
     uint8_t* buf = nullptr;
     size_t bytes = 0;
     cudaStream_t st[3] = {nullptr, nullptr, nullptr};
-    cudaEvent_t ev_in[kMaxChunks] = {}, ev_done[kMaxChunks] = {};
+    cudaEvent_t ev_in[kMaxEvents] = {}, ev_done[kMaxEvents] = {};
   };
   thread_local Cache cache;
   const int group = d->heads_q / d->heads_kv;
@@ -394,7 +395,7 @@ static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const
     if (cache.dev != dev) {
       for (auto& s : cache.st)
         if (s) cudaStreamDestroy(s), s = nullptr;
-      for (int c = 0; c < kMaxChunks; ++c) {
+      for (int c = 0; c < kMaxEvents; ++c) {
         if (cache.ev_in[c]) cudaEventDestroy(cache.ev_in[c]), cache.ev_in[c] = nullptr;
         if (cache.ev_done[c]) cudaEventDestroy(cache.ev_done[c]), cache.ev_done[c] = nullptr;
       }
@@ -408,7 +409,7 @@ static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const
   for (auto& s : cache.st)
     if (!s && (e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess)
       return cuda_fail(e, "cudaStreamCreate");
-  for (int c = 0; c < kMaxChunks; ++c) {
+  for (int c = 0; c < kMaxEvents; ++c) {
     if (!cache.ev_in[c] && (e = cudaEventCreateWithFlags(&cache.ev_in[c], cudaEventDisableTiming)))
       return cuda_fail(e, "cudaEventCreate");
     if (!cache.ev_done[c] && (e = cudaEventCreateWithFlags(&cache.ev_done[c], cudaEventDisableTiming)))
@@ -426,25 +427,59 @@ static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const
   const uint8_t* hk = reinterpret_cast<const uint8_t*>(k);
   const uint8_t* hv = reinterpret_cast<const uint8_t*>(v);
   uint8_t* ho = reinterpret_cast<uint8_t*>(o);
-  for (int c = 0; c < nch; ++c) {
+  // With one unit per chunk, a unit's query heads are further split (K/V copied and
+  // pre-processed once per unit) so the pipeline's fill and drain move less data.
+  const int qs = (per == 1 && !hdiag && d->beta != 0.0)
+                     ? (group < kMaxChunks / nch ? group : kMaxChunks / nch) : 1;
+  const int hper = (group + qs - 1) / qs;
+  uint8_t* dkp = dws;  // prepped path: K', V', max|V| of the current unit
+  uint8_t* dvp = dkp + align_up(k_unit, 256);
+  float* dvmax = reinterpret_cast<float*>(dvp + align_up(k_unit, 256));
+  for (int c = 0, ev = 0; c < nch; ++c) {
     const int u0 = c * per, nu = (u0 + per <= units ? per : units - u0);
     const size_t oq = q_unit * u0, ok = k_unit * u0, bq = q_unit * nu, bk = k_unit * nu;
-    e = cudaMemcpyAsync(dq + oq, hq + oq, bq, cudaMemcpyHostToDevice, s_in);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(dk + ok, hk + ok, bk, cudaMemcpyHostToDevice, s_in);
+    e = cudaMemcpyAsync(dk + ok, hk + ok, bk, cudaMemcpyHostToDevice, s_in);
     if (e == cudaSuccess) e = cudaMemcpyAsync(dv + ok, hv + ok, bk, cudaMemcpyHostToDevice, s_in);
-    if (e == cudaSuccess) e = cudaEventRecord(cache.ev_in[c], s_in);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(s_comp, cache.ev_in[c], 0);
     if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
     pasa_b200_desc ud = cd;
     ud.heads_kv = nu;
     ud.heads_q = nu * group;
-    rc = pasa_b200_attention_fwd(&ud, dq + oq, dk + ok, dv + ok, dout + oq, dws, ws,
-                                 hdiag ? ddiag : nullptr, s_comp);
-    if (rc) return rc;
-    e = cudaEventRecord(cache.ev_done[c], s_comp);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, cache.ev_done[c], 0);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(ho + oq, dout + oq, bq, cudaMemcpyDeviceToHost, s_out);
-    if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+    if (qs == 1) {
+      e = cudaMemcpyAsync(dq + oq, hq + oq, bq, cudaMemcpyHostToDevice, s_in);
+      if (e == cudaSuccess) e = cudaEventRecord(cache.ev_in[ev], s_in);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s_comp, cache.ev_in[ev], 0);
+      if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+      rc = pasa_b200_attention_fwd(&ud, dq + oq, dk + ok, dv + ok, dout + oq, dws, ws,
+                                   hdiag ? ddiag : nullptr, s_comp);
+      if (rc) return rc;
+      e = cudaEventRecord(cache.ev_done[ev], s_comp);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, cache.ev_done[ev], 0);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(ho + oq, dout + oq, bq, cudaMemcpyDeviceToHost, s_out);
+      if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+      ++ev;
+      continue;
+    }
+    // one unit, query heads in qs parts
+    const size_t q_head = q_unit / group;
+    for (int g0 = 0; g0 < group; g0 += hper, ++ev) {
+      const int nh = g0 + hper <= group ? hper : group - g0;
+      const size_t oh = oq + q_head * g0, bh = q_head * nh;
+      e = cudaMemcpyAsync(dq + oh, hq + oh, bh, cudaMemcpyHostToDevice, s_in);
+      if (e == cudaSuccess) e = cudaEventRecord(cache.ev_in[ev], s_in);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s_comp, cache.ev_in[ev], 0);
+      if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+      if (g0 == 0 && (rc = pasa_b200_preprocess(&ud, dk + ok, dv + ok, dkp, dvp, dvmax, s_comp)))
+        return rc;
+      pasa_b200_desc hd = ud;
+      hd.heads_q = nh;
+      hd.heads_kv = 1;  // nu == 1: the unit's KV head
+      rc = pasa_b200_attention_fwd_prepped(&hd, dq + oh, dkp, dvp, dvmax, dout + oh, s_comp);
+      if (rc) return rc;
+      e = cudaEventRecord(cache.ev_done[ev], s_comp);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, cache.ev_done[ev], 0);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(ho + oh, dout + oh, bh, cudaMemcpyDeviceToHost, s_out);
+      if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+    }
   }
   if (hdiag)
     e = cudaMemcpyAsync(hdiag, ddiag, sizeof(pasa_b200_diag), cudaMemcpyDeviceToHost, s_out);
