@@ -112,3 +112,23 @@ def test_integration_shim_links_reference_harness():
     nm = subprocess.run(["nm", "-C", exe], capture_output=True, text=True).stdout
     assert "pasa::sweep" in nm and "pasa::pasa_attention" in nm
     assert "pasa::OnlineState::absorb" not in nm  # the reference PASA core is not linked in
+
+
+def test_no_cpu_fallback_without_a_gpu(lib):
+    """On a machine without an sm_100 device every compute entry point fails loudly
+    (there is no CPU fallback); this container has no GPU."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_2503_01873_b200.api import PasaParams, make_problem, pasa_attention
+    d = _desc(seq_q=128, seq_kv=128)
+    buf = (C.c_uint16 * (2 * 128 * 128))()
+    rc = lib.pasa_b200_attention_host(C.byref(d), buf, buf, buf, buf)
+    assert rc in (_lib.ENODEV, _lib.ECUDA) and lib.pasa_b200_last_error()
+    q = torch.zeros(1, 2, 128, 128, dtype=torch.float16)
+    pb = make_problem(q, q, q, 128, 128)
+    with pytest.raises(_lib.PasaError):
+        pasa_attention(pb, PasaParams.make(128, BETA_STAR, pb.alpha))
+    from paper_2503_01873_b200 import pasa_attention_fwd
+    with pytest.raises(ValueError, match="CUDA tensors"):
+        pasa_attention_fwd(q, q, q)
