@@ -52,7 +52,9 @@ typedef struct pasa_b200_desc {
   int32_t head_dim;  /* d in {64, 128}                                         */
   int32_t s1;        /* query block; numerically irrelevant (any divisor of S1) */
   int32_t s2;        /* KV block = shifting-matrix size, <= 128 (128 is fastest)*/
-  int32_t causal;    /* 0: reference semantics; 1: causal (S1 == S2, s2 = 128) */
+  int32_t causal;    /* 0: reference semantics; 1: causal, bottom-right aligned: query
+                        row r sees keys <= r + S2 - S1 (s2 = 128; S1, S2 - S1 multiples
+                        of 128) */
   int32_t reserved;
   double beta;       /* shift fraction in [0, 1) (pasa.cpp:98-101); 0 = FP16 FA */
   double alpha;      /* static scale, must equal sqrt(d) (pasa.cpp:206-208)     */

@@ -125,7 +125,7 @@ def golden_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: 
     """attention.cpp:66-90 on the device: S = Q K^T, S /= sqrt(d), row softmax with max
     subtraction, O = P V -- unblocked, in ``dtype`` (FP64 like the reference by default;
     FP32 for the 128K sweeps).  Chunked over query rows so N = 128K fits.  ``rows``
-    restricts the query rows (a sampled golden); causal keeps col <= row."""
+    restricts the query rows (a sampled golden); causal keeps col <= row + S2 - S1."""
     B, Hq, S1, d = q.shape
     S2 = k.shape[2]
     r0, r1 = (0, S1) if rows is None else (rows.start or 0, rows.stop if rows.stop is not None else S1)
@@ -142,8 +142,8 @@ def golden_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: 
                 for i in range(r0, r1, chunk):
                     j = min(r1, i + chunk)
                     s = (q[b, h, i:j].to(dtype) @ kh.T) / math.sqrt(float(d))
-                    if causal:
-                        ri = torch.arange(i, j, device=q.device)[:, None]
+                    if causal:  # bottom-right aligned: row r sees keys <= r + S2 - S1
+                        ri = torch.arange(i, j, device=q.device)[:, None] + (S2 - S1)
                         cj = torch.arange(S2, device=q.device)[None, :]
                         s.masked_fill_(cj > ri, float("-inf"))
                     s = torch.softmax(s, dim=-1)

@@ -154,7 +154,8 @@ __device__ __forceinline__ TileInfo tile_info(const FwdParams& p, int hkv, int i
   ti.valid = idx < p.tiles_per_kv;
   ti.i = p.nq - 1 - idx / p.group;  // longest (causal) tiles first
   ti.hq = hkv * p.group + idx % p.group;
-  ti.nblk = ti.valid ? (causal ? min(ti.i + 1, p.nkv) : p.nkv) : 0;
+  // causal, bottom-right aligned: query row r sees keys <= r + (S2 - S1) (qblk = (S2-S1)/128)
+  ti.nblk = ti.valid ? (causal ? min(ti.i + 1 + p.qblk, p.nkv) : p.nkv) : 0;
   return ti;
 }
 

@@ -51,6 +51,7 @@ enum FwdMode : int { kModePasa = 0, kModeFa16 = 1 };
 struct FwdParams {
   int B, Hq, Hkv, S1, S2;
   int nq, nkv, group;     // ceil(S1/128), S2/s2, Hq/Hkv
+  int qblk;               // causal: (S2 - S1) / 128, the bottom-right alignment offset
   int s2;                 // KV block (shifting-matrix size), <= 128; < 128 masks columns
   float inv_s2;           // fl32(1/s2): the block mean S'bar = sum * inv_s2
   int tiles_per_kv;       // group * nq

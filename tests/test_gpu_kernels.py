@@ -455,3 +455,24 @@ def test_run_diagnostics_match_reference(dev, orc, ref):
                    AttnOptions(), d2)
     assert (d2.store_finite_min, d2.store_finite_max, d2.out_total) == (
         d1.store_finite_min, d1.store_finite_max, d1.out_total)
+
+
+@pytest.mark.parametrize("S1,S2,D", [(256, 640, 128), (128, 512, 64)])
+def test_fwd_causal_bottom_right(dev, orc, S1, S2, D):
+    """Causal with S1 < S2 (a query chunk after S2 - S1 cached keys): row r sees keys
+    <= r + S2 - S1; against the model with q_offset and the masked FP64 golden."""
+    from paper_2503_01873_b200 import pasa_attention_fwd
+    from paper_2503_01873_b200 import bench_api as ba
+    q = orc.generate("hybrid", 0.0, 10.0, 51, 1, 2, S1, D, tensor_ids=(0,))[0]
+    k, v = orc.generate("hybrid", 0.0, 10.0, 52, 1, 2, S2, D, tensor_ids=(1, 2))
+    pb = Problem(q, k, v, causal=True, q_offset=S2 - S1)
+    qt, kt, vt = (torch.from_numpy(x).half().to(dev) for x in (q, k, v))
+    o = pasa_attention_fwd(qt, kt, vt, causal=True).double().cpu().numpy()
+    gold = orc.golden(pb)
+    gold_dev = ba.golden_attention(qt, kt, vt, causal=True).cpu().numpy()
+    assert np.abs(gold_dev - gold).max() <= 1e-12  # the device golden's alignment agrees
+    model = orc.model_pasa(pb)
+    r_model = orc.rmse(model, gold)
+    assert orc.nan_pct(o) == 0.0
+    assert orc.rmse(o, gold) <= 1.25 * r_model + 2e-4
+    assert orc.rmse(o, model) <= 0.75 * r_model + 2e-4
