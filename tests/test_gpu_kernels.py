@@ -476,3 +476,35 @@ def test_fwd_causal_bottom_right(dev, orc, S1, S2, D):
     assert orc.nan_pct(o) == 0.0
     assert orc.rmse(o, gold) <= 1.25 * r_model + 2e-4
     assert orc.rmse(o, model) <= 0.75 * r_model + 2e-4
+
+
+@pytest.mark.parametrize("cfg", [(1, 28, 4, 16384, 128, True), (1, 8, 8, 32768, 128, False),
+                                 (2, 5, 5, 9216, 64, False)],
+                         ids=["qwen_16k_causal", "h8_32k", "svd_9216_d64"])
+def test_full_size_properties(dev, cfg):
+    """Size-independent properties at BASELINE sizes (no CPU oracle at this scale):
+    (1) O is a convex combination of V rows: every output lies within the column range of
+        the visible V (the prefix for causal rows, checked on the whole V here);
+    (2) V -> 2 V doubles O bit for bit (2^-c0 absorbs the exact power of two) outside the
+        FP16 subnormal range;
+    (3) the run is deterministic."""
+    from paper_2503_01873_b200 import bench_api as ba, pasa_attention_fwd
+    B, Hq, Hkv, S, D, causal = cfg
+    gi = ba.generate(ba.DistributionSpec(ba.DistKind.HYBRID, 0.0, 10.0, 0.001, 3, B, Hq, S, D,
+                                         Hkv), dev)
+    q, k, v = gi.q, gi.k, gi.v
+    o = pasa_attention_fwd(q, k, v, causal=causal)
+    assert bool(torch.isfinite(o).all())
+    g = Hq // Hkv
+    vmin = v.float().amin(dim=2).repeat_interleave(g, dim=1)[:, :, None, :]
+    vmax = v.float().amax(dim=2).repeat_interleave(g, dim=1)[:, :, None, :]
+    of = o.float()
+    tol = 2e-3 * torch.maximum(vmax.abs(), vmin.abs()) + 1e-3  # FP16 rounding of O
+    assert bool(((of >= vmin - tol) & (of <= vmax + tol)).all())
+    o2 = pasa_attention_fwd(q, k, v * 2, causal=causal)
+    # exact except where O is an FP16 subnormal (the final rounding grid is absolute there)
+    normal = o.float().abs() > 2.0 ** -14  # 2^-14 itself can be a rounded-up subnormal
+    assert torch.equal(o2[normal], (o * 2)[normal])
+    assert float((o2.float() - 2 * o.float())[~normal].abs().max().item() if (~normal).any()
+                 else 0.0) <= 2.0 ** -23
+    assert torch.equal(pasa_attention_fwd(q, k, v, causal=causal), o)
