@@ -227,17 +227,20 @@ def _desc(q: torch.Tensor, k: torch.Tensor, s1: int, s2: int, beta: float, alpha
     return _lib.Desc(B, Hq, k.shape[1], S1, k.shape[2], d, s1, s2, int(causal), 0, beta, alpha)
 
 
-_WS: dict[tuple[int, int], torch.Tensor] = {}
+_WS: dict[int, torch.Tensor] = {}
 
 
 def workspace_for(desc: _lib.Desc, device: torch.device) -> torch.Tensor:
+    """One cached workspace per device, grown to the largest request (the caching
+    allocator keeps reuse stream-ordered on the current stream; pass ``workspace=``
+    explicitly when launching on several streams at once)."""
     n = _lib.load().pasa_b200_workspace_size(C.byref(desc))
-    key = (device.index or 0, n)
+    key = device.index if device.index is not None else torch.cuda.current_device()
     ws = _WS.get(key)
-    if ws is None:
+    if ws is None or ws.numel() < n:
         ws = torch.empty(n, dtype=torch.uint8, device=device)
         _WS[key] = ws
-    return ws
+    return ws[:n]
 
 
 def pasa_attention_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, beta: float = BETA_STAR,
