@@ -51,11 +51,12 @@ constexpr bool kPingPong = (D == 64 ? PASA_PINGPONG_D64 : PASA_PINGPONG) != 0;
 #define PASA_DYN_ORDER 1
 #endif
 // One exp pair in kPolyEvery on the FMA-pipe polynomial (0: MUFU only).  d = 128
-// balances MUFU against issue slots at 4; at d = 64 the FMA pipe and the issue
-// slots are shared with twice the softmax work per FLOP and MUFU-only wins
-// (measured: tools/variants.py, +6 % at d = 64, -2 % at d = 128).
+// balances MUFU against issue slots at 6 (5-7 within noise, +2-3 % over 4 once P is
+// released in parts and the tiles' exp passes overlap); at d = 64 the FMA pipe and the
+// issue slots are shared with twice the softmax work per FLOP and MUFU-only wins
+// (measured: tools/variants.py, +6 % at d = 64).
 #ifndef PASA_POLY_EVERY
-#define PASA_POLY_EVERY 4
+#define PASA_POLY_EVERY 6
 #endif
 #ifndef PASA_POLY_EVERY_D64
 #define PASA_POLY_EVERY_D64 0
@@ -220,7 +221,7 @@ __device__ __forceinline__ void row_exp_range(uint32_t* s, int lim, int pbase, u
       const __half2 d = __hsub2(u32_as_h2(s[i]), u32_as_h2(cj2));
       x = h2_as_u32(__hadd2(d, d));
     }
-    // one pair in four on the FMA pipe, the rest on MUFU: balances MUFU time
+    // one pair in kPolyEvery on the FMA pipe, the rest on MUFU: balances MUFU time
     // (8 cycles / pair / SMSP) against issue slots (poly ~11 vs MUFU 3 per pair)
     constexpr int PE = kPolyEvery<D>;
     uint32_t pv = (PE > 0 && (i % (PE > 0 ? PE : 1)) == PE - 1)
