@@ -153,10 +153,12 @@ PASA_B200_API int pasa_b200_diag_reset(pasa_b200_diag* diag, void* stream);
 /* pasa_b200_attention_fwd from HOST buffers (binary16 bit patterns): copies
  * Q, K, V in, runs, copies O back and synchronizes.  The drop-in for a CPU
  * caller of pasa_attention (the reference's `sweep`, bench.cpp:224).  Pipelined
- * over chunks of (batch, kv head) units on three streams: the copy-in of chunk
- * c+1 and the copy-out of chunk c-1 overlap the compute of chunk c.  Device
- * buffers are cached per thread and device; pinned host buffers copy at DMA
- * speed (and overlap), pageable ones through the driver's staging path. */
+ * over ~32 pieces of query heads (a few heads of one (batch, kv head) unit, or a
+ * run of whole units): one H2D stream, a pre-pass stream, four compute streams and
+ * one D2H stream, so copy-in, compute and copy-out of different pieces overlap and
+ * the call is bound by the H2D copy.  Device buffers are cached per thread and
+ * device; pinned host buffers copy at DMA speed (and overlap), pageable ones
+ * through the driver's staging path. */
 PASA_B200_API int pasa_b200_attention_host(const pasa_b200_desc* desc, const uint16_t* q, const uint16_t* k,
                              const uint16_t* v, uint16_t* o);
 

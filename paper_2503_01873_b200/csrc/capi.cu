@@ -361,133 +361,154 @@ static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const
   if (!q || !k || !v || !o) return fail(PASA_B200_EINVAL, "attention_host: NULL buffer");
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(PASA_B200_ENODEV, "no CUDA device");
-  // The problem is pipelined over chunks of (batch, kv head) units -- the Q/O rows of a
-  // unit's query heads and its K/V are contiguous in BHSD -- so the host-to-device copy of
-  // chunk c+1 and the device-to-host copy of chunk c-1 overlap the compute of chunk c
-  // (three streams; PCIe is full duplex).  Per-thread, per-device cache of the device
-  // buffers, streams and events.
-  constexpr int kMaxChunks = 8;
-  constexpr int kMaxEvents = 2 * kMaxChunks;  // chunks x query-head parts
+  // The problem is cut into ~kTargetPieces pieces of query heads -- a few query heads of
+  // one (batch, kv head) unit, or a run of whole units -- that are copied in, computed and
+  // copied out in a pipeline: one H2D stream (K/V of a unit before its first piece, then the
+  // piece's Q), one pre-pass stream (K', V' per unit), kComp compute streams (so the small
+  // kernels of consecutive pieces share the SMs) and one D2H stream (PCIe is full duplex).
+  // Small pieces keep the pipeline's fill (the first piece's H2D) and drain (the last
+  // piece's kernel and D2H) short; the whole call is then bound by the H2D copy
+  // (tools/pcie_probe.py).  Device buffers, streams and events are cached per thread and device.
+  constexpr int kTargetPieces = 32, kComp = 4, kRing = 64;
   struct Cache {
     int dev = -1;
     uint8_t* buf = nullptr;
     size_t bytes = 0;
-    cudaStream_t st[3] = {nullptr, nullptr, nullptr};
-    cudaEvent_t ev_in[kMaxEvents] = {}, ev_done[kMaxEvents] = {};
+    cudaStream_t st[3 + kComp] = {};
+    cudaEvent_t ev[3][kRing] = {};  // kv copied / piece copied in / piece computed
+    cudaEvent_t prep[kRing] = {}, comp_done[kComp] = {};
   };
   thread_local Cache cache;
   const int group = d->heads_q / d->heads_kv;
   const int units = d->batch * d->heads_kv;
-  const size_t q_unit = static_cast<size_t>(group) * d->seq_q * d->head_dim * 2;
+  const size_t q_head = static_cast<size_t>(d->seq_q) * d->head_dim * 2;
+  const size_t q_unit = q_head * group;
   const size_t k_unit = static_cast<size_t>(d->seq_kv) * d->head_dim * 2;
   const size_t nq = q_unit * units, nk = k_unit * units;
-  // chunking: up to kMaxChunks, but only when each chunk still moves >= 4 MiB
-  int nch = units < kMaxChunks ? units : kMaxChunks;
-  while (nch > 1 && (nq + 2 * nk) / nch < (4u << 20)) --nch;
-  const int per = (units + nch - 1) / nch;
-  nch = (units + per - 1) / per;
-  pasa_b200_desc cd = *d;  // the largest chunk
-  cd.batch = 1;
-  cd.heads_kv = per;
-  cd.heads_q = per * group;
-  const size_t ws = pasa_b200_workspace_size(&cd);
-  const size_t total = 2 * align_up(nq, 256) + 2 * align_up(nk, 256) + align_up(ws, 256) + 256;
+  const bool pasa = d->beta != 0.0;
+  // piece size in query heads; below a unit's group the unit is split, above it whole units
+  const int total = units * group;
+  const int ph = (total + kTargetPieces - 1) / kTargetPieces;
+  int hper = group, uper = 1;
+  if (ph < group) {
+    const int parts = (group + ph - 1) / ph;
+    hper = (group + parts - 1) / parts;
+  } else {
+    uper = ph / group;
+  }
+  const size_t total_bytes = 2 * align_up(nq, 256) + 4 * align_up(nk, 256) +
+                             align_up(static_cast<size_t>(units) * 4, 256) + 256;
   cudaError_t e = cudaSuccess;
-  if (cache.dev != dev || cache.bytes < total) {
+  if (cache.dev != dev || cache.bytes < total_bytes) {
     if (cache.buf) cudaFree(cache.buf);
     if (cache.dev != dev) {
-      for (auto& s : cache.st)
-        if (s) cudaStreamDestroy(s), s = nullptr;
-      for (int c = 0; c < kMaxEvents; ++c) {
-        if (cache.ev_in[c]) cudaEventDestroy(cache.ev_in[c]), cache.ev_in[c] = nullptr;
-        if (cache.ev_done[c]) cudaEventDestroy(cache.ev_done[c]), cache.ev_done[c] = nullptr;
-      }
+      for (auto& st : cache.st)
+        if (st) cudaStreamDestroy(st), st = nullptr;
+      for (auto& row : cache.ev)
+        for (auto& x : row)
+          if (x) cudaEventDestroy(x), x = nullptr;
+      for (auto& x : cache.prep)
+        if (x) cudaEventDestroy(x), x = nullptr;
+      for (auto& x : cache.comp_done)
+        if (x) cudaEventDestroy(x), x = nullptr;
     }
     cache.buf = nullptr;
     cache.bytes = 0;
-    if ((e = cudaMalloc(&cache.buf, total)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
-    cache.bytes = total;
+    if ((e = cudaMalloc(&cache.buf, total_bytes)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    cache.bytes = total_bytes;
     cache.dev = dev;
   }
-  for (auto& s : cache.st)
-    if (!s && (e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess)
+  for (auto& st : cache.st)
+    if (!st && (e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess)
       return cuda_fail(e, "cudaStreamCreate");
-  for (int c = 0; c < kMaxEvents; ++c) {
-    if (!cache.ev_in[c] && (e = cudaEventCreateWithFlags(&cache.ev_in[c], cudaEventDisableTiming)))
-      return cuda_fail(e, "cudaEventCreate");
-    if (!cache.ev_done[c] && (e = cudaEventCreateWithFlags(&cache.ev_done[c], cudaEventDisableTiming)))
-      return cuda_fail(e, "cudaEventCreate");
-  }
+  auto mk = [&](cudaEvent_t& x) {
+    return x ? cudaSuccess : cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+  };
+  for (auto& row : cache.ev)
+    for (auto& x : row)
+      if ((e = mk(x)) != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+  for (auto& x : cache.prep)
+    if ((e = mk(x)) != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+  for (auto& x : cache.comp_done)
+    if ((e = mk(x)) != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
   uint8_t* dq = cache.buf;
   uint8_t* dk = dq + align_up(nq, 256);
   uint8_t* dv = dk + align_up(nk, 256);
-  uint8_t* dout = dv + align_up(nk, 256);
-  uint8_t* dws = dout + align_up(nq, 256);
-  pasa_b200_diag* ddiag = reinterpret_cast<pasa_b200_diag*>(dws + align_up(ws, 256));
-  cudaStream_t s_in = cache.st[0], s_comp = cache.st[1], s_out = cache.st[2];
-  if (hdiag && (rc = pasa_b200_diag_reset(ddiag, s_comp))) return rc;
+  uint8_t* dkp = dv + align_up(nk, 256);  // K', V', max|V| of every unit (pre-pass output)
+  uint8_t* dvp = dkp + align_up(nk, 256);
+  uint8_t* dout = dvp + align_up(nk, 256);
+  float* dvmax = reinterpret_cast<float*>(dout + align_up(nq, 256));
+  pasa_b200_diag* ddiag = nullptr;
+  cudaStream_t s_in = cache.st[0], s_prep = cache.st[1], s_out = cache.st[2];
+  const cudaStream_t* s_comp = cache.st + 3;
+  if (hdiag) {
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&ddiag), sizeof(pasa_b200_diag), s_prep)))
+      return cuda_fail(e, "cudaMallocAsync");
+    if ((rc = pasa_b200_diag_reset(ddiag, s_prep))) return rc;
+    if ((e = cudaEventRecord(cache.prep[0], s_prep)) != cudaSuccess) return cuda_fail(e, "event");
+    for (int c = 0; c < kComp; ++c)
+      if ((e = cudaStreamWaitEvent(s_comp[c], cache.prep[0], 0)) != cudaSuccess) return cuda_fail(e, "event");
+  }
   const uint8_t* hq = reinterpret_cast<const uint8_t*>(q);
   const uint8_t* hk = reinterpret_cast<const uint8_t*>(k);
   const uint8_t* hv = reinterpret_cast<const uint8_t*>(v);
   uint8_t* ho = reinterpret_cast<uint8_t*>(o);
-  // With one unit per chunk, a unit's query heads are further split (K/V copied and
-  // pre-processed once per unit) so the pipeline's fill and drain move less data.
-  const int qs = (per == 1 && !hdiag && d->beta != 0.0)
-                     ? (group < kMaxChunks / nch ? group : kMaxChunks / nch) : 1;
-  const int hper = (group + qs - 1) / qs;
-  uint8_t* dkp = dws;  // prepped path: K', V', max|V| of the current unit
-  uint8_t* dvp = dkp + align_up(k_unit, 256);
-  float* dvmax = reinterpret_cast<float*>(dvp + align_up(k_unit, 256));
-  for (int c = 0, ev = 0; c < nch; ++c) {
-    const int u0 = c * per, nu = (u0 + per <= units ? per : units - u0);
-    const size_t oq = q_unit * u0, ok = k_unit * u0, bq = q_unit * nu, bk = k_unit * nu;
+  int piece = 0, kvc = 0;
+  for (int u0 = 0; u0 < units; u0 += uper) {
+    const int nu = u0 + uper <= units ? uper : units - u0;
+    const size_t ok = k_unit * u0, bk = k_unit * nu;
+    // K and V of the piece's units, then (PASA) their pre-pass on its own stream
+    cudaEvent_t ev_kv = cache.ev[0][kvc % kRing], ev_prep = cache.prep[kvc % kRing];
+    ++kvc;
     e = cudaMemcpyAsync(dk + ok, hk + ok, bk, cudaMemcpyHostToDevice, s_in);
     if (e == cudaSuccess) e = cudaMemcpyAsync(dv + ok, hv + ok, bk, cudaMemcpyHostToDevice, s_in);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_kv, s_in);
     if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-    pasa_b200_desc ud = cd;
+    pasa_b200_desc ud = *d;
+    ud.batch = 1;
     ud.heads_kv = nu;
     ud.heads_q = nu * group;
-    if (qs == 1) {
+    if (pasa) {
+      if ((e = cudaStreamWaitEvent(s_prep, ev_kv, 0)) != cudaSuccess) return cuda_fail(e, "event");
+      if ((rc = pasa_b200_preprocess(&ud, dk + ok, dv + ok, dkp + ok, dvp + ok, dvmax + u0, s_prep)))
+        return rc;
+      if ((e = cudaEventRecord(ev_prep, s_prep)) != cudaSuccess) return cuda_fail(e, "event");
+    }
+    for (int g0 = 0; g0 < group; g0 += hper, ++piece) {
+      const int nh = g0 + hper <= group ? hper : group - g0;
+      // query heads [g0, g0 + nh) of each unit: contiguous only for one unit or all heads
+      const size_t oq = q_unit * u0 + q_head * g0, bq = nu == 1 ? q_head * nh : q_unit * nu;
+      cudaEvent_t ev_in = cache.ev[1][piece % kRing], ev_done = cache.ev[2][piece % kRing];
+      const cudaStream_t sc = s_comp[piece % kComp];
       e = cudaMemcpyAsync(dq + oq, hq + oq, bq, cudaMemcpyHostToDevice, s_in);
-      if (e == cudaSuccess) e = cudaEventRecord(cache.ev_in[ev], s_in);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(s_comp, cache.ev_in[ev], 0);
+      if (e == cudaSuccess) e = cudaEventRecord(ev_in, s_in);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(sc, ev_in, 0);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(sc, pasa ? ev_prep : ev_kv, 0);
       if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-      rc = pasa_b200_attention_fwd(&ud, dq + oq, dk + ok, dv + ok, dout + oq, dws, ws,
-                                   hdiag ? ddiag : nullptr, s_comp);
+      pasa_b200_desc pd = ud;
+      pd.heads_q = nu == 1 ? nh : nu * group;
+      rc = pasa ? launch_forward(&pd, kModePasa, dq + oq, dkp + ok, dvp + ok, dvmax + u0, dout + oq, sc, ddiag)
+                : launch_forward(&pd, kModeFa16, dq + oq, dk + ok, dv + ok, nullptr, dout + oq, sc, ddiag);
       if (rc) return rc;
-      e = cudaEventRecord(cache.ev_done[ev], s_comp);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, cache.ev_done[ev], 0);
+      e = cudaEventRecord(ev_done, sc);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, ev_done, 0);
       if (e == cudaSuccess) e = cudaMemcpyAsync(ho + oq, dout + oq, bq, cudaMemcpyDeviceToHost, s_out);
       if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
-      ++ev;
-      continue;
-    }
-    // one unit, query heads in qs parts
-    const size_t q_head = q_unit / group;
-    for (int g0 = 0; g0 < group; g0 += hper, ++ev) {
-      const int nh = g0 + hper <= group ? hper : group - g0;
-      const size_t oh = oq + q_head * g0, bh = q_head * nh;
-      e = cudaMemcpyAsync(dq + oh, hq + oh, bh, cudaMemcpyHostToDevice, s_in);
-      if (e == cudaSuccess) e = cudaEventRecord(cache.ev_in[ev], s_in);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(s_comp, cache.ev_in[ev], 0);
-      if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-      if (g0 == 0 && (rc = pasa_b200_preprocess(&ud, dk + ok, dv + ok, dkp, dvp, dvmax, s_comp)))
-        return rc;
-      pasa_b200_desc hd = ud;
-      hd.heads_q = nh;
-      hd.heads_kv = 1;  // nu == 1: the unit's KV head
-      rc = pasa_b200_attention_fwd_prepped(&hd, dq + oh, dkp, dvp, dvmax, dout + oh, s_comp);
-      if (rc) return rc;
-      e = cudaEventRecord(cache.ev_done[ev], s_comp);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, cache.ev_done[ev], 0);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(ho + oh, dout + oh, bh, cudaMemcpyDeviceToHost, s_out);
-      if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+      if (nu > 1) break;  // whole units: one piece covers all their query heads
     }
   }
-  if (hdiag)
+  if (hdiag) {
+    for (int c = 0; c < kComp; ++c) {
+      e = cudaEventRecord(cache.comp_done[c], s_comp[c]);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, cache.comp_done[c], 0);
+      if (e != cudaSuccess) return cuda_fail(e, "event");
+    }
     e = cudaMemcpyAsync(hdiag, ddiag, sizeof(pasa_b200_diag), cudaMemcpyDeviceToHost, s_out);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s_out);
-  if (e != cudaSuccess) return cuda_fail(e, "D2H copy / kernel");
+    if (e == cudaSuccess) e = cudaFreeAsync(ddiag, s_out);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+  }
+  // every compute stream's last kernel precedes a D2H on s_out, so s_out completes last
+  if ((e = cudaStreamSynchronize(s_out)) != cudaSuccess) return cuda_fail(e, "D2H copy / kernel");
   return PASA_B200_OK;
 }
 

@@ -424,6 +424,34 @@ def test_fused_prepass_rank1_bitexact(dev, orc, D):
         assert np.array_equal(vp[0, h].double().cpu().numpy(), orc.f16(v[0, h] * 2.0 ** -c0))
 
 
+@pytest.mark.parametrize("B,Hq,Hkv,S,D,causal,beta", [
+    (1, 28, 4, 512, 128, True, BETA_STAR),   # 28 pieces of one query head (GQA units split)
+    (5, 14, 2, 256, 64, True, BETA_STAR),    # pieces of 3, 3, 1 query heads per unit
+    (3, 20, 20, 256, 64, False, BETA_STAR),  # runs of two whole units per piece
+    (2, 8, 2, 384, 128, True, 0.0),          # beta = 0: FA16, no pre-pass
+])
+def test_host_pipeline_pieces_bit_identical(dev, B, Hq, Hkv, S, D, causal, beta):
+    """pasa_b200_attention_host (pieces of query heads over H2D / pre-pass / four compute /
+    D2H streams) returns exactly the device path's output for every piece layout."""
+    from paper_2503_01873_b200 import _lib, flash_fp16_fwd, pasa_attention_fwd
+    g = torch.Generator().manual_seed(B * 1000 + Hq)
+    q = (torch.randn(B, Hq, S, D, generator=g) * 3).half()
+    k = (torch.randn(B, Hkv, S, D, generator=g) * 3).half()
+    v = torch.randn(B, Hkv, S, D, generator=g).half()
+    qd, kd, vd = (x.to(dev) for x in (q, k, v))
+    want = (pasa_attention_fwd(qd, kd, vd, beta, causal=causal) if beta
+            else flash_fp16_fwd(qd, kd, vd, causal=causal)).cpu()
+    L = _lib.load()
+    desc = _lib.Desc(B, Hq, Hkv, S, S, D, 128, 128, int(causal), 0, beta, math.sqrt(D))
+    qh, kh, vh = (x.pin_memory() for x in (q, k, v))
+    oh = torch.empty_like(qh).pin_memory()
+    for _ in range(2):  # second call reuses the cached buffers, streams and events
+        oh.zero_()
+        _lib.check(L.pasa_b200_attention_host(C.byref(desc), qh.data_ptr(), kh.data_ptr(),
+                                              vh.data_ptr(), oh.data_ptr()))
+        assert torch.equal(oh, want)
+
+
 def test_run_diagnostics_match_reference(dev, orc, ref):
     """RunDiagnostics from the device (attention.hpp:30-48): the FP16 FA store overflows on
     every score of uniform(30, 0.5) like the reference's; PASA's stored-score range matches the
