@@ -306,19 +306,20 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
   using Cfg = FwdCfg<D>;
   constexpr int NT = Cfg::NT, KS = Cfg::KS, VS = Cfg::VS;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::SMEM_BAR);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = q_full + NT;
-  uint64_t* k_empty = k_full + KS;
-  uint64_t* v_full = k_empty + KS;
-  uint64_t* v_empty = v_full + VS;
-  uint64_t* s_full = v_empty + VS;
-  uint64_t* t_full = s_full + NT;
-  uint64_t* t_empty = t_full + NT;
-  uint64_t* p_part = t_empty + NT;  // [q][t]: P of part q stored (pass 2 in kPParts parts)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + Cfg::NUM_BARS);
+  // 1024-byte aligned base (SW128 tiles) as a 32-bit shared address; barriers and tiles are
+  // constant offsets from it, so the loops address them without generic-pointer conversions
+  const uint32_t sb = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (sb - smem_u32(smem_raw));  // generic view of the same base
+  const uint32_t q_full = sb + Cfg::SMEM_BAR;  // mbarriers, 8 bytes each
+  const uint32_t k_full = q_full + 8 * NT;
+  const uint32_t k_empty = k_full + 8 * KS;
+  const uint32_t v_full = k_empty + 8 * KS;
+  const uint32_t v_empty = v_full + 8 * VS;
+  const uint32_t s_full = v_empty + 8 * VS;
+  const uint32_t t_full = s_full + 8 * NT;
+  const uint32_t t_empty = t_full + 8 * NT;
+  const uint32_t p_part = t_empty + 8 * NT;  // [q][t]: P of part q stored (pass 2 in kPParts parts)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Cfg::SMEM_BAR + 8 * Cfg::NUM_BARS);
 
   const int warp = static_cast<int>(warp_id());
   const int lane = threadIdx.x & 31;
@@ -338,19 +339,19 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int t = 0; t < NT; ++t) {
-      mbar_init(&q_full[t], 1);
-      mbar_init(&s_full[t], 1);
-      for (int q = 0; q < kPParts<D>; ++q) mbar_init(&p_part[q * NT + t], 4 * Cfg::HALVES);
-      mbar_init(&t_full[t], 1);
-      mbar_init(&t_empty[t], 4 * Cfg::HALVES);
+      mbar_init(q_full + 8 * (t), 1);
+      mbar_init(s_full + 8 * (t), 1);
+      for (int q = 0; q < kPParts<D>; ++q) mbar_init(p_part + 8 * (q * NT + t), 4 * Cfg::HALVES);
+      mbar_init(t_full + 8 * (t), 1);
+      mbar_init(t_empty + 8 * (t), 4 * Cfg::HALVES);
     }
     for (int s = 0; s < KS; ++s) {
-      mbar_init(&k_full[s], 1);
-      mbar_init(&k_empty[s], 1);
+      mbar_init(k_full + 8 * (s), 1);
+      mbar_init(k_empty + 8 * (s), 1);
     }
     for (int s = 0; s < VS; ++s) {
-      mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], 1);
+      mbar_init(v_full + 8 * (s), 1);
+      mbar_init(v_empty + 8 * (s), 1);
     }
     fence_barrier_init();
   }
@@ -366,7 +367,11 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
+  // A 512-column allocation is the whole TMEM of the SM, so it starts at lane 0, column 0:
+  // the base is the constant 0 (no per-thread register, no spill, uniform addressing).
+  static_assert(Cfg::TMEM_COLS == 512, "tmem_base = 0 needs the full allocation");
+  constexpr uint32_t tmem_base = 0;
+  (void)tmem_holder;
 
   // Register budget: 640 threads x 96 at launch = 61440 per CTA; setmaxnreg
   // moves registers only within the CTA: 128 x 56 + 512 x 104 = 60416.
@@ -380,23 +385,23 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       tma_prefetch(&tm_v);
       for (int t = 0; t < NT; ++t) {
         if (!tl[t].valid) continue;
-        mbar_expect_tx(&q_full[t], Cfg::TILE_BYTES);
+        mbar_expect_tx(q_full + 8 * (t), Cfg::TILE_BYTES);
         for (int bx = 0; bx < Cfg::NBOX; ++bx)
-          tma_load_3d(smem + Cfg::SMEM_Q + t * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_q,
-                      &q_full[t], bx * 64, tl[t].i * kTile, b * p.Hq + tl[t].hq);
+          tma_load_3d(sb + Cfg::SMEM_Q + t * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_q,
+                      q_full + 8 * (t), bx * 64, tl[t].i * kTile, b * p.Hq + tl[t].hq);
       }
       for (int j = 0; j < nmax; ++j) {
         const int ks = j % KS, vs = j % VS;
-        mbar_wait(&k_empty[ks], ((j / KS) & 1) ^ 1);
-        mbar_expect_tx(&k_full[ks], Cfg::NBOX * 128 * p.s2);
+        mbar_wait(k_empty + 8 * (ks), ((j / KS) & 1) ^ 1);
+        mbar_expect_tx(k_full + 8 * (ks), Cfg::NBOX * 128 * p.s2);
         for (int bx = 0; bx < Cfg::NBOX; ++bx)
-          tma_load_3d(smem + Cfg::SMEM_K + ks * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_kp,
-                      &k_full[ks], bx * 64, j * p.s2, b * p.Hkv + hkv);
-        mbar_wait(&v_empty[vs], ((j / VS) & 1) ^ 1);
-        mbar_expect_tx(&v_full[vs], Cfg::NBOX * 128 * p.s2);
+          tma_load_3d(sb + Cfg::SMEM_K + ks * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_kp,
+                      k_full + 8 * (ks), bx * 64, j * p.s2, b * p.Hkv + hkv);
+        mbar_wait(v_empty + 8 * (vs), ((j / VS) & 1) ^ 1);
+        mbar_expect_tx(v_full + 8 * (vs), Cfg::NBOX * 128 * p.s2);
         for (int bx = 0; bx < Cfg::NBOX; ++bx)
-          tma_load_3d(smem + Cfg::SMEM_V + vs * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_v,
-                      &v_full[vs], bx * 64, j * p.s2, b * p.Hkv + hkv);
+          tma_load_3d(sb + Cfg::SMEM_V + vs * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_v,
+                      v_full + 8 * (vs), bx * 64, j * p.s2, b * p.Hkv + hkv);
       }
     }
   } else if (warp == 1) {
@@ -406,8 +411,8 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       constexpr uint32_t kIdPV = idesc_f16(128, D, 0, 0, 1);   // F16 acc, V MN-major
       auto issue_s = [&](int t, int ks) {
         const uint32_t d_tmem = tmem_base + t * Cfg::TMEM_TILE;
-        const uint32_t qa = smem_u32(smem + Cfg::SMEM_Q + t * Cfg::TILE_BYTES);
-        const uint32_t ka = smem_u32(smem + Cfg::SMEM_K + ks * Cfg::TILE_BYTES);
+        const uint32_t qa = sb + Cfg::SMEM_Q + t * Cfg::TILE_BYTES;
+        const uint32_t ka = sb + Cfg::SMEM_K + ks * Cfg::TILE_BYTES;
 #pragma unroll
         for (int s = 0; s < D / 16; ++s) {
           const uint32_t off = (s / 4) * Cfg::BOX_BYTES + (s % 4) * 32;
@@ -420,7 +425,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       auto issue_pv = [&](int t, int vs, int part) {
         const uint32_t d_tmem = tmem_base + t * Cfg::TMEM_TILE + 128;
         const uint32_t a_tmem = tmem_base + t * Cfg::TMEM_TILE;
-        const uint32_t va = smem_u32(smem + Cfg::SMEM_V + vs * Cfg::TILE_BYTES);
+        const uint32_t va = sb + Cfg::SMEM_V + vs * Cfg::TILE_BYTES;
         constexpr int SP = 4 / kPParts<D>;  // K-steps per half per part
 #pragma unroll
         for (int k = 0; k < 2 * SP; ++k) {
@@ -430,57 +435,57 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         }
       };
       for (int t = 0; t < NT; ++t)
-        if (tl[t].valid) mbar_wait(&q_full[t], 0);
+        if (tl[t].valid) mbar_wait(q_full + 8 * (t), 0);
       if (nmax > 0) {
-        mbar_wait(&k_full[0], 0);
+        mbar_wait(k_full + 8 * (0), 0);
         tc_fence_after();
         for (int t = 0; t < NT; ++t) {
           if (tl[t].nblk == 0) continue;
           issue_s(t, 0);
-          tc_commit(&s_full[t]);
+          tc_commit(s_full + 8 * (t));
         }
-        tc_commit(&k_empty[0]);
+        tc_commit(k_empty + 8 * (0));
       }
       for (int j = 0; j < nmax; ++j) {
         const int vs = j % VS;
-        mbar_wait(&v_full[vs], (j / VS) & 1);
+        mbar_wait(v_full + 8 * (vs), (j / VS) & 1);
         bool k_next = false;
         // Serve the tile whose first P part is ready first (no head-of-line blocking
         // when the two tiles' exp passes overlap).
         int first = 0;
         if (PASA_DYN_ORDER && j < tl[0].nblk && j < tl[1].nblk &&
-            !mbar_test_wait(&p_part[0], j & 1) && mbar_test_wait(&p_part[1], j & 1))
+            !mbar_test_wait(p_part + 8 * (0), j & 1) && mbar_test_wait(p_part + 8 * (1), j & 1))
           first = 1;
         for (int tt = 0; tt < NT; ++tt) {
           const int t = tt ^ first;
           if (j >= tl[t].nblk) continue;
           PASA_TR(2, j, 4 * t + 0);
-          mbar_wait(&p_part[t], j & 1);
+          mbar_wait(p_part + 8 * (t), j & 1);
           PASA_TR(2, j, 4 * t + 1);
-          mbar_wait(&t_empty[t], (j & 1) ^ 1);
+          mbar_wait(t_empty + 8 * (t), (j & 1) ^ 1);
           tc_fence_after();
           issue_pv(t, vs, 0);
           for (int q = 1; q < kPParts<D>; ++q) {
-            mbar_wait(&p_part[q * NT + t], j & 1);
+            mbar_wait(p_part + 8 * (q * NT + t), j & 1);
             tc_fence_after();
             issue_pv(t, vs, q);
           }
           PASA_TR(2, j, 4 * t + 2);
-          tc_commit(&t_full[t]);
+          tc_commit(t_full + 8 * (t));
           if (j + 1 < tl[t].nblk) {
             const int ks = (j + 1) % KS;
             if (!k_next) {
-              mbar_wait(&k_full[ks], ((j + 1) / KS) & 1);
+              mbar_wait(k_full + 8 * (ks), ((j + 1) / KS) & 1);
               tc_fence_after();
               k_next = true;
             }
             issue_s(t, ks);
-            tc_commit(&s_full[t]);
+            tc_commit(s_full + 8 * (t));
             PASA_TR(2, j, 4 * t + 3);
           }
         }
-        tc_commit(&v_empty[vs]);
-        if (k_next) tc_commit(&k_empty[(j + 1) % KS]);
+        tc_commit(v_empty + 8 * (vs));
+        if (k_next) tc_commit(k_empty + 8 * ((j + 1) % KS));
       }
     }
   }
@@ -499,10 +504,10 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     const TileInfo ti = tile_info(p, hkv, unit * NT + t, CAUSAL);
     const uint32_t t_s = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + t * Cfg::TMEM_TILE;
     const uint32_t t_t = t_s + 128;
-    float2* xch = reinterpret_cast<float2*>(smem + Cfg::SMEM_XCH);
-    auto xslot = [&](int parity, int half) -> float2* {
-      return xch + ((parity * NT + t) * Cfg::HALVES + half) * kTile + row;
-    };
+    // exchange slots [parity][t][half][row] of float2, as shared-memory addresses
+    const uint32_t xs_mine = sb + Cfg::SMEM_XCH + ((t * Cfg::HALVES + h) * kTile + row) * 8;
+    const uint32_t xs_other = xs_mine + (1 - 2 * h) * kTile * 8;
+    constexpr uint32_t kXPar = NT * Cfg::HALVES * kTile * 8;  // parity stride
     const uint32_t xbar = 3 + t * 4 + quad;  // named barrier of this row quadrant's two warps
     float* dslot = reinterpret_cast<float*>(smem + Cfg::SMEM_DIAG) + (threadIdx.x - 128) * 5;
     if (DIAGNOSE) {
@@ -528,7 +533,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       for (int j = 0; j < ti.nblk; ++j) {
         const bool tr = h == 0 && quad == 0 && lane == 0;
         if (tr) PASA_TR(t, j, 0);
-        mbar_wait(&s_full[t], j & 1);
+        mbar_wait(s_full + 8 * (t), j & 1);
         if (tr) PASA_TR(t, j, 1);
         tc_fence_after();
         tmem_ld_32cols_pack16(t_s + 64 * h, s);
@@ -544,9 +549,9 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         float mh, sh = 0.f;
         if (diag) row_max_sum<true, NP, kSum>(s, lim, NP * h, mh, sh);
         else row_max_sum<false, NP, kSum>(s, lim, NP * h, mh, sh);
-        *xslot(j & 1, h) = make_float2(mh, sh);
+        st_shared_f2(xs_mine + (j & 1) * kXPar, mh, sh);
         named_bar_sync(xbar, 64);
-        const float2 other = *xslot(j & 1, 1 - h);
+        const float2 other = ld_shared_f2(xs_other + (j & 1) * kXPar);
         const float mloc = fmaxf(mh, other.x);
         const int jc = j + 1;
         float mnew, ep, fnew = 0.f;
@@ -599,7 +604,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&p_part[q * NT + t]);
+          if (lane == 0) mbar_arrive(p_part + 8 * (q * NT + t));
         };
         float lsum;
         if (MODE == kModeFa16 || fast2)
@@ -625,7 +630,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         fbar = fnew;
         rcp_j = __frcp_rn(static_cast<float>(jc + 1));
         // T = P V_j -> this half's D/2 output columns
-        mbar_wait(&t_full[t], j & 1);
+        mbar_wait(t_full + 8 * (t), j & 1);
         if (tr) PASA_TR(t, j, 5);
         tc_fence_after();
 #pragma unroll
@@ -633,7 +638,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&t_empty[t]);
+        if (lane == 0) mbar_arrive(t_empty + 8 * (t));
         if (tr) PASA_TR(t, j, 6);
         {  // O <- e_prev O + T; block 1 has e_prev = 0 and O = 0 (no branch, no copies)
           const __half2 ep2 = __float2half2_rn(ep);
@@ -643,9 +648,9 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         }
       }
       // Epilogue: global recovering O / l (pasa.cpp:184-194), fp16 store.
-      *xslot(ti.nblk & 1, h) = make_float2(l_run, 0.f);
+      st_shared_f2(xs_mine + (ti.nblk & 1) * kXPar, l_run, 0.f);
       named_bar_sync(xbar, 64);
-      const float lo_other = xslot(ti.nblk & 1, 1 - h)->x;
+      const float lo_other = ld_shared_f2(xs_other + (ti.nblk & 1) * kXPar).x;
       const float l_tot = h == 0 ? __fadd_rn(l_run, lo_other) : __fadd_rn(lo_other, l_run);
       const float inv_l = __fmul_rn(__frcp_rn(l_tot), ldexpf(1.0f, c0));  // exact 2^c0
       const bool row_ok = ti.i * kTile + row < p.S1;  // ragged last query tile
