@@ -547,7 +547,9 @@ ORC_API int orc_pasa_ref(const orc_shape* sh, const double* q, const double* k,
 /* exact in real arithmetic:                                                 */
 /*  - every score lives in the L domain (lscale = log2 e: 2^x replaces e^x), */
 /*  - row statistics (sum of S', mean, F, corrections, running max, l) are   */
-/*    FP32; the S' and P row sums run as eight chains (kernel order),        */
+/*    FP32; the S' row sum runs as eight chains (kernel order) or, at d <=  */
+/*    112, is the tensor core's q . (sum of the block's K' columns) (the    */
+/*    pseudo-average GEMM); the P row sum runs as eight chains               */
 /*  - F_j = F_{j-1} + (Sbar - F_{j-1}) * fl32(1/j) (no (j-1)*F product),     */
 /*  - e_cur is folded into P: P = 2^(fl16(S' - c_j)) with c_j = fl16(m_j -   */
 /*    dm_cur), so O <- fl16(e_p * O + T); V enters as V' = fl16(V 2^-c0) with */
@@ -636,6 +638,9 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
     float* fbar = calloc(s1, sizeof(float));
     double* oacc = calloc(s1 * d, sizeof(double));
     double* S = malloc(sizeof(double) * s2);
+    const int tcsum = (128 + d + 16 <= 256); /* the kernel's pasa_tc_rowsum(d) */
+    double* ksh = malloc(sizeof(double) * d); /* K' block sums, hi / lo parts */
+    double* ksl = malloc(sizeof(double) * d);
     size_t jc = 0; /* consumed blocks */
     for (size_t j = 0; j < nkv; ++j) {
       const size_t row0 = sh->q_offset + i * s1;
@@ -643,29 +648,56 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
       ++jc;
       const double* kpj = kp + ((b * sh->Hkv + hk) * sh->S2 + j * s2) * d;
       const double* vj = vsc + j * s2 * d;
+      /* the K'-sum kernel: per head-dim index t, four FP32 chains over the keys
+       * (c % 4), ((a0 + a1) + (a2 + a3)), split hi = fl16(sum), lo = fl16(sum - hi) */
+      for (size_t t = 0; tcsum && t < d; ++t) {
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        size_t c = 0;
+        for (; c + 4 <= s2; c += 4)
+          for (int u = 0; u < 4; ++u) acc[u] += (float)kpj[(c + u) * d + t];
+        for (; c < s2; ++c) acc[0] += (float)kpj[c * d + t];
+        const float sum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        ksh[t] = fl16((double)sum);
+        ksl[t] = fl16((double)(sum - (float)ksh[t]));
+      }
       for (size_t r = 0; r < s1; ++r) {
         const double* qr = row_ptr(q, sh->Hq, sh->S1, d, b, h, i * s1 + r);
         const size_t pos = row0 + r;
         for (size_t c = 0; c < s2; ++c) S[c] = tc_dot(qr, 1, kpj + c * d, 1, d, mp->tc_mode);
-        /* Two threads per row (tile columns [0, 64) and [64, 128)); in each half
-         * eight FP32 chains: column c -> chain 2*((c/2)%4) + c%2 (the kernel's
-         * pair-register order), combined ((t0+t1)+(t2+t3)), t_r = a_2r + a_2r+1;
-         * the row total is half0 + half1. */
-        float sacc[2][8] = {{0.f}};
-        double mloc = -INFINITY;
-        for (size_t c = 0; c < s2; ++c) {
-          const int ch = 2 * (int)((c / 2) % 4) + (int)(c % 2);
-          sacc[c >= 64][ch] = sacc[c >= 64][ch] + (float)S[c];
+        /* Pseudo-average.  D <= 112 (pasa_tc_rowsum): from the tensor core,
+         * sum_c S'_c = q . ksum_j with the
+         * block's K' column sums split as (hi, lo) FP16 (the K'-sum kernel), each
+         * product exact, accumulated to FP32 (modelled as FP64 then one rounding),
+         * columns hi and lo added in FP32. */
+        float ssum;
+        if (tcsum) {
+          double ghi = 0.0, glo = 0.0;
+          for (size_t t = 0; t < d; ++t) {
+            ghi += qr[t] * ksh[t];
+            glo += qr[t] * ksl[t];
+          }
+          ssum = (float)ghi + (float)glo;
+        } else {
+          /* D = 128 (no free TMEM columns): two threads per row (tile columns [0, 64)
+           * and [64, 128)); in each half eight FP32 chains: column c -> chain
+           * 2*((c/2)%4) + c%2 (the kernel's pair-register order), combined
+           * ((t0+t1)+(t2+t3)), t_r = a_2r + a_2r+1; the row total is half0 + half1. */
+          float sacc[2][8] = {{0.f}};
+          for (size_t c = 0; c < s2; ++c) {
+            const int ch = 2 * (int)((c / 2) % 4) + (int)(c % 2);
+            sacc[c >= 64][ch] = sacc[c >= 64][ch] + (float)S[c];
+          }
+          float shalf[2];
+          for (int hh = 0; hh < 2; ++hh)
+            shalf[hh] = ((sacc[hh][0] + sacc[hh][1]) + (sacc[hh][2] + sacc[hh][3])) +
+                        ((sacc[hh][4] + sacc[hh][5]) + (sacc[hh][6] + sacc[hh][7]));
+          ssum = shalf[0] + shalf[1];
         }
+        double mloc = -INFINITY;
         for (size_t c = 0; c < s2; ++c) {
           const int masked = sh->causal && (j * s2 + c > pos);
           if (!masked && S[c] > mloc) mloc = S[c];
         }
-        float shalf[2];
-        for (int hh = 0; hh < 2; ++hh)
-          shalf[hh] = ((sacc[hh][0] + sacc[hh][1]) + (sacc[hh][2] + sacc[hh][3])) +
-                      ((sacc[hh][4] + sacc[hh][5]) + (sacc[hh][6] + sacc[hh][7]));
-        const float ssum = shalf[0] + shalf[1];
         const float sbar = ssum * (float)(1.0 / (double)s2);
         const float rcp = 1.0f / (float)jc; /* the kernel multiplies by 1/j */
         float fnew = (jc == 1) ? sbar : fbar[r] + (sbar - fbar[r]) * rcp;
@@ -711,7 +743,7 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
       const float invl = (1.0f / (l[2 * r] + l[2 * r + 1])) * ldexpf(1.0f, (int)c0);
       for (size_t n = 0; n < d; ++n) dst[n] = fl16((float)oacc[r * d + n] * invl);
     }
-    free(m); free(l); free(fbar); free(oacc); free(S); free(vsc);
+    free(m); free(l); free(fbar); free(oacc); free(S); free(vsc); free(ksh); free(ksl);
   }
   free(kp);
   return 0;

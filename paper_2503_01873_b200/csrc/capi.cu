@@ -20,8 +20,10 @@
 namespace pasa_b200 {
 cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stream);
 cudaError_t launch_vscale(const VscaleParams& p, cudaStream_t stream);
+cudaError_t launch_ksum(const void* kp, void* ks, int BH, int S2, int s2, int D, cudaStream_t stream);
 cudaError_t launch_fwd(int D, bool causal, int mode, const CUtensorMap& tq, const CUtensorMap& tk,
-                       const CUtensorMap& tv, const FwdParams& p, cudaStream_t stream);
+                       const CUtensorMap& tv, const CUtensorMap& tks, const FwdParams& p,
+                       cudaStream_t stream);
 cudaError_t launch_generate(const GenParams& p, void* out, cudaStream_t stream);
 cudaError_t launch_generate_resonance(const ResonanceParams& p, void* out, cudaStream_t stream);
 }  // namespace pasa_b200
@@ -243,6 +245,24 @@ int pasa_b200_preprocess(const pasa_b200_desc* d, const void* k, const void* v, 
   return PASA_B200_OK;
 }
 
+// Stream-ordered scratch comes from the device's default memory pool; keep its freed
+// blocks cached (release threshold = max) so a per-launch cudaMallocAsync is a pool hit,
+// not a fresh mapping.  Once per device.
+static void keep_pool_memory() {
+  static std::mutex mu;
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
+
 static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, const void* keys,
                           const void* v, const float* vmax, void* o, void* stream,
                           pasa_b200_diag* diag = nullptr) {
@@ -274,8 +294,26 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
   p.trace = g_trace;
   p.diag = diag;
   p.diag_scale = mode == kModePasa ? static_cast<float>(2.0 / kLog2e) : 1.0f;
-  cudaError_t e = launch_fwd(d->head_dim, d->causal != 0, mode, tq, tk, tv, p,
-                             static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // PASA at D = 64: the S' row sums come from the tensor core (pseudo-average GEMM
+  // against the block sums of K', pasa_tc_rowsum); the sums are a stream-ordered scratch
+  // of B Hkv (S2 / s2) 2 D halves (1.6 % of K' at s2 = 128).
+  CUtensorMap tks = tk;
+  void* ks = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (mode == kModePasa && pasa_tc_rowsum(d->head_dim)) {
+    const int bh = d->batch * d->heads_kv, nblk = d->seq_kv / d->s2;
+    keep_pool_memory();
+    e = cudaMallocAsync(&ks, static_cast<size_t>(bh) * nblk * 2 * d->head_dim * 2, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+    if ((rc = make_tmap(&tks, ks, d->head_dim, 2 * nblk, bh, 2))) {
+      cudaFreeAsync(ks, st);
+      return rc;
+    }
+    e = launch_ksum(keys, ks, bh, d->seq_kv, d->s2, d->head_dim, st);
+  }
+  if (e == cudaSuccess) e = launch_fwd(d->head_dim, d->causal != 0, mode, tq, tk, tv, tks, p, st);
+  if (ks) cudaFreeAsync(ks, st);
   if (e != cudaSuccess) return cuda_fail(e, "pasa_fwd launch");
   return PASA_B200_OK;
 }

@@ -79,6 +79,9 @@ static_assert(PASA_PPARTS_D64 == 1 || PASA_PPARTS_D64 == 2 || PASA_PPARTS_D64 ==
 // setmaxnreg split of the per-CTA register pool (640 x 96 = 61440 at launch):
 // warpgroup 0 (TMA, MMA, 2 idle warps) drops to PASA_WG0_REGS, the four softmax
 // warpgroups rise to PASA_SM_REGS; 128 * WG0 + 512 * SM <= 61440.
+#ifndef PASA_SPLIT_ISSUE_D64
+#define PASA_SPLIT_ISSUE_D64 1
+#endif
 #ifndef PASA_WG0_REGS
 #define PASA_WG0_REGS 56
 #endif
@@ -128,7 +131,12 @@ struct FwdCfg {
   static constexpr int SMEM_Q = 0;
   static constexpr int SMEM_K = SMEM_Q + NT * TILE_BYTES;
   static constexpr int SMEM_V = SMEM_K + KS * TILE_BYTES;
-  static constexpr int SMEM_BAR = SMEM_V + VS * TILE_BYTES;
+  // PASA with the tensor-core row sum (pasa_tc_rowsum): per K' stage the block sums
+  // as the N = 16 B operand of G, rows (hi, lo) of a zeroed 16-row box per 64 columns
+  static constexpr bool TCSUM = pasa_tc_rowsum(D);
+  static constexpr int KS_BOX = 2048;
+  static constexpr int SMEM_KS = SMEM_V + VS * TILE_BYTES;
+  static constexpr int SMEM_BAR = SMEM_KS + (TCSUM ? KS * NBOX * KS_BOX : 0);
   static constexpr int NUM_BARS = NT + 2 * KS + 2 * VS + (3 + kPParts<D>) * NT;
   static constexpr int HALVES = 2;  // threads per row: each owns 64 S' columns, D/2 outputs
   static constexpr int SMEM_XCH = SMEM_BAR + NUM_BARS * 8 + 16;  // row max/sum exchange
@@ -139,6 +147,7 @@ struct FwdCfg {
   static constexpr int THREADS = 128 + NT * HALVES * 128;  // WG0: TMA, MMA, 2 idle; 4 softmax WGs
   static constexpr uint32_t TMEM_COLS = 512;
   static constexpr uint32_t TMEM_TILE = 256;               // S/P at +0, T at +128
+  static constexpr uint32_t TM_G = 128 + D;                // G (TCSUM): 16 free columns after T
 };
 
 namespace {
@@ -302,7 +311,13 @@ template <int D, bool CAUSAL, int MODE, bool DIAGNOSE>
 __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     pasa_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_kp,
-                    const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
+                    const __grid_constant__ CUtensorMap tm_v,
+                    const __grid_constant__ CUtensorMap tm_ks, const FwdParams p) {
+  constexpr bool kTcSum = FwdCfg<D>::TCSUM && MODE == kModePasa;
+  // MMA issue: one warp for both tiles (PV of the first-ready tile, then its S'(j+1);
+  // best at D = 128, where an S' MMA queued ahead of the other tile's PV stalls it) or,
+  // at D = 64, one warp per tile (+5 %, tools/variants.py).
+  constexpr bool kSplitIssue = PASA_SPLIT_ISSUE_D64 && D == 64;
   using Cfg = FwdCfg<D>;
   constexpr int NT = Cfg::NT, KS = Cfg::KS, VS = Cfg::VS;
   extern __shared__ uint8_t smem_raw[];
@@ -347,13 +362,19 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     }
     for (int s = 0; s < KS; ++s) {
       mbar_init(k_full + 8 * (s), 1);
-      mbar_init(k_empty + 8 * (s), 1);
+      mbar_init(k_empty + 8 * (s), kSplitIssue ? NT : 1);  // one release per MMA issuer
     }
     for (int s = 0; s < VS; ++s) {
       mbar_init(v_full + 8 * (s), 1);
-      mbar_init(v_empty + 8 * (s), 1);
+      mbar_init(v_empty + 8 * (s), kSplitIssue ? NT : 1);
     }
     fence_barrier_init();
+  }
+  if (kTcSum) {  // rows 2-15 of the K'-sum boxes read as zero (TMA writes rows 0-1)
+    uint4* z = reinterpret_cast<uint4*>(smem + Cfg::SMEM_KS);
+    for (int e = threadIdx.x; e < KS * Cfg::NBOX * Cfg::KS_BOX / 16; e += blockDim.x)
+      z[e] = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (p.s2 < kTile) {
     // Short KV blocks: TMA fills rows [0, s2) of each stage, the rest must read as
@@ -383,6 +404,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       tma_prefetch(&tm_q);
       tma_prefetch(&tm_kp);
       tma_prefetch(&tm_v);
+      if (kTcSum) tma_prefetch(&tm_ks);
       for (int t = 0; t < NT; ++t) {
         if (!tl[t].valid) continue;
         mbar_expect_tx(q_full + 8 * (t), Cfg::TILE_BYTES);
@@ -393,10 +415,14 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       for (int j = 0; j < nmax; ++j) {
         const int ks = j % KS, vs = j % VS;
         mbar_wait(k_empty + 8 * (ks), ((j / KS) & 1) ^ 1);
-        mbar_expect_tx(k_full + 8 * (ks), Cfg::NBOX * 128 * p.s2);
-        for (int bx = 0; bx < Cfg::NBOX; ++bx)
+        mbar_expect_tx(k_full + 8 * (ks), Cfg::NBOX * 128 * (p.s2 + (kTcSum ? 2 : 0)));
+        for (int bx = 0; bx < Cfg::NBOX; ++bx) {
           tma_load_3d(sb + Cfg::SMEM_K + ks * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_kp,
                       k_full + 8 * (ks), bx * 64, j * p.s2, b * p.Hkv + hkv);
+          if (kTcSum)
+            tma_load_3d(sb + Cfg::SMEM_KS + (ks * Cfg::NBOX + bx) * Cfg::KS_BOX, &tm_ks,
+                        k_full + 8 * (ks), bx * 64, 2 * j, b * p.Hkv + hkv);
+        }
         mbar_wait(v_empty + 8 * (vs), ((j / VS) & 1) ^ 1);
         mbar_expect_tx(v_full + 8 * (vs), Cfg::NBOX * 128 * p.s2);
         for (int bx = 0; bx < Cfg::NBOX; ++bx)
@@ -404,11 +430,107 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
                       v_full + 8 * (vs), bx * 64, j * p.s2, b * p.Hkv + hkv);
       }
     }
-  } else if (warp == 1) {
+  } else if (kSplitIssue ? warp <= NT : warp == 1) {
+   if constexpr (kSplitIssue) {
+    // ------------------------------------------------------------ MMA issuers
+    // Warp 1 issues tile 0's MMAs, warp 2 tile 1's (tcgen05.commit tracks the issuing
+    // thread's MMAs), each a linear sequence with blocking waits, so neither tile's
+    // waits hold up the other's MMAs:
+    //   S'(0) [G(0)] | PV(0) parts, S'(1) [G(1)] | PV(1) parts, S'(2) [G(2)] | ...
+    // G(j) (tensor-core row sum, kTcSum): Q K'sum_j, M = 128, N = 16, FP32 accumulator,
+    // B rows = (hi, lo) of the block's K' column sums -> TMEM columns TM_G + {0, 1}.
+    const int t = warp - 1;
+    if (elect_one()) {
+      constexpr uint32_t kIdS = idesc_f16(128, 128, 0, 0, 0);  // F16 acc, K-major A/B
+      constexpr uint32_t kIdPV = idesc_f16(128, D, 0, 0, 1);   // F16 acc, V MN-major
+      constexpr uint32_t kIdG = idesc_f16(128, 16, 1, 0, 0);   // F32 acc, K-major A/B, N = 16
+      const uint32_t s_tmem = tmem_base + t * Cfg::TMEM_TILE;
+      const uint32_t o_tmem = s_tmem + 128;
+      const uint32_t qa = sb + Cfg::SMEM_Q + t * Cfg::TILE_BYTES;
+      auto issue_s = [&](int ks) {
+        const uint32_t ka = sb + Cfg::SMEM_K + ks * Cfg::TILE_BYTES;
+#pragma unroll
+        for (int s = 0; s < D / 16; ++s) {
+          const uint32_t off = (s / 4) * Cfg::BOX_BYTES + (s % 4) * 32;
+          umma_ss(s_tmem, smem_desc_sw128(qa + off, 16, 1024), smem_desc_sw128(ka + off, 16, 1024),
+                  kIdS, s > 0);
+        }
+        if (kTcSum) {
+          const uint32_t ga = sb + Cfg::SMEM_KS + ks * Cfg::NBOX * Cfg::KS_BOX;
+#pragma unroll
+          for (int s = 0; s < D / 16; ++s) {
+            const uint32_t qoff = (s / 4) * Cfg::BOX_BYTES + (s % 4) * 32;
+            const uint32_t goff = (s / 4) * Cfg::KS_BOX + (s % 4) * 32;
+            umma_ss(s_tmem + Cfg::TM_G, smem_desc_sw128(qa + qoff, 16, 1024),
+                    smem_desc_sw128(ga + goff, 16, 1024), kIdG, s > 0);
+          }
+        }
+      };
+      // PV in kPParts parts: part q covers the K-steps whose keys pass 2 stored in its
+      // part q (half h's pairs -> K-steps 4h + [q, q + 4/kPParts)), issued on p_part[q].
+      auto issue_pv = [&](int vs, int part) {
+        const uint32_t va = sb + Cfg::SMEM_V + vs * Cfg::TILE_BYTES;
+        constexpr int SP = 4 / kPParts<D>;  // K-steps per half per part
+#pragma unroll
+        for (int k = 0; k < 2 * SP; ++k) {
+          const int s = 4 * (k / SP) + part * SP + k % SP;
+          umma_ts(o_tmem, s_tmem + s * 8, smem_desc_sw128(va + s * 2048, Cfg::BOX_BYTES, 1024),
+                  kIdPV, part > 0 || k > 0);
+        }
+      };
+      const int nb = tl[t].nblk;
+      if (nb > 0) {
+        mbar_wait(q_full + 8 * t, 0);
+        mbar_wait(k_full, 0);
+        tc_fence_after();
+        issue_s(0);
+        tc_commit(s_full + 8 * t);
+        tc_commit(k_empty);
+      }
+      for (int j = 0; j < nb; ++j) {
+        const int vs = j % VS;
+        PASA_TR(2, j, 4 * t + 0);
+        mbar_wait(p_part + 8 * t, j & 1);
+        PASA_TR(2, j, 4 * t + 1);
+        mbar_wait(v_full + 8 * vs, (j / VS) & 1);
+        mbar_wait(t_empty + 8 * t, (j & 1) ^ 1);  // T(j-1) read
+        tc_fence_after();
+        issue_pv(vs, 0);
+        for (int q = 1; q < kPParts<D>; ++q) {
+          mbar_wait(p_part + 8 * (q * NT + t), j & 1);
+          tc_fence_after();
+          issue_pv(vs, q);
+        }
+        PASA_TR(2, j, 4 * t + 2);
+        tc_commit(t_full + 8 * t);
+        tc_commit(v_empty + 8 * vs);
+        if (j + 1 < nb) {
+          const int ks = (j + 1) % KS;
+          mbar_wait(k_full + 8 * ks, ((j + 1) / KS) & 1);
+          tc_fence_after();
+          issue_s(ks);
+          tc_commit(s_full + 8 * t);
+          tc_commit(k_empty + 8 * ks);
+          PASA_TR(2, j, 4 * t + 3);
+        }
+      }
+      // Blocks of the CTA this tile does not need (causal tiles differ in length):
+      // release their K'/V stages in the producer's order so it can proceed.
+      for (int j = nb; j < nmax; ++j) {
+        mbar_wait(k_empty + 8 * (j % KS), ((j / KS) & 1) ^ 1);
+        mbar_arrive(k_empty + 8 * (j % KS));
+        mbar_wait(v_empty + 8 * (j % VS), ((j / VS) & 1) ^ 1);
+        mbar_arrive(v_empty + 8 * (j % VS));
+      }
+    }
+   } else {
     // ------------------------------------------------------------ MMA issuer
     if (elect_one()) {
       constexpr uint32_t kIdS = idesc_f16(128, 128, 0, 0, 0);  // F16 acc, K-major A/B
       constexpr uint32_t kIdPV = idesc_f16(128, D, 0, 0, 1);   // F16 acc, V MN-major
+      // S'(j) and, with the tensor-core row sum, G(j) = Q K'sum_j (M = 128, N = 16, FP32
+      // accumulator; B rows = (hi, lo) of the block's K' column sums) -> this tile's S' row
+      // sums in TMEM columns TM_G + {0, 1}, committed together on s_full.
       auto issue_s = [&](int t, int ks) {
         const uint32_t d_tmem = tmem_base + t * Cfg::TMEM_TILE;
         const uint32_t qa = sb + Cfg::SMEM_Q + t * Cfg::TILE_BYTES;
@@ -418,6 +540,17 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
           const uint32_t off = (s / 4) * Cfg::BOX_BYTES + (s % 4) * 32;
           umma_ss(d_tmem, smem_desc_sw128(qa + off, 16, 1024), smem_desc_sw128(ka + off, 16, 1024),
                   kIdS, s > 0);
+        }
+        if (kTcSum) {
+          constexpr uint32_t kIdG = idesc_f16(128, 16, 1, 0, 0);
+          const uint32_t ga = sb + Cfg::SMEM_KS + ks * Cfg::NBOX * Cfg::KS_BOX;
+#pragma unroll
+          for (int s = 0; s < D / 16; ++s) {
+            const uint32_t qoff = (s / 4) * Cfg::BOX_BYTES + (s % 4) * 32;
+            const uint32_t goff = (s / 4) * Cfg::KS_BOX + (s % 4) * 32;
+            umma_ss(d_tmem + Cfg::TM_G, smem_desc_sw128(qa + qoff, 16, 1024),
+                    smem_desc_sw128(ga + goff, 16, 1024), kIdG, s > 0);
+          }
         }
       };
       // PV in kPParts parts: part q covers the K-steps whose keys pass 2 stored in its
@@ -488,6 +621,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         if (k_next) tc_commit(k_empty + 8 * ((j + 1) % KS));
       }
     }
+   }
   }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 " PASA_STR(PASA_SM_REGS) ";");
@@ -538,6 +672,8 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         tc_fence_after();
         tmem_ld_32cols_pack16(t_s + 64 * h, s);
         tmem_ld_32cols_pack16(t_s + 64 * h + 32, s + 16);
+        uint32_t g[2] = {0u, 0u};  // tensor-core row sum: this row's S' sum as hi and lo parts
+        if (kTcSum) tmem_ld_2cols_b32(t_s + Cfg::TM_G, g);
         tmem_wait_ld();
         if (tr) PASA_TR(t, j, 2);
         // masked columns: causal diagonal block (c > row) or a short KV block (c >= s2)
@@ -545,7 +681,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         const bool diag = cdiag || p.s2 < kTile;
         const int lim = cdiag ? row + 1 : p.s2;
         if (DIAGNOSE) track_store_block<NP>(s, lim, NP * h, diag, dslot);
-        constexpr bool kSum = MODE == kModePasa;
+        constexpr bool kSum = MODE == kModePasa && !kTcSum;
         float mh, sh = 0.f;
         if (diag) row_max_sum<true, NP, kSum>(s, lim, NP * h, mh, sh);
         else row_max_sum<false, NP, kSum>(s, lim, NP * h, mh, sh);
@@ -558,7 +694,9 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         uint32_t cj2, scale2 = 0;
         bool fast2 = true;  // PASA: the exp argument is one HFMA2 (see below)
         if (MODE == kModePasa) {
-          const float ssum = h == 0 ? __fadd_rn(sh, other.y) : __fadd_rn(other.y, sh);
+          // sum_c S'_c (pasa.cpp:131): the two halves' FP32 sums, or G's hi + lo columns
+          const float ssum = kTcSum ? __fadd_rn(__uint_as_float(g[0]), __uint_as_float(g[1]))
+                                    : (h == 0 ? __fadd_rn(sh, other.y) : __fadd_rn(other.y, sh));
           const float sbar = __fmul_rn(ssum, p.inv_s2);
           fnew = (jc == 1) ? sbar : __fadd_rn(fbar, __fmul_rn(__fsub_rn(sbar, fbar), rcp_j));
           const float dmc = __fmul_rn(p.inva, __fsub_rn(sbar, fnew));
@@ -708,7 +846,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
 // ---------------------------------------------------------------- launcher
 template <int D, bool CAUSAL, int MODE>
 cudaError_t launch_fwd_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                         const FwdParams& p, cudaStream_t stream) {
+                         const CUtensorMap& tks, const FwdParams& p, cudaStream_t stream) {
   using Cfg = FwdCfg<D>;
   // RunDiagnostics is a separate instantiation so the production kernel's schedule is
   // untouched by the diagnostic code.
@@ -718,14 +856,15 @@ cudaError_t launch_fwd_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
   if (e != cudaSuccess) return e;
   const int units = (p.tiles_per_kv + Cfg::NT - 1) / Cfg::NT;
   const dim3 grid = CAUSAL ? dim3(p.B * p.Hkv, units) : dim3(units, p.B * p.Hkv);
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(tq, tk, tv, p);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(tq, tk, tv, tks, p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fwd(int D, bool causal, int mode, const CUtensorMap& tq, const CUtensorMap& tk,
-                       const CUtensorMap& tv, const FwdParams& p, cudaStream_t stream) {
+                       const CUtensorMap& tv, const CUtensorMap& tks, const FwdParams& p,
+                       cudaStream_t stream) {
 #define PASA_LAUNCH(DD, CC, MM) \
-  if (D == DD && causal == CC && mode == MM) return launch_fwd_t<DD, CC, MM>(tq, tk, tv, p, stream);
+  if (D == DD && causal == CC && mode == MM) return launch_fwd_t<DD, CC, MM>(tq, tk, tv, tks, p, stream);
   PASA_LAUNCH(128, false, kModePasa)
   PASA_LAUNCH(128, true, kModePasa)
   PASA_LAUNCH(64, false, kModePasa)

@@ -48,6 +48,12 @@ struct VscaleParams {
 // 1/alpha scale is applied after the FP16 store, FP16 running max, no
 // pseudo-average shift and no O inflation -- the naive FP16 FlashAttention.
 enum FwdMode : int { kModePasa = 0, kModeFa16 = 1 };
+// PASA mode, head dims with free TMEM columns (S' 128 + T D <= 240 of a tile's 256):
+// the S' row sums come from the tensor core -- the pseudo-average GEMM G = Q K'sum_j
+// (M = 128, N = 16, FP32 accumulator) against the block sums of K' (pasa_ksum_kernel)
+// -- instead of 64 FP32 adds per thread and block.  At D = 128 all 512 columns are in use
+// and the sums stay on the CUDA cores.
+__host__ __device__ constexpr bool pasa_tc_rowsum(int D) { return 128 + D + 16 <= 256; }
 struct FwdParams {
   int B, Hq, Hkv, S1, S2;
   int nq, nkv, group;     // ceil(S1/128), S2/s2, Hq/Hkv

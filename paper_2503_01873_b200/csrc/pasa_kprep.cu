@@ -253,4 +253,32 @@ cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stre
   return cudaGetLastError();
 }
 
+// Block sums of K' for the fused kernel's pseudo-average GEMM:
+// ks[(bh, 2j + r), t], r = 0: hi = fl16(sum_c K'_j[c][t]), r = 1: lo = fl16(sum - hi),
+// the FP32 sum over the block's s2 keys.  One thread per head-dim index t.
+__global__ void pasa_ksum_kernel(const uint16_t* __restrict__ kp, uint16_t* __restrict__ ks,
+                                 int S2, int s2, int D) {
+  const int j = blockIdx.x, bh = blockIdx.y, t = threadIdx.x;
+  const __half* src = reinterpret_cast<const __half*>(kp) +
+                      (static_cast<size_t>(bh) * S2 + static_cast<size_t>(j) * s2) * D + t;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  int c = 0;
+  for (; c + 4 <= s2; c += 4)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] += __half2float(src[static_cast<size_t>(c + u) * D]);
+  for (; c < s2; ++c) acc[0] += __half2float(src[static_cast<size_t>(c) * D]);
+  const float sum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  const __half hi = __float2half_rn(sum);
+  const __half lo = __float2half_rn(sum - __half2float(hi));
+  __half* dst = reinterpret_cast<__half*>(ks) + (static_cast<size_t>(bh) * 2 * (S2 / s2) + 2 * j) * D + t;
+  dst[0] = hi;
+  dst[D] = lo;
+}
+
+cudaError_t launch_ksum(const void* kp, void* ks, int BH, int S2, int s2, int D, cudaStream_t stream) {
+  pasa_ksum_kernel<<<dim3(S2 / s2, BH), D, 0, stream>>>(static_cast<const uint16_t*>(kp),
+                                                        static_cast<uint16_t*>(ks), S2, s2, D);
+  return cudaGetLastError();
+}
+
 }  // namespace pasa_b200

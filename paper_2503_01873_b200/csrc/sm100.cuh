@@ -179,6 +179,12 @@ __device__ __forceinline__ void tmem_ld_16cols_b32(uint32_t taddr, uint32_t* r) 
         "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+// 32 lanes x 2 columns, 32-bit each (2 regs).
+__device__ __forceinline__ void tmem_ld_2cols_b32(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];"
+               : "=r"(r[0]), "=r"(r[1])
+               : "r"(taddr));
+}
 // 32 lanes x 8 columns of 32-bit registers.
 __device__ __forceinline__ void tmem_st_8cols_b32(uint32_t taddr, const uint32_t* r) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),

@@ -1,25 +1,41 @@
 """Build a variant of libpasa_b200.so with extra -D flags on pasa_fwd.cu (tool).
-    python tools/build_variant.py NAME [--src other_pasa_fwd.cu] -DPASA_POLY_EVERY=2 ...
-writes paper_2503_01873_b200/_build/NAME.so (for tools/variants.py); --src builds the
-fused kernel from another copy of pasa_fwd.cu (e.g. the previous commit's, for A/B runs)."""
-import os, subprocess, sys
+    python tools/build_variant.py NAME [--rev GIT_REV] -DPASA_POLY_EVERY=2 ...
+writes paper_2503_01873_b200/_build/NAME.so (for tools/variants.py).  --rev builds
+every CUDA source (and header) of the library as of another commit (e.g. HEAD for an
+A/B run of uncommitted changes against the last commit)."""
+import os, subprocess, sys, tempfile
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2503_01873_b200 import build as B  # noqa: E402
 name, flags = sys.argv[1], sys.argv[2:]
-src_fwd = os.path.join(B.CSRC, "pasa_fwd.cu")
-if flags[:1] == ["--src"]:
-    src_fwd, flags = os.path.abspath(flags[1]), flags[2:]
-B.build()
+rev = None
+if flags[:1] == ["--rev"]:
+    rev, flags = flags[1], flags[2:]
 out = os.path.join(B.OUT, "var_" + name)
 os.makedirs(out, exist_ok=True)
+csrc, inc = B.CSRC, os.path.join(ROOT, "include")
+if rev:
+    tmp = tempfile.mkdtemp(prefix="pasa_rev_")
+    csrc, inc = os.path.join(tmp, "pkg", "csrc"), os.path.join(tmp, "include")  # ../../include
+    os.makedirs(csrc), os.makedirs(inc)
+    for f in B.SOURCES + B.HEADERS:
+        rel = f"paper_2503_01873_b200/csrc/{f}"
+        open(os.path.join(csrc, f), "wb").write(
+            subprocess.run(["git", "-C", ROOT, "show", f"{rev}:{rel}"], check=True, capture_output=True).stdout)
+    open(os.path.join(inc, "pasa_b200.h"), "wb").write(
+        subprocess.run(["git", "-C", ROOT, "show", f"{rev}:include/pasa_b200.h"], check=True,
+                       capture_output=True).stdout)
+else:
+    B.build()
+flags_base = [f for f in B.FLAGS if f not in ("-Xptxas", "-v") and not f.startswith("-I")]
 objs = []
 for src in B.SOURCES:
     o = os.path.join(B.OUT, src.replace(".cu", ".o"))
-    if src == "pasa_fwd.cu":
-        o = os.path.join(out, "pasa_fwd.o")
-        subprocess.run([B.NVCC, *B.ARCH, *[f for f in B.FLAGS if f not in ("-Xptxas", "-v")], *flags,
-                        f"-I{B.CSRC}", "-c", src_fwd, "-o", o], check=True)
+    if rev or src == "pasa_fwd.cu":
+        o = os.path.join(out, src.replace(".cu", ".o"))
+        subprocess.run([B.NVCC, *B.ARCH, *flags_base, f"-I{inc}", f"-I{csrc}",
+                        *(flags if src == "pasa_fwd.cu" else []),
+                        "-c", os.path.join(csrc, src), "-o", o], check=True)
     objs.append(o)
 subprocess.run([B.NVCC, *B.ARCH, "-shared", "-cudart", "static", "-o",
                 os.path.join(B.OUT, name + ".so"), *objs], check=True)

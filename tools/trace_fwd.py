@@ -29,13 +29,14 @@ def main():
     ap.add_argument("--hq", type=int, default=28)
     ap.add_argument("--hkv", type=int, default=4)
     ap.add_argument("--causal", type=int, default=1)
+    ap.add_argument("--d", type=int, default=128)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "trace.json"))
     a = ap.parse_args()
     from paper_2503_01873_b200 import _lib
     lib = _lib.load(os.path.join(ROOT, "paper_2503_01873_b200", "_build", "libpasa_b200_trace.so"))
     lib.pasa_b200_debug_set_trace.argtypes = [C.c_void_p]
     dev = torch.device("cuda:0")
-    S, D = a.seq, 128
+    S, D = a.seq, a.d
     q = torch.randn(1, a.hq, S, D, device=dev).half()
     k = torch.randn(1, a.hkv, S, D, device=dev).half()
     v = torch.randn(1, a.hkv, S, D, device=dev).half()
