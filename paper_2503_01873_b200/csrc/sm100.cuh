@@ -232,16 +232,6 @@ __host__ __device__ constexpr uint32_t idesc_f16(uint32_t M, uint32_t N, uint32_
          ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
-// shared-memory float2 store / load at a 32-bit shared address
-__device__ __forceinline__ void st_shared_f2(uint32_t addr, float x, float y) {
-  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(x), "f"(y) : "memory");
-}
-__device__ __forceinline__ float2 ld_shared_f2(uint32_t addr) {
-  float2 r;
-  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "r"(addr) : "memory");
-  return r;
-}
-
 // ---------------------------------------------------------------- f16 helpers
 __device__ __forceinline__ uint32_t h2_as_u32(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 __device__ __forceinline__ __half2 u32_as_h2(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }

@@ -27,11 +27,18 @@ def setup(L, B, Hq, Hkv, S, D, causal):
     return (d, q, kp, vp, vmax, o, st)
 
 
+FA16 = False  # --fa16: time the beta = 0 naive FP16 FlashAttention mode instead
+
+
 def time_once(L, args, n=10):
     d, q, kp, vp, vmax, o, st = args
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(n):
+        if FA16:  # raw K, V (kp, vp hold the pre-pass output; any K/V of the shape times alike)
+            assert L.pasa_b200_flash_fp16_fwd(C.byref(d), q.data_ptr(), kp.data_ptr(),
+                                              vp.data_ptr(), o.data_ptr(), st) == 0
+            continue
         assert L.pasa_b200_attention_fwd_prepped(C.byref(d), q.data_ptr(), kp.data_ptr(),
                                                  vp.data_ptr(), vmax.data_ptr(), o.data_ptr(), st) == 0
     e1.record()
@@ -42,13 +49,17 @@ def time_once(L, args, n=10):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rounds", type=int, default=5)
+    ap.add_argument("--fa16", action="store_true")
     ap.add_argument("libs", nargs="+")
     a = ap.parse_args()
+    global FA16
+    FA16 = a.fa16
     libs = []
     for so in a.libs:
         L = C.CDLL(os.path.join(ROOT, "paper_2503_01873_b200", "_build", so))
         L.pasa_b200_preprocess.argtypes = [C.POINTER(_lib.Desc)] + [C.c_void_p] * 6
         L.pasa_b200_attention_fwd_prepped.argtypes = [C.POINTER(_lib.Desc)] + [C.c_void_p] * 6
+        L.pasa_b200_flash_fp16_fwd.argtypes = [C.POINTER(_lib.Desc)] + [C.c_void_p] * 5
         libs.append(L)
     res = {so: [] for so in a.libs}
     for name, B, Hq, Hkv, S, D, causal in CFGS:
