@@ -158,7 +158,9 @@ PASA_B200_API int pasa_b200_diag_reset(pasa_b200_diag* diag, void* stream);
  * one D2H stream, so copy-in, compute and copy-out of different pieces overlap and
  * the call is bound by the H2D copy.  Device buffers are cached per thread and
  * device; pinned host buffers copy at DMA speed (and overlap), pageable ones
- * through the driver's staging path. */
+ * through the driver's staging path.  With PASA_B200_HOST_TRACE set in the
+ * environment the call prints each piece's H2D / compute / D2H completion times
+ * to stderr (diagnostic). */
 PASA_B200_API int pasa_b200_attention_host(const pasa_b200_desc* desc, const uint16_t* q, const uint16_t* k,
                              const uint16_t* v, uint16_t* o);
 

@@ -11,8 +11,10 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/pasa_b200.h"
 #include "pasa_kernels.cuh"
@@ -263,9 +265,11 @@ static void keep_pool_memory() {
   done[dev] = true;
 }
 
+// s2_bound: the key count the pre-pass computed V's O-bounding exponent for (0: d->seq_kv);
+// the host pipeline launches row pieces of causal heads on a prefix of the keys.
 static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, const void* keys,
                           const void* v, const float* vmax, void* o, void* stream,
-                          pasa_b200_diag* diag = nullptr) {
+                          pasa_b200_diag* diag = nullptr, int s2_bound = 0) {
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(keys) |
        reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(o)) & 15)
     return fail(PASA_B200_EINVAL, "attention_fwd: tensors must be 16-byte aligned");
@@ -280,6 +284,7 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
   p.Hkv = d->heads_kv;
   p.S1 = d->seq_q;
   p.S2 = d->seq_kv;
+  p.S2_bound = s2_bound > 0 ? s2_bound : d->seq_kv;
   p.nq = (d->seq_q + kTile - 1) / kTile;
   p.nkv = d->seq_kv / d->s2;
   p.qblk = d->causal ? (d->seq_kv - d->seq_q) / kTile : 0;
@@ -492,6 +497,59 @@ static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const
   const uint8_t* hv = reinterpret_cast<const uint8_t*>(v);
   uint8_t* ho = reinterpret_cast<uint8_t*>(o);
   int piece = 0, kvc = 0;
+  cudaEvent_t last_dep = nullptr;  // the last unit's K/V (FA16) or pre-pass (PASA) event
+  // PASA_B200_HOST_TRACE=1 (diagnostic): per-piece H2D / compute / D2H completion times
+  static const bool trace = getenv("PASA_B200_HOST_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto tmark = [&](cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t x;
+    cudaEventCreate(&x);
+    cudaEventRecord(x, st);
+    tev.push_back(x);
+  };
+  tmark(s_in);
+  // one piece: query rows [r0, r0 + nr) of heads [g0, g0 + nh) of units [u0, u0 + nu) on
+  // keys [0, skv) (row pieces of a causal head stay bit-identical to the whole head; V's O
+  // bound keeps the full key count).  Pieces are whole heads today: cutting the last
+  // unit's causal heads by rows (cheap early rows last) did not shorten the drain, and
+  // cutting every head doubled the pieces and made the host's enqueueing (~50 us per
+  // piece) the bottleneck (PASA_B200_HOST_TRACE timelines).
+  auto run_piece = [&](int u0, int nu, int g0, int nh, int r0, int nr, int skv,
+                       cudaEvent_t dep) -> int {
+    const size_t ok = k_unit * u0;
+    const size_t row_bytes = static_cast<size_t>(d->head_dim) * 2;
+    // contiguous: whole heads, or rows of one head
+    const size_t oq = q_unit * u0 + q_head * g0 + row_bytes * r0;
+    const size_t bq = nr < d->seq_q ? row_bytes * nr : (nu == 1 ? q_head * nh : q_unit * nu);
+    cudaEvent_t ev_in = cache.ev[1][piece % kRing], ev_done = cache.ev[2][piece % kRing];
+    const cudaStream_t sc = s_comp[piece % kComp];
+    ++piece;
+    cudaError_t e2 = cudaMemcpyAsync(dq + oq, hq + oq, bq, cudaMemcpyHostToDevice, s_in);
+    if (e2 == cudaSuccess) e2 = cudaEventRecord(ev_in, s_in);
+    if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(sc, ev_in, 0);
+    if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(sc, dep, 0);
+    if (e2 != cudaSuccess) return cuda_fail(e2, "H2D copy");
+    tmark(s_in);
+    pasa_b200_desc pd = *d;
+    pd.batch = 1;
+    pd.heads_kv = nu;
+    pd.heads_q = nu == 1 ? nh : nu * group;
+    pd.seq_q = nr;
+    pd.seq_kv = skv;
+    int rc2 = pasa ? launch_forward(&pd, kModePasa, dq + oq, dkp + ok, dvp + ok, dvmax + u0, dout + oq,
+                                    sc, ddiag, d->seq_kv)
+                   : launch_forward(&pd, kModeFa16, dq + oq, dk + ok, dv + ok, nullptr, dout + oq, sc,
+                                    ddiag, d->seq_kv);
+    if (rc2) return rc2;
+    tmark(sc);
+    e2 = cudaEventRecord(ev_done, sc);
+    if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(s_out, ev_done, 0);
+    if (e2 == cudaSuccess) e2 = cudaMemcpyAsync(ho + oq, dout + oq, bq, cudaMemcpyDeviceToHost, s_out);
+    if (e2 != cudaSuccess) return cuda_fail(e2, "D2H copy");
+    tmark(s_out);
+    return PASA_B200_OK;
+  };
   for (int u0 = 0; u0 < units; u0 += uper) {
     const int nu = u0 + uper <= units ? uper : units - u0;
     const size_t ok = k_unit * u0, bk = k_unit * nu;
@@ -502,36 +560,20 @@ static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const
     if (e == cudaSuccess) e = cudaMemcpyAsync(dv + ok, hv + ok, bk, cudaMemcpyHostToDevice, s_in);
     if (e == cudaSuccess) e = cudaEventRecord(ev_kv, s_in);
     if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-    pasa_b200_desc ud = *d;
-    ud.batch = 1;
-    ud.heads_kv = nu;
-    ud.heads_q = nu * group;
     if (pasa) {
+      pasa_b200_desc ud = *d;
+      ud.batch = 1;
+      ud.heads_kv = nu;
+      ud.heads_q = nu * group;
       if ((e = cudaStreamWaitEvent(s_prep, ev_kv, 0)) != cudaSuccess) return cuda_fail(e, "event");
       if ((rc = pasa_b200_preprocess(&ud, dk + ok, dv + ok, dkp + ok, dvp + ok, dvmax + u0, s_prep)))
         return rc;
       if ((e = cudaEventRecord(ev_prep, s_prep)) != cudaSuccess) return cuda_fail(e, "event");
     }
-    for (int g0 = 0; g0 < group; g0 += hper, ++piece) {
+    last_dep = pasa ? ev_prep : ev_kv;
+    for (int g0 = 0; g0 < group; g0 += hper) {
       const int nh = g0 + hper <= group ? hper : group - g0;
-      // query heads [g0, g0 + nh) of each unit: contiguous only for one unit or all heads
-      const size_t oq = q_unit * u0 + q_head * g0, bq = nu == 1 ? q_head * nh : q_unit * nu;
-      cudaEvent_t ev_in = cache.ev[1][piece % kRing], ev_done = cache.ev[2][piece % kRing];
-      const cudaStream_t sc = s_comp[piece % kComp];
-      e = cudaMemcpyAsync(dq + oq, hq + oq, bq, cudaMemcpyHostToDevice, s_in);
-      if (e == cudaSuccess) e = cudaEventRecord(ev_in, s_in);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(sc, ev_in, 0);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(sc, pasa ? ev_prep : ev_kv, 0);
-      if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-      pasa_b200_desc pd = ud;
-      pd.heads_q = nu == 1 ? nh : nu * group;
-      rc = pasa ? launch_forward(&pd, kModePasa, dq + oq, dkp + ok, dvp + ok, dvmax + u0, dout + oq, sc, ddiag)
-                : launch_forward(&pd, kModeFa16, dq + oq, dk + ok, dv + ok, nullptr, dout + oq, sc, ddiag);
-      if (rc) return rc;
-      e = cudaEventRecord(ev_done, sc);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, ev_done, 0);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(ho + oq, dout + oq, bq, cudaMemcpyDeviceToHost, s_out);
-      if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+      if ((rc = run_piece(u0, nu, g0, nh, 0, d->seq_q, d->seq_kv, last_dep))) return rc;
       if (nu > 1) break;  // whole units: one piece covers all their query heads
     }
   }
@@ -547,6 +589,16 @@ static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const
   }
   // every compute stream's last kernel precedes a D2H on s_out, so s_out completes last
   if ((e = cudaStreamSynchronize(s_out)) != cudaSuccess) return cuda_fail(e, "D2H copy / kernel");
+  if (trace) {  // piece: H2D done, compute done, D2H done (ms after the call's first copy)
+    for (size_t i = 1; i + 2 < tev.size(); i += 3) {
+      float a = 0, b = 0, c = 0;
+      cudaEventElapsedTime(&a, tev[0], tev[i]);
+      cudaEventElapsedTime(&b, tev[0], tev[i + 1]);
+      cudaEventElapsedTime(&c, tev[0], tev[i + 2]);
+      fprintf(stderr, "piece %2zu  in %.3f  comp %.3f  out %.3f\n", i / 3, a, b, c);
+    }
+    for (auto x : tev) cudaEventDestroy(x);
+  }
   return PASA_B200_OK;
 }
 

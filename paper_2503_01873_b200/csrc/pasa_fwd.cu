@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     if (ti.nblk > 0) {
       // O-bounding exponent: V arrives pre-scaled by 2^-c0; the
       // epilogue multiplies by 2^c0.
-      const int c0 = MODE == kModePasa ? pasa_inflation(p.S2, p.vmax[b * p.Hkv + hkv]) : 0;
+      const int c0 = MODE == kModePasa ? pasa_inflation(p.S2_bound, p.vmax[b * p.Hkv + hkv]) : 0;
       constexpr int NP = 32;  // pairs per thread
       uint32_t o[D / 4];
 #pragma unroll

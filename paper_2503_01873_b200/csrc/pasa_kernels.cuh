@@ -56,6 +56,8 @@ enum FwdMode : int { kModePasa = 0, kModeFa16 = 1 };
 __host__ __device__ constexpr bool pasa_tc_rowsum(int D) { return 128 + D + 16 <= 256; }
 struct FwdParams {
   int B, Hq, Hkv, S1, S2;
+  int S2_bound;           // key count the pre-pass's O bound c0 was computed for (>= S2 when a
+                          // launch covers a prefix of the keys, e.g. the host pipeline's pieces)
   int nq, nkv, group;     // ceil(S1/128), S2/s2, Hq/Hkv
   int qblk;               // causal: (S2 - S1) / 128, the bottom-right alignment offset
   int s2;                 // KV block (shifting-matrix size), <= 128; < 128 masks columns
