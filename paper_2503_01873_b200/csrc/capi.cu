@@ -32,6 +32,32 @@ cudaError_t launch_generate_resonance(const ResonanceParams& p, void* out, cudaS
 
 using namespace pasa_b200;
 
+// Stream-ordered scratch (the K' block sums of the d = 64 path) comes from a memory pool
+// the library owns, one per device, whose freed blocks stay cached (release threshold =
+// max): a per-launch allocation is then a pool hit, not a fresh mapping (which cost
+// 2.8 ms per launch), and the process's default pool is left untouched.
+static cudaMemPool_t scratch_pool() {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return nullptr;
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    pools[dev] = pool;
+  }
+  return pools[dev];
+}
+
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -170,9 +196,11 @@ static int preprocess_impl(const pasa_b200_desc* d, const void* k, const void* v
   p.kp = static_cast<uint16_t*>(kp);
   float* scratch = nullptr;
   if (!vmax) {
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch),
-                                    static_cast<size_t>(d->batch) * d->heads_kv * 4, st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+    cudaMemPool_t pool = scratch_pool();
+    if (!pool) return fail(PASA_B200_ECUDA, "cudaMemPoolCreate failed");
+    cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&scratch),
+                                    static_cast<size_t>(d->batch) * d->heads_kv * 4, pool, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocFromPoolAsync");
   }
   p.vmax = vmax ? vmax : scratch;
   p.S2 = d->seq_kv;
@@ -247,26 +275,6 @@ int pasa_b200_preprocess(const pasa_b200_desc* d, const void* k, const void* v, 
   return PASA_B200_OK;
 }
 
-// Stream-ordered scratch comes from the device's default memory pool; keep its freed
-// blocks cached (release threshold = max) so a per-launch cudaMallocAsync is a pool hit,
-// not a fresh mapping.  Once per device.
-static void keep_pool_memory() {
-  static std::mutex mu;
-  static bool done[64] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
-  std::lock_guard<std::mutex> lock(mu);
-  if (done[dev]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t keep = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-  }
-  done[dev] = true;
-}
-
-// s2_bound: the key count the pre-pass computed V's O-bounding exponent for (0: d->seq_kv);
-// the host pipeline launches row pieces of causal heads on a prefix of the keys.
 static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, const void* keys,
                           const void* v, const float* vmax, void* o, void* stream,
                           pasa_b200_diag* diag = nullptr, int s2_bound = 0) {
@@ -302,15 +310,16 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // PASA at D = 64: the S' row sums come from the tensor core (pseudo-average GEMM
   // against the block sums of K', pasa_tc_rowsum); the sums are a stream-ordered scratch
-  // of B Hkv (S2 / s2) 2 D halves (1.6 % of K' at s2 = 128).
+  // of B Hkv (S2 / s2) 2 D halves (1.6 % of K' at s2 = 128) from the library's pool.
   CUtensorMap tks = tk;
   void* ks = nullptr;
   cudaError_t e = cudaSuccess;
   if (mode == kModePasa && pasa_tc_rowsum(d->head_dim)) {
     const int bh = d->batch * d->heads_kv, nblk = d->seq_kv / d->s2;
-    keep_pool_memory();
-    e = cudaMallocAsync(&ks, static_cast<size_t>(bh) * nblk * 2 * d->head_dim * 2, st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+    cudaMemPool_t pool = scratch_pool();
+    if (!pool) return fail(PASA_B200_ECUDA, "cudaMemPoolCreate failed");
+    e = cudaMallocFromPoolAsync(&ks, static_cast<size_t>(bh) * nblk * 2 * d->head_dim * 2, pool, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocFromPoolAsync");
     if ((rc = make_tmap(&tks, ks, d->head_dim, 2 * nblk, bh, 2))) {
       cudaFreeAsync(ks, st);
       return rc;
@@ -485,8 +494,11 @@ static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const
   cudaStream_t s_in = cache.st[0], s_prep = cache.st[1], s_out = cache.st[2];
   const cudaStream_t* s_comp = cache.st + 3;
   if (hdiag) {
-    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&ddiag), sizeof(pasa_b200_diag), s_prep)))
-      return cuda_fail(e, "cudaMallocAsync");
+    cudaMemPool_t pool = scratch_pool();
+    if (!pool) return fail(PASA_B200_ECUDA, "cudaMemPoolCreate failed");
+    if ((e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&ddiag), sizeof(pasa_b200_diag), pool,
+                                     s_prep)))
+      return cuda_fail(e, "cudaMallocFromPoolAsync");
     if ((rc = pasa_b200_diag_reset(ddiag, s_prep))) return rc;
     if ((e = cudaEventRecord(cache.prep[0], s_prep)) != cudaSuccess) return cuda_fail(e, "event");
     for (int c = 0; c < kComp; ++c)
