@@ -614,9 +614,9 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
   const double xs = mp->xscale > 0.0 ? mp->xscale : 1.0;
   const int nt = resolve_threads(threads);
   double* kp = malloc(sizeof(double) * sh->B * sh->Hkv * sh->S2 * d);
-  /* the kernel's pre-pass: rank-1 form for full blocks, FP32 chains for s2 < 128 */
+  /* the kernel's pre-pass: the rank-1 form (any block size) */
   orc_preprocess_keys(k, sh->B, sh->Hkv, sh->S2, d, s2, mp->diag, mp->off,
-                      (L != 1.0 && s2 == 128) ? PR1 : P32, P16, L, kp, nt);
+                      L != 1.0 ? PR1 : P32, P16, L, kp, nt);
 #pragma omp parallel for num_threads(nt) schedule(dynamic)
   for (long long x = 0; x < (long long)(sh->B * sh->Hq * nq); ++x) {
     const size_t i = (size_t)x % nq;

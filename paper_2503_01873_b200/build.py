@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "_build")
 SO = os.path.join(OUT, "libpasa_b200.so")
-SOURCES = ["capi.cu", "pasa_kprep.cu", "pasa_fwd.cu", "pasa_gen.cu"]
+SOURCES = ["capi.cu", "pasa_kprep.cu", "pasa_fwd.cu", "pasa_fwd_packed.cu", "pasa_gen.cu"]
 HEADERS = ["sm100.cuh", "pasa_kernels.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -23,6 +23,8 @@ namespace pasa_b200 {
 cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stream);
 cudaError_t launch_vscale(const VscaleParams& p, cudaStream_t stream);
 cudaError_t launch_ksum(const void* kp, void* ks, int BH, int S2, int s2, int D, cudaStream_t stream);
+cudaError_t launch_fwd_packed(int D, int mode, const CUtensorMap& tq, const CUtensorMap& tk,
+                              const CUtensorMap& tv, const PackedParams& p, cudaStream_t stream);
 cudaError_t launch_fwd(int D, bool causal, int mode, const CUtensorMap& tq, const CUtensorMap& tk,
                        const CUtensorMap& tv, const CUtensorMap& tks, const FwdParams& p,
                        cudaStream_t stream);
@@ -208,7 +210,7 @@ static int preprocess_impl(const pasa_b200_desc* d, const void* k, const void* v
   p.diag = __half2float(dg);
   p.off = __half2float(of);
   p.lscale = lscale;
-  p.rank1 = rank1 && d->s2 == kTile;
+  p.rank1 = rank1;  // the fused path: rank-1 form for any block size
   cudaError_t e = cudaMemsetAsync(p.vmax, 0, static_cast<size_t>(d->batch) * d->heads_kv * 4, st);
   if (e == cudaSuccess) e = launch_kprep(p, d->batch, d->heads_kv, st);
   if (scratch) cudaFreeAsync(scratch, st);
@@ -283,6 +285,25 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
     return fail(PASA_B200_EINVAL, "attention_fwd: tensors must be 16-byte aligned");
   int rc;
   CUtensorMap tq, tk, tv;
+  // Short sequences (one KV block each, N <= 64): packed P = 128 / N per tensor-core tile
+  if (!diag && !d->causal && d->heads_q == d->heads_kv && d->seq_q == d->seq_kv &&
+      d->seq_kv == d->s2 && d->s2 <= 64 && (s2_bound <= 0 || s2_bound == d->seq_kv)) {
+    const int bh = d->batch * d->heads_q, rows = bh * d->seq_q, n = d->seq_q;
+    if ((rc = make_tmap(&tq, q, d->head_dim, rows, 1, n))) return rc;
+    if ((rc = make_tmap(&tk, keys, d->head_dim, rows, 1, n))) return rc;
+    if ((rc = make_tmap(&tv, v, d->head_dim, rows, 1, n))) return rc;
+    PackedParams pp{};
+    pp.BH = bh;
+    pp.N = n;
+    pp.W = 16 * ((n + 15) / 16);
+    pp.P = kTile / pp.W;
+    pp.qk_scale = static_cast<float>(kLog2e / d->alpha);
+    pp.vmax = vmax;
+    pp.out = static_cast<uint16_t*>(o);
+    cudaError_t e = launch_fwd_packed(d->head_dim, mode, tq, tk, tv, pp, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "pasa_fwd_packed launch");
+    return PASA_B200_OK;
+  }
   if ((rc = make_tmap(&tq, q, d->head_dim, d->seq_q, d->batch * d->heads_q))) return rc;
   if ((rc = make_tmap(&tk, keys, d->head_dim, d->seq_kv, d->batch * d->heads_kv, d->s2))) return rc;
   if ((rc = make_tmap(&tv, v, d->head_dim, d->seq_kv, d->batch * d->heads_kv, d->s2))) return rc;

@@ -1,0 +1,246 @@
+// pasa_fwd_packed.cu -- PASA forward for short sequences (one KV block per sequence:
+// S1 = S2 = s2 = N <= 64, e.g. the SVD temporal attention with N = 25 frames), packed
+// in 16-aligned slots, 128 / (16 ceil(N / 16)) sequences to a 128-row tensor-core tile.
+//
+// With a single KV block the PASA recursion (pasa.cpp:117-194) collapses: j = 1, so
+// F = S'bar, both corrections are zero and m = m' -- the output is the softmax of the
+// shifted scores S' = fl16(Q K'^T) of the sequence, computed exactly like the fused
+// kernel's first block (pasa_fwd.cu; numerics DESIGN.md section 4): P = fl16(2^(2 S' - 2 m'))
+// (K' carries log2(e)/2), T = P V' with an F16 accumulator, O = T 2^c0 / l.  The
+// pseudo-average drops out of the result and is not computed.  FA16 mode (beta = 0) is
+// the naive FP16 FlashAttention's single block (attention.cpp:92-180).
+//
+// Layout: Q, K', V' (and O) are flat [B H N, d] row matrices.  Tile i holds sequences
+// [i P, i P + P), sequence s of the tile in the 16-aligned slot of rows / keys
+// [s W, s W + N), W = 16 ceil(N / 16), P = 128 / W (one TMA box of N rows per sequence;
+// V' gaps are zero).  Each row attends only to the N keys of its own slot (block-diagonal
+// mask within the 128 x 128 S').  Because every slot starts on a 16-key boundary, the
+// tensor core's F16 accumulation chunks and the row-sum chains see a sequence exactly as
+// the fused kernel does when the sequence is alone: the output is bit-identical to
+// pasa_fwd.cu's, whatever the packing (host pipeline pieces, multi-GPU shards).
+//
+// One CTA per tile, 5 warps: warp 0 loads (TMA) and issues the MMAs, warps 1-4 run the
+// softmax with one thread per row (TMEM lane quadrant = warp % 4).  256 TMEM columns (S'/P
+// at +0, T at +128), so two CTAs share an SM.
+#include <cuda.h>
+#include <cuda_fp16.h>
+
+#include "pasa_kernels.cuh"
+#include "sm100.cuh"
+
+namespace pasa_b200 {
+using namespace sm100;
+
+namespace {
+
+template <int D>
+struct PackedCfg {
+  static constexpr int NBOX = D / 64;
+  static constexpr int BOX_BYTES = kTile * 128;
+  static constexpr int TILE_BYTES = NBOX * BOX_BYTES;
+  static constexpr int SMEM_Q = 0, SMEM_K = TILE_BYTES, SMEM_V = 2 * TILE_BYTES;
+  static constexpr int SMEM_BAR = 3 * TILE_BYTES;
+  static constexpr int SMEM_USED = SMEM_BAR + 64 + 1024;
+  // at least 80 KB so at most two CTAs (= 2 x 256 TMEM columns) are resident per SM
+  static constexpr int SMEM_BYTES = SMEM_USED > 80 * 1024 ? SMEM_USED : 80 * 1024;
+  static constexpr int THREADS = 160;
+};
+
+__device__ __forceinline__ float lo_f(uint32_t u) { return __low2float(u32_as_h2(u)); }
+__device__ __forceinline__ float hi_f(uint32_t u) { return __high2float(u32_as_h2(u)); }
+
+// keep lo / hi of the pair of columns (2i, 2i + 1) that fall in [lo, hi)
+__device__ __forceinline__ uint32_t range_keep(int i, int lo, int hi) {
+  const uint32_t a = (2 * i >= lo && 2 * i < hi) ? 0x0000FFFFu : 0u;
+  const uint32_t b = (2 * i + 1 >= lo && 2 * i + 1 < hi) ? 0xFFFF0000u : 0u;
+  return a | b;
+}
+
+}  // namespace
+
+template <int D, int MODE>
+__global__ void __launch_bounds__(PackedCfg<D>::THREADS, 1)
+    pasa_fwd_packed_kernel(const __grid_constant__ CUtensorMap tm_q,
+                           const __grid_constant__ CUtensorMap tm_kp,
+                           const __grid_constant__ CUtensorMap tm_v, const PackedParams p) {
+  using Cfg = PackedCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t sb = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (sb - smem_u32(smem_raw));
+  const uint32_t in_full = sb + Cfg::SMEM_BAR, s_full = in_full + 8, p_full = in_full + 16,
+                 t_full = in_full + 24;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Cfg::SMEM_BAR + 32);
+  const int warp = static_cast<int>(warp_id());
+  const int lane = threadIdx.x & 31;
+  const int tile = blockIdx.x;
+  const int seq0 = tile * p.P;                      // first sequence of the tile
+  const int nseq = min(p.P, p.BH - seq0);           // sequences in this tile
+  const int W = p.W;                                // slot stride (rows / keys)
+
+  if (threadIdx.x == 0) {
+    mbar_init(in_full, 1);
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 4);
+    mbar_init(t_full, 1);
+    fence_barrier_init();
+  }
+  {  // V' rows outside the sequences' N-row slots must read as zero (P = 0 there, and 0 x
+     // stale shared memory could be NaN); the TMA writes below land after this
+    uint4* z = reinterpret_cast<uint4*>(smem + Cfg::SMEM_V);
+    for (int e = threadIdx.x; e < Cfg::TILE_BYTES / 16; e += blockDim.x) z[e] = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc<256>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // ---- loads: each sequence's N rows of Q, K', V' into its slot (boxes of N rows)
+      mbar_expect_tx(in_full, 3 * Cfg::NBOX * nseq * p.N * 128);
+      for (int sl = 0; sl < nseq; ++sl) {
+        const int r = (seq0 + sl) * p.N;  // flat row of the sequence
+        for (int bx = 0; bx < Cfg::NBOX; ++bx) {
+          const uint32_t off = bx * Cfg::BOX_BYTES + sl * W * 128;
+          tma_load_3d(sb + Cfg::SMEM_Q + off, &tm_q, in_full, bx * 64, r, 0);
+          tma_load_3d(sb + Cfg::SMEM_K + off, &tm_kp, in_full, bx * 64, r, 0);
+          tma_load_3d(sb + Cfg::SMEM_V + off, &tm_v, in_full, bx * 64, r, 0);
+        }
+      }
+      mbar_wait(in_full, 0);
+      tc_fence_after();
+      // ---- S' = Q K'^T (SS, F16 accumulator) into columns [0, 128)
+      constexpr uint32_t kIdS = idesc_f16(128, 128, 0, 0, 0);
+#pragma unroll
+      for (int s = 0; s < D / 16; ++s) {
+        const uint32_t off = (s / 4) * Cfg::BOX_BYTES + (s % 4) * 32;
+        umma_ss(tmem_base, smem_desc_sw128(sb + Cfg::SMEM_Q + off, 16, 1024),
+                smem_desc_sw128(sb + Cfg::SMEM_K + off, 16, 1024), kIdS, s > 0);
+      }
+      tc_commit(s_full);
+      // ---- T = P V' (TS: P packed in columns [0, 64), V' MN-major) into [128, 128 + D)
+      mbar_wait(p_full, 0);
+      tc_fence_after();
+      constexpr uint32_t kIdPV = idesc_f16(128, D, 0, 0, 1);
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        umma_ts(tmem_base + 128, tmem_base + s * 8,
+                smem_desc_sw128(sb + Cfg::SMEM_V + s * 2048, Cfg::BOX_BYTES, 1024), kIdPV, s > 0);
+      tc_commit(t_full);
+    }
+  } else {
+    // ---- softmax: one thread per row
+    const int quad = warp % 4;
+    const int row = quad * 32 + lane;
+    const uint32_t t_s = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+    const int sl = row / W, rr = row % W;            // the row's slot and row in the slot
+    const bool row_ok = sl < nseq && rr < p.N;
+    const int lo = sl * W, hi = lo + p.N;            // its sequence's key columns
+    uint32_t s[64];
+    mbar_wait(s_full, 0);
+    tc_fence_after();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_ld_32cols_pack16(t_s + 32 * c, s + 16 * c);
+    tmem_wait_ld();
+    // row max over the sequence's columns
+    uint32_t mx = 0xFC00FC00u;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      const uint32_t keep = range_keep(i, lo, hi);
+      const uint32_t vm = (s[i] & keep) | (0xFC00FC00u & ~keep);
+      mx = h2_as_u32(__hmax2(u32_as_h2(mx), u32_as_h2(vm)));
+    }
+    const float mloc = fmaxf(lo_f(mx), hi_f(mx));
+    uint32_t cj2, scale2;
+    bool fast2 = true;
+    if (MODE == kModePasa) {
+      // j = 1: F = S'bar, both corrections 0, c = fl16(m'); x = fl16(2 S' - 2 c)
+      const __half cj = __float2half_rn(mloc);
+      fast2 = __all_sync(0xFFFFFFFFu, __habs(cj) <= __float2half_rn(32752.f));
+      cj2 = fast2 ? h2_as_u32(__half2half2(__hmul(cj, __float2half_rn(-2.f))))
+                  : h2_as_u32(__half2half2(cj));
+      scale2 = h2_as_u32(__float2half2_rn(2.f));
+    } else {
+      // naive FP16 FA: x = fl16(S s - fl16(m s)), s = log2(e) / alpha after the store
+      cj2 = h2_as_u32(__half2half2(__hneg(__float2half_rn(__fmul_rn(mloc, p.qk_scale)))));
+      scale2 = h2_as_u32(__half2half2(__float2half_rn(p.qk_scale)));
+    }
+    float acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      uint32_t x;
+      if (MODE == kModeFa16 || fast2) {
+        x = h2_as_u32(__hfma2(u32_as_h2(s[i]), u32_as_h2(scale2), u32_as_h2(cj2)));
+      } else {
+        const __half2 d2 = __hsub2(u32_as_h2(s[i]), u32_as_h2(cj2));
+        x = h2_as_u32(__hadd2(d2, d2));
+      }
+      const uint32_t pv = ex2_f16x2(x) & range_keep(i, lo, hi);
+      acc[2 * (i & 3)] = add_lo_f16(acc[2 * (i & 3)], pv);
+      acc[2 * (i & 3) + 1] = add_hi_f16(acc[2 * (i & 3) + 1], pv);
+      s[i] = pv;
+    }
+    const float l = __fadd_rn(__fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3])),
+                              __fadd_rn(__fadd_rn(acc[4], acc[5]), __fadd_rn(acc[6], acc[7])));
+    // P -> TMEM columns [0, 64) (two keys per column), then the PV MMA
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_st_16cols_b32(t_s + 16 * c, s + 16 * c);
+    tmem_wait_st();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(p_full);
+    // epilogue: O = T 2^c0 / l (global recovering, pasa.cpp:184-194)
+    const int c0 = MODE == kModePasa && row_ok ? pasa_inflation(p.N, p.vmax[seq0 + sl]) : 0;
+    const float inv_l = __fmul_rn(__frcp_rn(l), ldexpf(1.0f, c0));
+    mbar_wait(t_full, 0);
+    tc_fence_after();
+    uint32_t tv[D / 2];
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) tmem_ld_32cols_pack16(t_s + 128 + 32 * c, tv + 16 * c);
+    tmem_wait_ld();
+    uint16_t* dst = p.out + (static_cast<long long>(seq0 + sl) * p.N + rr) * D;
+#pragma unroll
+    for (int i = 0; i < D / 2; i += 4) {
+      uint32_t w[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const __half a = __float2half_rn(__fmul_rn(lo_f(tv[i + k]), inv_l));
+        const __half c = __float2half_rn(__fmul_rn(hi_f(tv[i + k]), inv_l));
+        w[k] = h2_as_u32(__halves2half2(a, c));
+      }
+      if (row_ok) *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc<256>(tmem_base);
+}
+
+template <int D, int MODE>
+static cudaError_t launch_packed_t(const CUtensorMap& tq, const CUtensorMap& tk,
+                                   const CUtensorMap& tv, const PackedParams& p,
+                                   cudaStream_t stream) {
+  using Cfg = PackedCfg<D>;
+  cudaError_t e = cudaFuncSetAttribute(pasa_fwd_packed_kernel<D, MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  const int tiles = (p.BH + p.P - 1) / p.P;  // p.P = 128 / p.W sequences per tile
+  pasa_fwd_packed_kernel<D, MODE><<<tiles, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(tq, tk, tv, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fwd_packed(int D, int mode, const CUtensorMap& tq, const CUtensorMap& tk,
+                              const CUtensorMap& tv, const PackedParams& p, cudaStream_t stream) {
+  if (D == 64) return mode == kModePasa ? launch_packed_t<64, kModePasa>(tq, tk, tv, p, stream)
+                                        : launch_packed_t<64, kModeFa16>(tq, tk, tv, p, stream);
+  if (D == 128) return mode == kModePasa ? launch_packed_t<128, kModePasa>(tq, tk, tv, p, stream)
+                                         : launch_packed_t<128, kModeFa16>(tq, tk, tv, p, stream);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace pasa_b200

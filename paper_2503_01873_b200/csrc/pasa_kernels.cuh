@@ -72,6 +72,16 @@ struct FwdParams {
   long long* trace;       // PASA_TRACE builds only: clock64 timeline (see pasa_fwd.cu)
 };
 
+// Packed short-sequence forward (pasa_fwd_packed.cu): B*H sequences of N <= 64 rows, each
+// a single KV block (S1 = S2 = s2 = N), in 16-aligned slots of W = 16 ceil(N/16) rows,
+// P = 128 / W per 128-row tile; Q, K' (or K), V' (or V) and O are flat [B H N, d] rows.
+struct PackedParams {
+  int BH, N, W, P;
+  float qk_scale;         // FA16 mode: log2(e) / alpha
+  const float* vmax;      // PASA: per sequence, from the pre-pass (V' = V 2^-c0)
+  uint16_t* out;
+};
+
 // Device generators (pasa_gen.cu; bench.cpp:28-56, rng.hpp).
 struct GenParams {
   int kind;            // 0 = uniform(x0 +- am), 1 = hybrid normal + Bernoulli(p) outlier

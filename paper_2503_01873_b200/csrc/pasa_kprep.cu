@@ -206,6 +206,55 @@ __global__ void __launch_bounds__(128) pasa_kprep_small_kernel(const KprepParams
   }
 }
 
+// The rank-1 pre-pass for KV blocks of s2 < 128 keys (ragged blocks, short sequences such
+// as the temporal attention's N = 25): one warp per block, each lane owns D/64 head-dim
+// pairs; FP32 column sums over the s2 keys ascending, then one FMA per element -- the same
+// arithmetic as pasa_kprep_rank1_kernel (orc_preprocess_keys, p_acc = PR1) -- and max|V|.
+template <int D>
+__global__ void __launch_bounds__(256) pasa_kprep_rank1_small_kernel(const KprepParams p,
+                                                                      int nblk_total) {
+  constexpr int U = D / 64;  // half2 columns per lane
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int blk = blockIdx.x * 8 + warp;
+  if (blk >= nblk_total) return;
+  const int nkv = p.S2 / p.s2, s2 = p.s2;
+  const int bh = blk / nkv, j = blk % nkv;
+  const size_t base = (static_cast<size_t>(bh) * p.S2 + static_cast<size_t>(j) * s2) * D;
+  const __half2* kg = reinterpret_cast<const __half2*>(reinterpret_cast<const __half*>(p.k) + base);
+  const __half2* vg = reinterpret_cast<const __half2*>(reinterpret_cast<const __half*>(p.v) + base);
+  float2 cs[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) cs[u] = make_float2(0.f, 0.f);
+  float vm = 0.f;
+  for (int c = 0; c < s2; ++c) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float2 k2 = __half22float2(kg[c * (D / 2) + lane + 32 * u]);
+      cs[u].x = __fadd_rn(cs[u].x, k2.x);
+      cs[u].y = __fadd_rn(cs[u].y, k2.y);
+      const float2 v2 = __half22float2(__habs2(vg[c * (D / 2) + lane + 32 * u]));
+      vm = fmaxf(vm, fmaxf(v2.x, v2.y));  // NaN ignored
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) vm = fmaxf(vm, __shfl_xor_sync(0xffffffffu, vm, o));
+  if (lane == 0) atomicMax(reinterpret_cast<int*>(p.vmax) + bh, __float_as_int(vm));  // vm >= 0
+  const float dm = p.diag - p.off;  // exact: both are FP16 values
+  float2 os[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) os[u] = make_float2(__fmul_rn(p.off, cs[u].x), __fmul_rn(p.off, cs[u].y));
+  __half2* out = reinterpret_cast<__half2*>(reinterpret_cast<__half*>(p.kp) + base);
+  for (int c = 0; c < s2; ++c) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float2 k2 = __half22float2(kg[c * (D / 2) + lane + 32 * u]);
+      const float a = __fmul_rn(__fmaf_rn(dm, k2.x, os[u].x), p.lscale);
+      const float b = __fmul_rn(__fmaf_rn(dm, k2.y, os[u].y), p.lscale);
+      out[c * (D / 2) + lane + 32 * u] = __floats2half2_rn(a, b);
+    }
+  }
+}
+
 // V' = V * 2^-c0 (exact power-of-two scaling; RNE only where V' is subnormal).
 __global__ void __launch_bounds__(256) pasa_vscale_kernel(const VscaleParams p) {
   const long long n8 = p.total / 8;
@@ -232,6 +281,13 @@ cudaError_t launch_vscale(const VscaleParams& p, cudaStream_t stream) {
 }
 
 cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stream) {
+  if (p.s2 != kTile && p.rank1 && p.v && (p.D == 64 || p.D == 128)) {
+    const int total = (p.S2 / p.s2) * B * Hkv;
+    const int grid = (total + 7) / 8;
+    if (p.D == 64) pasa_kprep_rank1_small_kernel<64><<<grid, 256, 0, stream>>>(p, total);
+    else pasa_kprep_rank1_small_kernel<128><<<grid, 256, 0, stream>>>(p, total);
+    return cudaGetLastError();
+  }
   if (p.s2 != kTile) {
     pasa_kprep_small_kernel<<<dim3(p.S2 / p.s2, B * Hkv), 128, 0, stream>>>(p);
     return cudaGetLastError();

@@ -361,6 +361,43 @@ def test_fwd_ragged_vs_model_and_reference(dev, orc, case):
     assert orc.rmse(on, gold) <= 1.25 * r_ref + 1e-3  # Tier 1 vs the reference
 
 
+PACKED = [
+    # B, H, N, d: short sequences, one KV block each, P = 128 // N per tensor-core tile
+    (3, 5, 25, 64),    # SVD temporal (P = 5), 15 sequences -> 3 tiles
+    (2, 7, 64, 128),   # P = 2, 14 sequences
+    (1, 11, 40, 64),   # P = 3, ragged last tile (11 = 3 * 3 + 2)
+    (4, 3, 16, 128),   # P = 8, ragged last tile (12 = 8 + 4)
+]
+
+
+@pytest.mark.parametrize("B,H,N,D", PACKED, ids=[f"n{c[2]}_d{c[3]}" for c in PACKED])
+def test_fwd_packed_short_sequences(dev, orc, B, H, N, D):
+    """Short sequences take the packed kernel (pasa_fwd_packed.cu): against the kernel
+    model and the FP64 golden (PASA), the FA16 model (beta = 0), and the host entry point
+    bit-identical to the device path."""
+    from paper_2503_01873_b200 import _lib, flash_fp16_fwd, pasa_attention_fwd
+    q, k, v = orc.generate("hybrid", 5.0, 10.0, 21, B, H, N, D)
+    qt, kt, vt = (torch.from_numpy(x).half().to(dev) for x in (q, k, v))
+    o = pasa_attention_fwd(qt, kt, vt, s1=N, s2=N)
+    of = flash_fp16_fwd(qt, kt, vt, s1=N, s2=N)
+    torch.cuda.synchronize()
+    pb = Problem(q, k, v, s1=N, s2=N)
+    gold, model, mfa = orc.golden(pb), orc.model_pasa(pb), orc.model_fa16(pb)
+    on, ofn = o.double().cpu().numpy(), of.double().cpu().numpy()
+    r_model = orc.rmse(model, gold)
+    assert orc.nan_pct(on) == 0.0
+    assert orc.rmse(on, gold) <= 1.25 * r_model + 2e-4, (orc.rmse(on, gold), r_model)
+    assert orc.rmse(on, model) <= 0.75 * r_model + 2e-4
+    assert orc.rmse(ofn, gold) <= 1.25 * orc.rmse(mfa, gold) + 2e-4
+    L = _lib.load()
+    desc = _lib.Desc(B, H, H, N, N, D, N, N, 0, 0, BETA_STAR, math.sqrt(D))
+    qh, kh, vh = (x.cpu().pin_memory() for x in (qt, kt, vt))
+    oh = torch.empty_like(qh).pin_memory()
+    _lib.check(L.pasa_b200_attention_host(C.byref(desc), qh.data_ptr(), kh.data_ptr(),
+                                          vh.data_ptr(), oh.data_ptr()))
+    assert torch.equal(oh, o.cpu())
+
+
 def test_fa16_ragged(dev, orc):
     from paper_2503_01873_b200 import flash_fp16_fwd
     q, k, v = orc.generate("hybrid", 0.0, 10.0, 14, 1, 2, 160, 64)
@@ -399,28 +436,31 @@ def test_fwd_store_headroom_beyond_reference(dev, orc):
 
 
 @pytest.mark.parametrize("D", [64, 128])
-def test_fused_prepass_rank1_bitexact(dev, orc, D):
+@pytest.mark.parametrize("s2", [128, 64, 25])
+def test_fused_prepass_rank1_bitexact(dev, orc, D, s2):
     """pasa_b200_preprocess (the fused path's pre-pass): K' in the rank-1 form is
-    bit-exact with the oracle's restatement (PR1), max|V| and V' = V 2^-c0 exact."""
+    bit-exact with the oracle's restatement (PR1) for full and short KV blocks, max|V|
+    and V' = V 2^-c0 exact."""
     from oracle.oracle import PR1
     from paper_2503_01873_b200 import _lib
     L = _lib.load()
-    q, k, v = orc.generate("hybrid", 20.0, 50.0, 41, 1, 2, 512, D)
+    S = 4 * s2
+    q, k, v = orc.generate("hybrid", 20.0, 50.0, 41, 1, 2, S, D)
     kt, vt = (torch.from_numpy(x).half().to(dev) for x in (k, v))
-    desc = _lib.Desc(1, 2, 2, 512, 512, D, 128, 128, 0, 0, BETA_STAR, math.sqrt(D))
+    desc = _lib.Desc(1, 2, 2, S, S, D, s2, s2, 0, 0, BETA_STAR, math.sqrt(D))
     kp, vp = torch.empty_like(kt), torch.empty_like(vt)
     vmax = torch.zeros(2, dtype=torch.float32, device=dev)
     _lib.check(L.pasa_b200_preprocess(C.byref(desc), kt.data_ptr(), vt.data_ptr(), kp.data_ptr(),
                                       vp.data_ptr(), vmax.data_ptr(),
                                       torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
-    diag, off = orc.shift_entries(128, BETA_STAR, math.sqrt(D), P16)
-    want = orc.preprocess_keys(k, 128, diag, off, lscale=LOG2E / 2, p_acc=PR1)
+    diag, off = orc.shift_entries(s2, BETA_STAR, math.sqrt(D), P16)
+    want = orc.preprocess_keys(k, s2, diag, off, lscale=LOG2E / 2, p_acc=PR1)
     assert np.array_equal(kp.double().cpu().numpy(), want)
     vm = np.abs(v).reshape(2, -1).max(axis=1)
     assert np.array_equal(vmax.cpu().numpy(), vm.astype(np.float32))
     for h in range(2):
-        c0 = int(orc.model_inflation(float(vm[h]), 512))
+        c0 = int(orc.model_inflation(float(vm[h]), S))
         assert np.array_equal(vp[0, h].double().cpu().numpy(), orc.f16(v[0, h] * 2.0 ** -c0))
 
 
