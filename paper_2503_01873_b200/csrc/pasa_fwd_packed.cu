@@ -19,9 +19,10 @@
 // the fused kernel does when the sequence is alone: the output is bit-identical to
 // pasa_fwd.cu's, whatever the packing (host pipeline pieces, multi-GPU shards).
 //
-// One CTA per tile, 5 warps: warp 0 loads (TMA) and issues the MMAs, warps 1-4 run the
+// Persistent CTAs walk the tiles; 6 warps: warp 0 loads (TMA, a two-stage ring, so the next
+// tile's loads overlap this one's compute), warp 1 issues the MMAs, warps 2-5 run the
 // softmax with one thread per row (TMEM lane quadrant = warp % 4).  256 TMEM columns (S'/P
-// at +0, T at +128), so two CTAs share an SM.
+// at +0, T at +128), so two CTAs share an SM at d = 64.
 #include <cuda.h>
 #include <cuda_fp16.h>
 
@@ -38,12 +39,11 @@ struct PackedCfg {
   static constexpr int NBOX = D / 64;
   static constexpr int BOX_BYTES = kTile * 128;
   static constexpr int TILE_BYTES = NBOX * BOX_BYTES;
-  static constexpr int SMEM_Q = 0, SMEM_K = TILE_BYTES, SMEM_V = 2 * TILE_BYTES;
-  static constexpr int SMEM_BAR = 3 * TILE_BYTES;
-  static constexpr int SMEM_USED = SMEM_BAR + 64 + 1024;
-  // at least 80 KB so at most two CTAs (= 2 x 256 TMEM columns) are resident per SM
-  static constexpr int SMEM_BYTES = SMEM_USED > 80 * 1024 ? SMEM_USED : 80 * 1024;
-  static constexpr int THREADS = 160;
+  static constexpr int STAGE_BYTES = 3 * TILE_BYTES;  // Q, K', V' of one tile
+  static constexpr int STAGES = 2;
+  static constexpr int SMEM_BAR = STAGES * STAGE_BYTES;
+  static constexpr int SMEM_BYTES = SMEM_BAR + 128 + 1024;
+  static constexpr int THREADS = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 softmax
 };
 
 __device__ __forceinline__ float lo_f(uint32_t u) { return __low2float(u32_as_h2(u)); }
@@ -58,36 +58,45 @@ __device__ __forceinline__ uint32_t range_keep(int i, int lo, int hi) {
 
 }  // namespace
 
+// Persistent: CTA b processes tiles b, b + gridDim.x, ...; the loads of the next tile run
+// in the second stage while the current one is computed.
 template <int D, int MODE>
-__global__ void __launch_bounds__(PackedCfg<D>::THREADS, 1)
+__global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
     pasa_fwd_packed_kernel(const __grid_constant__ CUtensorMap tm_q,
                            const __grid_constant__ CUtensorMap tm_kp,
                            const __grid_constant__ CUtensorMap tm_v, const PackedParams p) {
   using Cfg = PackedCfg<D>;
+  constexpr int ST = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sb = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (sb - smem_u32(smem_raw));
-  const uint32_t in_full = sb + Cfg::SMEM_BAR, s_full = in_full + 8, p_full = in_full + 16,
-                 t_full = in_full + 24;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Cfg::SMEM_BAR + 32);
+  const uint32_t in_full = sb + Cfg::SMEM_BAR;  // [ST]
+  const uint32_t in_empty = in_full + 8 * ST;   // [ST]: the stage's MMAs are done
+  const uint32_t s_full = in_empty + 8 * ST, p_full = s_full + 8, t_full = p_full + 8,
+                 t_empty = t_full + 8;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Cfg::SMEM_BAR + 8 * (2 * ST + 4));
   const int warp = static_cast<int>(warp_id());
   const int lane = threadIdx.x & 31;
-  const int tile = blockIdx.x;
-  const int seq0 = tile * p.P;                      // first sequence of the tile
-  const int nseq = min(p.P, p.BH - seq0);           // sequences in this tile
   const int W = p.W;                                // slot stride (rows / keys)
+  const int ntiles = (p.BH + p.P - 1) / p.P;
 
   if (threadIdx.x == 0) {
-    mbar_init(in_full, 1);
+    for (int st = 0; st < ST; ++st) {
+      mbar_init(in_full + 8 * st, 1);
+      mbar_init(in_empty + 8 * st, 1);
+    }
     mbar_init(s_full, 1);
     mbar_init(p_full, 4);
     mbar_init(t_full, 1);
+    mbar_init(t_empty, 4);
     fence_barrier_init();
   }
   {  // V' rows outside the sequences' N-row slots must read as zero (P = 0 there, and 0 x
-     // stale shared memory could be NaN); the TMA writes below land after this
-    uint4* z = reinterpret_cast<uint4*>(smem + Cfg::SMEM_V);
-    for (int e = threadIdx.x; e < Cfg::TILE_BYTES / 16; e += blockDim.x) z[e] = make_uint4(0, 0, 0, 0);
+     // uninitialised shared memory could be NaN); later tiles only overwrite slot rows
+    for (int st = 0; st < ST; ++st) {
+      uint4* z = reinterpret_cast<uint4*>(smem + st * Cfg::STAGE_BYTES + 2 * Cfg::TILE_BYTES);
+      for (int e = threadIdx.x; e < Cfg::TILE_BYTES / 16; e += blockDim.x) z[e] = make_uint4(0, 0, 0, 0);
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 0) tmem_alloc<256>(tmem_holder);
@@ -97,38 +106,61 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, 1)
   const uint32_t tmem_base = *tmem_holder;
 
   if (warp == 0) {
+    // ---- TMA producer: each sequence's N rows of Q, K', V' into its slot
     if (elect_one()) {
-      // ---- loads: each sequence's N rows of Q, K', V' into its slot (boxes of N rows)
-      mbar_expect_tx(in_full, 3 * Cfg::NBOX * nseq * p.N * 128);
-      for (int sl = 0; sl < nseq; ++sl) {
-        const int r = (seq0 + sl) * p.N;  // flat row of the sequence
-        for (int bx = 0; bx < Cfg::NBOX; ++bx) {
-          const uint32_t off = bx * Cfg::BOX_BYTES + sl * W * 128;
-          tma_load_3d(sb + Cfg::SMEM_Q + off, &tm_q, in_full, bx * 64, r, 0);
-          tma_load_3d(sb + Cfg::SMEM_K + off, &tm_kp, in_full, bx * 64, r, 0);
-          tma_load_3d(sb + Cfg::SMEM_V + off, &tm_v, in_full, bx * 64, r, 0);
+      tma_prefetch(&tm_q);
+      tma_prefetch(&tm_kp);
+      tma_prefetch(&tm_v);
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it % ST, seq0 = tile * p.P, nseq = min(p.P, p.BH - seq0);
+        mbar_wait(in_empty + 8 * st, ((it / ST) & 1) ^ 1);
+        mbar_expect_tx(in_full + 8 * st, 3 * Cfg::NBOX * nseq * p.N * 128);
+        const uint32_t base = sb + st * Cfg::STAGE_BYTES;
+        for (int sl = 0; sl < nseq; ++sl) {
+          const int r = (seq0 + sl) * p.N;  // flat row of the sequence
+          for (int bx = 0; bx < Cfg::NBOX; ++bx) {
+            const uint32_t off = bx * Cfg::BOX_BYTES + sl * W * 128;
+            tma_load_3d(base + off, &tm_q, in_full + 8 * st, bx * 64, r, 0);
+            tma_load_3d(base + Cfg::TILE_BYTES + off, &tm_kp, in_full + 8 * st, bx * 64, r, 0);
+            tma_load_3d(base + 2 * Cfg::TILE_BYTES + off, &tm_v, in_full + 8 * st, bx * 64, r, 0);
+          }
         }
       }
-      mbar_wait(in_full, 0);
-      tc_fence_after();
-      // ---- S' = Q K'^T (SS, F16 accumulator) into columns [0, 128)
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer
+    if (elect_one()) {
       constexpr uint32_t kIdS = idesc_f16(128, 128, 0, 0, 0);
-#pragma unroll
-      for (int s = 0; s < D / 16; ++s) {
-        const uint32_t off = (s / 4) * Cfg::BOX_BYTES + (s % 4) * 32;
-        umma_ss(tmem_base, smem_desc_sw128(sb + Cfg::SMEM_Q + off, 16, 1024),
-                smem_desc_sw128(sb + Cfg::SMEM_K + off, 16, 1024), kIdS, s > 0);
-      }
-      tc_commit(s_full);
-      // ---- T = P V' (TS: P packed in columns [0, 64), V' MN-major) into [128, 128 + D)
-      mbar_wait(p_full, 0);
-      tc_fence_after();
       constexpr uint32_t kIdPV = idesc_f16(128, D, 0, 0, 1);
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it % ST;
+        const uint32_t base = sb + st * Cfg::STAGE_BYTES;
+        mbar_wait(in_full + 8 * st, (it / ST) & 1);
+        tc_fence_after();
+        // S' = Q K'^T (SS, F16 accumulator) into columns [0, 128); in-order after the
+        // previous tile's PV, so its P columns are free
 #pragma unroll
-      for (int s = 0; s < 8; ++s)
-        umma_ts(tmem_base + 128, tmem_base + s * 8,
-                smem_desc_sw128(sb + Cfg::SMEM_V + s * 2048, Cfg::BOX_BYTES, 1024), kIdPV, s > 0);
-      tc_commit(t_full);
+        for (int s = 0; s < D / 16; ++s) {
+          const uint32_t off = (s / 4) * Cfg::BOX_BYTES + (s % 4) * 32;
+          umma_ss(tmem_base, smem_desc_sw128(base + off, 16, 1024),
+                  smem_desc_sw128(base + Cfg::TILE_BYTES + off, 16, 1024), kIdS, s > 0);
+        }
+        tc_commit(s_full);
+        // T = P V' (TS: P packed in columns [0, 64), V' MN-major) into [128, 128 + D), once
+        // the softmax has stored P and read the previous tile's T
+        mbar_wait(p_full, it & 1);
+        mbar_wait(t_empty, (it & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          umma_ts(tmem_base + 128, tmem_base + s * 8,
+                  smem_desc_sw128(base + 2 * Cfg::TILE_BYTES + s * 2048, Cfg::BOX_BYTES, 1024),
+                  kIdPV, s > 0);
+        tc_commit(t_full);
+        tc_commit(in_empty + 8 * st);
+      }
     }
   } else {
     // ---- softmax: one thread per row
@@ -136,83 +168,90 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, 1)
     const int row = quad * 32 + lane;
     const uint32_t t_s = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
     const int sl = row / W, rr = row % W;            // the row's slot and row in the slot
-    const bool row_ok = sl < nseq && rr < p.N;
     const int lo = sl * W, hi = lo + p.N;            // its sequence's key columns
-    uint32_t s[64];
-    mbar_wait(s_full, 0);
-    tc_fence_after();
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int seq0 = tile * p.P, nseq = min(p.P, p.BH - seq0);
+      const bool row_ok = sl < nseq && rr < p.N;
+      uint32_t s[64];
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
 #pragma unroll
-    for (int c = 0; c < 4; ++c) tmem_ld_32cols_pack16(t_s + 32 * c, s + 16 * c);
-    tmem_wait_ld();
-    // row max over the sequence's columns
-    uint32_t mx = 0xFC00FC00u;
+      for (int c = 0; c < 4; ++c) tmem_ld_32cols_pack16(t_s + 32 * c, s + 16 * c);
+      tmem_wait_ld();
+      // row max over the sequence's columns
+      uint32_t mx = 0xFC00FC00u;
 #pragma unroll
-    for (int i = 0; i < 64; ++i) {
-      const uint32_t keep = range_keep(i, lo, hi);
-      const uint32_t vm = (s[i] & keep) | (0xFC00FC00u & ~keep);
-      mx = h2_as_u32(__hmax2(u32_as_h2(mx), u32_as_h2(vm)));
-    }
-    const float mloc = fmaxf(lo_f(mx), hi_f(mx));
-    uint32_t cj2, scale2;
-    bool fast2 = true;
-    if (MODE == kModePasa) {
-      // j = 1: F = S'bar, both corrections 0, c = fl16(m'); x = fl16(2 S' - 2 c)
-      const __half cj = __float2half_rn(mloc);
-      fast2 = __all_sync(0xFFFFFFFFu, __habs(cj) <= __float2half_rn(32752.f));
-      cj2 = fast2 ? h2_as_u32(__half2half2(__hmul(cj, __float2half_rn(-2.f))))
-                  : h2_as_u32(__half2half2(cj));
-      scale2 = h2_as_u32(__float2half2_rn(2.f));
-    } else {
-      // naive FP16 FA: x = fl16(S s - fl16(m s)), s = log2(e) / alpha after the store
-      cj2 = h2_as_u32(__half2half2(__hneg(__float2half_rn(__fmul_rn(mloc, p.qk_scale)))));
-      scale2 = h2_as_u32(__half2half2(__float2half_rn(p.qk_scale)));
-    }
-    float acc[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) acc[k] = 0.f;
-#pragma unroll
-    for (int i = 0; i < 64; ++i) {
-      uint32_t x;
-      if (MODE == kModeFa16 || fast2) {
-        x = h2_as_u32(__hfma2(u32_as_h2(s[i]), u32_as_h2(scale2), u32_as_h2(cj2)));
+      for (int i = 0; i < 64; ++i) {
+        const uint32_t keep = range_keep(i, lo, hi);
+        const uint32_t vm = (s[i] & keep) | (0xFC00FC00u & ~keep);
+        mx = h2_as_u32(__hmax2(u32_as_h2(mx), u32_as_h2(vm)));
+      }
+      const float mloc = fmaxf(lo_f(mx), hi_f(mx));
+      uint32_t cj2, scale2;
+      bool fast2 = true;
+      if (MODE == kModePasa) {
+        // j = 1: F = S'bar, both corrections 0, c = fl16(m'); x = fl16(2 S' - 2 c)
+        const __half cj = __float2half_rn(mloc);
+        fast2 = __all_sync(0xFFFFFFFFu, __habs(cj) <= __float2half_rn(32752.f));
+        cj2 = fast2 ? h2_as_u32(__half2half2(__hmul(cj, __float2half_rn(-2.f))))
+                    : h2_as_u32(__half2half2(cj));
+        scale2 = h2_as_u32(__float2half2_rn(2.f));
       } else {
-        const __half2 d2 = __hsub2(u32_as_h2(s[i]), u32_as_h2(cj2));
-        x = h2_as_u32(__hadd2(d2, d2));
+        // naive FP16 FA: x = fl16(S s - fl16(m s)), s = log2(e) / alpha after the store
+        cj2 = h2_as_u32(__half2half2(__hneg(__float2half_rn(__fmul_rn(mloc, p.qk_scale)))));
+        scale2 = h2_as_u32(__half2half2(__float2half_rn(p.qk_scale)));
       }
-      const uint32_t pv = ex2_f16x2(x) & range_keep(i, lo, hi);
-      acc[2 * (i & 3)] = add_lo_f16(acc[2 * (i & 3)], pv);
-      acc[2 * (i & 3) + 1] = add_hi_f16(acc[2 * (i & 3) + 1], pv);
-      s[i] = pv;
-    }
-    const float l = __fadd_rn(__fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3])),
-                              __fadd_rn(__fadd_rn(acc[4], acc[5]), __fadd_rn(acc[6], acc[7])));
-    // P -> TMEM columns [0, 64) (two keys per column), then the PV MMA
+      float acc[8];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) tmem_st_16cols_b32(t_s + 16 * c, s + 16 * c);
-    tmem_wait_st();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(p_full);
-    // epilogue: O = T 2^c0 / l (global recovering, pasa.cpp:184-194)
-    const int c0 = MODE == kModePasa && row_ok ? pasa_inflation(p.N, p.vmax[seq0 + sl]) : 0;
-    const float inv_l = __fmul_rn(__frcp_rn(l), ldexpf(1.0f, c0));
-    mbar_wait(t_full, 0);
-    tc_fence_after();
-    uint32_t tv[D / 2];
+      for (int k = 0; k < 8; ++k) acc[k] = 0.f;
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) tmem_ld_32cols_pack16(t_s + 128 + 32 * c, tv + 16 * c);
-    tmem_wait_ld();
-    uint16_t* dst = p.out + (static_cast<long long>(seq0 + sl) * p.N + rr) * D;
-#pragma unroll
-    for (int i = 0; i < D / 2; i += 4) {
-      uint32_t w[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const __half a = __float2half_rn(__fmul_rn(lo_f(tv[i + k]), inv_l));
-        const __half c = __float2half_rn(__fmul_rn(hi_f(tv[i + k]), inv_l));
-        w[k] = h2_as_u32(__halves2half2(a, c));
+      for (int i = 0; i < 64; ++i) {
+        uint32_t x;
+        if (MODE == kModeFa16 || fast2) {
+          x = h2_as_u32(__hfma2(u32_as_h2(s[i]), u32_as_h2(scale2), u32_as_h2(cj2)));
+        } else {
+          const __half2 d2 = __hsub2(u32_as_h2(s[i]), u32_as_h2(cj2));
+          x = h2_as_u32(__hadd2(d2, d2));
+        }
+        const uint32_t pv = ex2_f16x2(x) & range_keep(i, lo, hi);
+        acc[2 * (i & 3)] = add_lo_f16(acc[2 * (i & 3)], pv);
+        acc[2 * (i & 3) + 1] = add_hi_f16(acc[2 * (i & 3) + 1], pv);
+        s[i] = pv;
       }
-      if (row_ok) *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(w[0], w[1], w[2], w[3]);
+      const float l = __fadd_rn(__fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3])),
+                                __fadd_rn(__fadd_rn(acc[4], acc[5]), __fadd_rn(acc[6], acc[7])));
+      // P -> TMEM columns [0, 64) (two keys per column), then the PV MMA
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_st_16cols_b32(t_s + 16 * c, s + 16 * c);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      // epilogue: O = T 2^c0 / l (global recovering, pasa.cpp:184-194)
+      const int c0 = MODE == kModePasa && row_ok ? pasa_inflation(p.N, p.vmax[seq0 + sl]) : 0;
+      const float inv_l = __fmul_rn(__frcp_rn(l), ldexpf(1.0f, c0));
+      mbar_wait(t_full, it & 1);
+      tc_fence_after();
+      uint32_t tv[D / 2];
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) tmem_ld_32cols_pack16(t_s + 128 + 32 * c, tv + 16 * c);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(t_empty);
+      uint16_t* dst = p.out + (static_cast<long long>(seq0 + sl) * p.N + rr) * D;
+#pragma unroll
+      for (int i = 0; i < D / 2; i += 4) {
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const __half a = __float2half_rn(__fmul_rn(lo_f(tv[i + k]), inv_l));
+          const __half c = __float2half_rn(__fmul_rn(hi_f(tv[i + k]), inv_l));
+          w[k] = h2_as_u32(__halves2half2(a, c));
+        }
+        if (row_ok) *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
     }
   }
   tc_fence_before();
@@ -230,7 +269,11 @@ static cudaError_t launch_packed_t(const CUtensorMap& tq, const CUtensorMap& tk,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int tiles = (p.BH + p.P - 1) / p.P;  // p.P = 128 / p.W sequences per tile
-  pasa_fwd_packed_kernel<D, MODE><<<tiles, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(tq, tk, tv, p);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int per_sm = D == 64 ? 2 : 1;  // shared memory: 2 x 98 KB (d = 64), 194 KB (d = 128)
+  const int grid = tiles < per_sm * sms ? tiles : per_sm * sms;
+  pasa_fwd_packed_kernel<D, MODE><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(tq, tk, tv, p);
   return cudaGetLastError();
 }
 
