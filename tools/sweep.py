@@ -9,7 +9,8 @@ the FP64 golden, and the non-finite count.  Inputs come from the device
 generators, identical to the reference's generate().
 Configs (BASELINE.json):
   configs[1] Qwen2-7B attn 28/4 GQA d=128 causal, N in {8K, 16K, 32K}
-  configs[2] SVD spatial d=64 (50 x 5 heads, N = 9216) with resonance Q/K
+  configs[2] SVD spatial d=64 (50 x 5 heads, N = 9216) and temporal (9216 x 5 heads,
+             N = 25 frames, the packed kernel) with resonance Q/K
   configs[3] long sweep d=128, H=32 (B=1) N in {4K .. 128K}, non-causal
 """
 import argparse
@@ -49,7 +50,8 @@ def gen(kind, B, Hq, Hkv, S, d, dev, seed):
 
 def run(L, name, kind, B, Hq, Hkv, S, d, causal, iters, dev, full_rmse=True):
     q, k, v = gen(kind, B, Hq, Hkv, S, d, dev, 7)
-    desc = _lib.Desc(B, Hq, Hkv, S, S, d, 128, 128, int(causal), 0, BETA, math.sqrt(d))
+    sb = min(128, S)  # short sequences (one KV block) run on the packed kernel
+    desc = _lib.Desc(B, Hq, Hkv, S, S, d, sb, sb, int(causal), 0, BETA, math.sqrt(d))
     _lib.check(L.pasa_b200_check(C.byref(desc)))
     kp = torch.empty_like(k)
     vp = torch.empty_like(v)
@@ -83,7 +85,7 @@ def run(L, name, kind, B, Hq, Hkv, S, d, causal, iters, dev, full_rmse=True):
     # few heads vs the FP64 golden (the reference's golden_attention precision)
     full = ba.golden_rmse(o, q, k, v, causal, torch.float32) if full_rmse else None
     err = nrm = 0.0
-    r0 = S - 256
+    r0 = max(0, S - 256)
     for b in range(min(B, 2)):
         for h in sorted({0, Hq // 2, Hq - 1}):
             g = ba.golden_attention(q[b:b + 1, h:h + 1], k[b:b + 1, h // (Hq // Hkv):][:, :1],
@@ -116,6 +118,7 @@ def main():
     for S in (8192, 16384, 32768):
         rows.append(run(L, "qwen2-7b (configs[1])", "hybrid", 1, 28, 4, S, 128, True, it, dev))
     rows.append(run(L, "svd-spatial d=64 (configs[2])", "resonance", 50, 5, 5, 9216, 64, False, it, dev))
+    rows.append(run(L, "svd-temporal d=64 (configs[2])", "resonance", 9216, 5, 5, 25, 64, False, it, dev))
     for S in (4096, 8192, 16384, 32768, 65536, 131072):
         if a.quick and S > 32768:
             break
