@@ -8,7 +8,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 P = os.path.join(ROOT, "DESIGN.md")
 s = open(P).read()
 i = s.index("Headline (one B200, `profiles/r01_bench_16k.json`")
-j = s.index("d = 64 is MUFU/ALU-bound")
+j = s.index("The SVD temporal row")
 sw = json.load(open(os.path.join(ROOT, "profiles", "r01_sweep.json")))
 b = json.load(open(os.path.join(ROOT, "profiles", "r01_bench_16k.json")))
 ncu = open(os.path.join(ROOT, "profiles", "r01_ncu_pasa_fwd_summary.txt")).read()
