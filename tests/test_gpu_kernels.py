@@ -436,15 +436,15 @@ def test_fwd_store_headroom_beyond_reference(dev, orc):
 
 
 @pytest.mark.parametrize("D", [64, 128])
-@pytest.mark.parametrize("s2", [128, 64, 25])
-def test_fused_prepass_rank1_bitexact(dev, orc, D, s2):
+@pytest.mark.parametrize("s2,nblk", [(128, 4), (64, 4), (25, 4), (25, 1)])
+def test_fused_prepass_rank1_bitexact(dev, orc, D, s2, nblk):
     """pasa_b200_preprocess (the fused path's pre-pass): K' in the rank-1 form is
     bit-exact with the oracle's restatement (PR1) for full and short KV blocks, max|V|
     and V' = V 2^-c0 exact."""
     from oracle.oracle import PR1
     from paper_2503_01873_b200 import _lib
     L = _lib.load()
-    S = 4 * s2
+    S = nblk * s2
     q, k, v = orc.generate("hybrid", 20.0, 50.0, 41, 1, 2, S, D)
     kt, vt = (torch.from_numpy(x).half().to(dev) for x in (k, v))
     desc = _lib.Desc(1, 2, 2, S, S, D, s2, s2, 0, 0, BETA_STAR, math.sqrt(D))
