@@ -277,6 +277,8 @@ int pasa_b200_preprocess(const pasa_b200_desc* d, const void* k, const void* v, 
   return PASA_B200_OK;
 }
 
+constexpr long long kMaxGridY = 65535;
+
 static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, const void* keys,
                           const void* v, const float* vmax, void* o, void* stream,
                           pasa_b200_diag* diag = nullptr, int s2_bound = 0) {
@@ -284,6 +286,34 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
        reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(o)) & 15)
     return fail(PASA_B200_EINVAL, "attention_fwd: tensors must be 16-byte aligned");
   int rc;
+  // The fused kernel's grid has B Hkv kv heads in one dimension (y when non-causal) and the
+  // query units in the other; beyond the 65535 limit of y the batch is cut into launches.
+  {
+    const long long units = (static_cast<long long>(d->heads_q / d->heads_kv) *
+                                 ((d->seq_q + kTile - 1) / kTile) + 1) / 2;
+    const bool packed = !diag && !d->causal && d->heads_q == d->heads_kv &&
+                        d->seq_q == d->seq_kv && d->seq_kv == d->s2 && d->s2 <= 64;
+    const long long ydim = d->causal ? units : static_cast<long long>(d->batch) * d->heads_kv;
+    if (!packed && ydim > kMaxGridY && d->batch > 1) {
+      const int per_b = d->causal ? 0 : static_cast<int>(kMaxGridY / d->heads_kv);
+      if (per_b < 1) return fail(PASA_B200_EUNSUPPORTED, "attention_fwd: grid too large");
+      const size_t qb = static_cast<size_t>(d->heads_q) * d->seq_q * d->head_dim * 2;
+      const size_t kb = static_cast<size_t>(d->heads_kv) * d->seq_kv * d->head_dim * 2;
+      for (int b0 = 0; b0 < d->batch; b0 += per_b) {
+        pasa_b200_desc cd = *d;
+        cd.batch = b0 + per_b <= d->batch ? per_b : d->batch - b0;
+        rc = launch_forward(&cd, mode, static_cast<const uint8_t*>(q) + qb * b0,
+                            static_cast<const uint8_t*>(keys) + kb * b0,
+                            static_cast<const uint8_t*>(v) + kb * b0,
+                            vmax ? vmax + static_cast<size_t>(b0) * d->heads_kv : nullptr,
+                            static_cast<uint8_t*>(o) + qb * b0, stream, diag, s2_bound);
+        if (rc) return rc;
+      }
+      return PASA_B200_OK;
+    }
+    if (!packed && ydim > kMaxGridY)
+      return fail(PASA_B200_EUNSUPPORTED, "attention_fwd: grid too large");
+  }
   CUtensorMap tq, tk, tv;
   // Short sequences (one KV block each, N <= 64): packed P = 128 / N per tensor-core tile
   if (!diag && !d->causal && d->heads_q == d->heads_kv && d->seq_q == d->seq_kv &&

@@ -27,8 +27,8 @@ __global__ void __launch_bounds__(D * 4) pasa_kprep_kernel(const KprepParams p) 
   __shared__ __align__(16) __half kt[D * ROW];
   __shared__ float red[D * 4 / 32];
 
-  const int j = blockIdx.x;    // KV block
-  const int bh = blockIdx.y;   // b * Hkv + h
+  const int j = blockIdx.y;    // KV block
+  const int bh = blockIdx.x;   // b * Hkv + h (x: up to 2^31 - 1 kv heads)
   const int t = threadIdx.x;   // head-dim index owned by this thread
   const int y = threadIdx.y;   // column-group slot 0..3
   const int tid = y * D + t;
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(256) pasa_kprep_rank1_kernel(const KprepParams
   __shared__ __align__(16) __half kb[S2 * D];
   __shared__ float os[D];
   __shared__ float red[NT / 32];
-  const int j = blockIdx.x, bh = blockIdx.y, tid = threadIdx.x;
+  const int j = blockIdx.y, bh = blockIdx.x, tid = threadIdx.x;
   const size_t base = (static_cast<size_t>(bh) * p.S2 + static_cast<size_t>(j) * S2) * D;
   const uint4* kg = reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(p.k) + base);
   const uint4* vg = reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(p.v) + base);
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(256) pasa_kprep_rank1_kernel(const KprepParams
 // e.g. temporal attention with S2 = 25): one thread per head-dim index, the
 // block read straight from global memory (L1-resident), no column groups.
 __global__ void __launch_bounds__(128) pasa_kprep_small_kernel(const KprepParams p) {
-  const int j = blockIdx.x, bh = blockIdx.y, t = threadIdx.x, s2 = p.s2, D = p.D;
+  const int j = blockIdx.y, bh = blockIdx.x, t = threadIdx.x, s2 = p.s2, D = p.D;
   const size_t base = (static_cast<size_t>(bh) * p.S2 + static_cast<size_t>(j) * s2) * D;
   const __half* kg = reinterpret_cast<const __half*>(p.k) + base;
   __half* out = reinterpret_cast<__half*>(p.kp) + base;
@@ -289,10 +289,10 @@ cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stre
     return cudaGetLastError();
   }
   if (p.s2 != kTile) {
-    pasa_kprep_small_kernel<<<dim3(p.S2 / p.s2, B * Hkv), 128, 0, stream>>>(p);
+    pasa_kprep_small_kernel<<<dim3(B * Hkv, p.S2 / p.s2), 128, 0, stream>>>(p);
     return cudaGetLastError();
   }
-  dim3 grid(p.S2 / kTile, B * Hkv);
+  dim3 grid(B * Hkv, p.S2 / kTile);  // kv heads on x (no 65535 limit)
   if (p.rank1) {  // the fused path's pre-pass: rank-1 form, memory-bound
     if (p.D == 128) pasa_kprep_rank1_kernel<128><<<grid, 256, 0, stream>>>(p);
     else if (p.D == 64) pasa_kprep_rank1_kernel<64><<<grid, 256, 0, stream>>>(p);
@@ -314,7 +314,7 @@ cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stre
 // the FP32 sum over the block's s2 keys.  One thread per head-dim index t.
 __global__ void pasa_ksum_kernel(const uint16_t* __restrict__ kp, uint16_t* __restrict__ ks,
                                  int S2, int s2, int D) {
-  const int j = blockIdx.x, bh = blockIdx.y, t = threadIdx.x;
+  const int j = blockIdx.y, bh = blockIdx.x, t = threadIdx.x;
   const __half* src = reinterpret_cast<const __half*>(kp) +
                       (static_cast<size_t>(bh) * S2 + static_cast<size_t>(j) * s2) * D + t;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -332,7 +332,7 @@ __global__ void pasa_ksum_kernel(const uint16_t* __restrict__ kp, uint16_t* __re
 }
 
 cudaError_t launch_ksum(const void* kp, void* ks, int BH, int S2, int s2, int D, cudaStream_t stream) {
-  pasa_ksum_kernel<<<dim3(S2 / s2, BH), D, 0, stream>>>(static_cast<const uint16_t*>(kp),
+  pasa_ksum_kernel<<<dim3(BH, S2 / s2), D, 0, stream>>>(static_cast<const uint16_t*>(kp),
                                                         static_cast<uint16_t*>(ks), S2, s2, D);
   return cudaGetLastError();
 }

@@ -398,6 +398,23 @@ def test_fwd_packed_short_sequences(dev, orc, B, H, N, D):
     assert torch.equal(oh, o.cpu())
 
 
+def test_fwd_batch_beyond_grid_limit(dev):
+    """B * Hkv > 65535 kv heads (the fused kernel's grid-y limit): the launcher cuts the
+    batch into launches; the output equals per-slice launches bit for bit."""
+    from paper_2503_01873_b200 import pasa_attention_fwd
+    B, S, D = 70000, 128, 64
+    g = torch.Generator(device=dev).manual_seed(5)
+    q = torch.randn(B, 1, S, D, device=dev, generator=g).half()
+    k = torch.randn(B, 1, S, D, device=dev, generator=g).half()
+    v = torch.randn(B, 1, S, D, device=dev, generator=g).half()
+    o = pasa_attention_fwd(q, k, v)
+    cut = 40000
+    o1 = pasa_attention_fwd(q[:cut].contiguous(), k[:cut].contiguous(), v[:cut].contiguous())
+    o2 = pasa_attention_fwd(q[cut:].contiguous(), k[cut:].contiguous(), v[cut:].contiguous())
+    assert torch.isfinite(o).all()
+    assert torch.equal(o, torch.cat([o1, o2]))
+
+
 def test_fa16_ragged(dev, orc):
     from paper_2503_01873_b200 import flash_fp16_fwd
     q, k, v = orc.generate("hybrid", 0.0, 10.0, 14, 1, 2, 160, 64)
