@@ -55,7 +55,11 @@ typedef struct pasa_b200_desc {
   int32_t causal;    /* 0: reference semantics; 1: causal, bottom-right aligned: query
                         row r sees keys <= r + S2 - S1 (s2 = 128; S1, S2 - S1 multiples
                         of 128) */
-  int32_t reserved;
+  int32_t layout;    /* Q, K, V, O memory order: 0 = BHSD (the reference's Tensor4D,
+                        tensor.hpp:27-29), 1 = BSHD ((B, S, H, d) row-major, as most model
+                        code stores activations); the workspace (K', V') is always BHSD.
+                        BSHD: fused path and host entry point; the reference-parity
+                        pasa_b200_preprocess_keys* stay BHSD */
   double beta;       /* shift fraction in [0, 1) (pasa.cpp:98-101); 0 = FP16 FA */
   double alpha;      /* static scale, must equal sqrt(d) (pasa.cpp:206-208)     */
 } pasa_b200_desc;

@@ -23,7 +23,7 @@ class Desc(C.Structure):
         ("batch", C.c_int32), ("heads_q", C.c_int32), ("heads_kv", C.c_int32),
         ("seq_q", C.c_int32), ("seq_kv", C.c_int32), ("head_dim", C.c_int32),
         ("s1", C.c_int32), ("s2", C.c_int32), ("causal", C.c_int32),
-        ("reserved", C.c_int32), ("beta", C.c_double), ("alpha", C.c_double),
+        ("layout", C.c_int32), ("beta", C.c_double), ("alpha", C.c_double),
     ]
 
 

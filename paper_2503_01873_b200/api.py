@@ -221,10 +221,21 @@ def make_problem(q, k, v, s1: int, s2: int, check_finite: bool = True) -> Attent
     return AttentionProblem(q, k, v, s1, s2, math.sqrt(float(d)))
 
 
+_LAYOUTS = {"bhsd": 0, "bshd": 1}
+
+
 def _desc(q: torch.Tensor, k: torch.Tensor, s1: int, s2: int, beta: float, alpha: float,
-          causal: bool) -> _lib.Desc:
-    B, Hq, S1, d = q.shape
-    return _lib.Desc(B, Hq, k.shape[1], S1, k.shape[2], d, s1, s2, int(causal), 0, beta, alpha)
+          causal: bool, layout: str = "bhsd") -> _lib.Desc:
+    """``layout`` "bhsd" (the reference's Tensor4D order) or "bshd" (tensors (B, S, H, d))."""
+    if layout not in _LAYOUTS:
+        raise ValueError(f"layout must be one of {sorted(_LAYOUTS)}")
+    if layout == "bshd":
+        B, S1, Hq, d = q.shape
+        S2, Hkv = k.shape[1], k.shape[2]
+    else:
+        B, Hq, S1, d = q.shape
+        Hkv, S2 = k.shape[1], k.shape[2]
+    return _lib.Desc(B, Hq, Hkv, S1, S2, d, s1, s2, int(causal), _LAYOUTS[layout], beta, alpha)
 
 
 _WS: dict[int, torch.Tensor] = {}
@@ -247,15 +258,16 @@ def pasa_attention_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, beta: 
                        causal: bool = False, s1: int = 128, s2: int = 128,
                        out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
                        stream: torch.cuda.Stream | None = None,
-                       diag: "RunDiagnostics | None" = None) -> torch.Tensor:
-    """Device entry point: fp16 CUDA tensors (BHSD), asynchronous on ``stream``.
-    ``diag`` (optional) is merged with the device RunDiagnostics of this call (the
-    diagnostic kernel instantiation; synchronises the stream)."""
+                       diag: "RunDiagnostics | None" = None, layout: str = "bhsd") -> torch.Tensor:
+    """Device entry point: fp16 CUDA tensors (BHSD, or BSHD with ``layout="bshd"``),
+    asynchronous on ``stream``.  ``diag`` (optional) is merged with the device
+    RunDiagnostics of this call (the diagnostic kernel instantiation; synchronises the
+    stream)."""
     L = _lib.load()
     if not (q.is_cuda and k.is_cuda and v.is_cuda):
         raise ValueError("pasa_attention_fwd expects CUDA tensors; use pasa_attention for host data")
     q, k, v = (t if t.is_contiguous() else t.contiguous() for t in (q, k, v))
-    desc = _desc(q, k, s1, s2, beta, math.sqrt(float(q.shape[-1])), causal)
+    desc = _desc(q, k, s1, s2, beta, math.sqrt(float(q.shape[-1])), causal, layout)
     _lib.check(L.pasa_b200_check(C.byref(desc)))
     if out is None:
         out = torch.empty_like(q)
@@ -278,13 +290,13 @@ def pasa_attention_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, beta: 
 
 def flash_fp16_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: bool = False,
                    s1: int = 128, s2: int = 128, out: torch.Tensor | None = None,
-                   stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+                   stream: torch.cuda.Stream | None = None, layout: str = "bhsd") -> torch.Tensor:
     """The naive FP16 FlashAttention baseline on the same pipeline (FA_PARTIAL_FP16
     semantics of flash_attention, attention.cpp:92-180): scale after the FP16 score
     store, so inputs whose |QK^T| exceeds 65504 produce NaN -- the failure PASA removes."""
     L = _lib.load()
     q, k, v = (t if t.is_contiguous() else t.contiguous() for t in (q, k, v))
-    desc = _desc(q, k, s1, s2, 0.0, math.sqrt(float(q.shape[-1])), causal)
+    desc = _desc(q, k, s1, s2, 0.0, math.sqrt(float(q.shape[-1])), causal, layout)
     _lib.check(L.pasa_b200_check(C.byref(desc)))
     if out is None:
         out = torch.empty_like(q)

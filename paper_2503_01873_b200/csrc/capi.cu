@@ -128,6 +128,8 @@ int check_desc(const pasa_b200_desc* d) {
                     std::to_string(d->seq_q) + ", s1=" + std::to_string(d->s1) +
                     ", S2=" + std::to_string(d->seq_kv) + ", s2=" + std::to_string(d->s2) +
                     "); ragged inputs are rejected, use truncation explicitly");  // tensor.cpp:31-38
+  if (d->layout != 0 && d->layout != 1)
+    return fail(PASA_B200_EINVAL, "desc: layout must be 0 (BHSD) or 1 (BSHD)");
   if (!(d->beta >= 0.0 && d->beta < 1.0))
     return fail(PASA_B200_EINVAL, "pasa params: beta must lie in [0, 1); beta == 1 has no recovery");
   if (d->alpha != std::sqrt(static_cast<double>(d->head_dim)))
@@ -211,6 +213,13 @@ static int preprocess_impl(const pasa_b200_desc* d, const void* k, const void* v
   p.off = __half2float(of);
   p.lscale = lscale;
   p.rank1 = rank1;  // the fused path: rank-1 form for any block size
+  p.Hkv = d->heads_kv;
+  const Strides3 is = layout_strides(d->layout, d->heads_kv, d->seq_kv, d->head_dim);
+  p.in_bs = is.bs;
+  p.in_hs = is.hs;
+  p.in_ss = is.ss;
+  if (d->layout != 0 && !(rank1 && v && (d->head_dim == 64 || d->head_dim == 128)))
+    return fail(PASA_B200_EUNSUPPORTED, "preprocess_keys: the reference-form pre-pass reads BHSD only");
   cudaError_t e = cudaMemsetAsync(p.vmax, 0, static_cast<size_t>(d->batch) * d->heads_kv * 4, st);
   if (e == cudaSuccess) e = launch_kprep(p, d->batch, d->heads_kv, st);
   if (scratch) cudaFreeAsync(scratch, st);
@@ -272,6 +281,12 @@ int pasa_b200_preprocess(const pasa_b200_desc* d, const void* k, const void* v, 
   vs.per_head = static_cast<long long>(d->seq_kv) * d->head_dim;
   vs.total = vs.per_head * d->batch * d->heads_kv;
   vs.S2 = d->seq_kv;
+  vs.D = d->head_dim;
+  vs.Hkv = d->heads_kv;
+  const Strides3 vst = layout_strides(d->layout, d->heads_kv, d->seq_kv, d->head_dim);
+  vs.in_bs = vst.bs;
+  vs.in_hs = vst.hs;
+  vs.in_ss = vst.ss;
   cudaError_t e = launch_vscale(vs, st);
   if (e != cudaSuccess) return cuda_fail(e, "pasa_vscale launch");
   return PASA_B200_OK;
@@ -291,7 +306,7 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
   {
     const long long units = (static_cast<long long>(d->heads_q / d->heads_kv) *
                                  ((d->seq_q + kTile - 1) / kTile) + 1) / 2;
-    const bool packed = !diag && !d->causal && d->heads_q == d->heads_kv &&
+    const bool packed = !diag && !d->causal && d->heads_q == d->heads_kv && d->layout == 0 &&
                         d->seq_q == d->seq_kv && d->seq_kv == d->s2 && d->s2 <= 64;
     const long long ydim = d->causal ? units : static_cast<long long>(d->batch) * d->heads_kv;
     if (!packed && ydim > kMaxGridY && d->batch > 1) {
@@ -316,8 +331,9 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
   }
   CUtensorMap tq, tk, tv;
   // Short sequences (one KV block each, N <= 64): packed P = 128 / N per tensor-core tile
-  if (!diag && !d->causal && d->heads_q == d->heads_kv && d->seq_q == d->seq_kv &&
-      d->seq_kv == d->s2 && d->s2 <= 64 && (s2_bound <= 0 || s2_bound == d->seq_kv)) {
+  if (!diag && !d->causal && d->heads_q == d->heads_kv && d->layout == 0 &&
+      d->seq_q == d->seq_kv && d->seq_kv == d->s2 && d->s2 <= 64 &&
+      (s2_bound <= 0 || s2_bound == d->seq_kv)) {
     const int bh = d->batch * d->heads_q, rows = bh * d->seq_q, n = d->seq_q;
     if ((rc = make_tmap(&tq, q, d->head_dim, rows, 1, n))) return rc;
     if ((rc = make_tmap(&tk, keys, d->head_dim, rows, 1, n))) return rc;
@@ -334,9 +350,22 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
     if (e != cudaSuccess) return cuda_fail(e, "pasa_fwd_packed launch");
     return PASA_B200_OK;
   }
-  if ((rc = make_tmap(&tq, q, d->head_dim, d->seq_q, d->batch * d->heads_q))) return rc;
-  if ((rc = make_tmap(&tk, keys, d->head_dim, d->seq_kv, d->batch * d->heads_kv, d->s2))) return rc;
-  if ((rc = make_tmap(&tv, v, d->head_dim, d->seq_kv, d->batch * d->heads_kv, d->s2))) return rc;
+  // BHSD: a {d, S, B H} map, box coordinates (c, s, b H + h); BSHD: the rows of a batch
+  // hold every head's d values, so a {H d, S, B} map with coordinates (h d + c, s, b).
+  // K and V are the caller's in FA16 mode, the BHSD workspace (K', V') in PASA mode.
+  const bool kv_bshd = mode == kModeFa16 && d->layout == 1;
+  if (d->layout == 1) {
+    if ((rc = make_tmap(&tq, q, d->heads_q * d->head_dim, d->seq_q, d->batch))) return rc;
+  } else if ((rc = make_tmap(&tq, q, d->head_dim, d->seq_q, d->batch * d->heads_q))) {
+    return rc;
+  }
+  if (kv_bshd) {
+    if ((rc = make_tmap(&tk, keys, d->heads_kv * d->head_dim, d->seq_kv, d->batch, d->s2))) return rc;
+    if ((rc = make_tmap(&tv, v, d->heads_kv * d->head_dim, d->seq_kv, d->batch, d->s2))) return rc;
+  } else {
+    if ((rc = make_tmap(&tk, keys, d->head_dim, d->seq_kv, d->batch * d->heads_kv, d->s2))) return rc;
+    if ((rc = make_tmap(&tv, v, d->head_dim, d->seq_kv, d->batch * d->heads_kv, d->s2))) return rc;
+  }
   FwdParams p{};
   p.B = d->batch;
   p.Hq = d->heads_q;
@@ -344,6 +373,8 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
   p.S1 = d->seq_q;
   p.S2 = d->seq_kv;
   p.S2_bound = s2_bound > 0 ? s2_bound : d->seq_kv;
+  p.q_bshd = d->layout == 1;
+  p.kv_bshd = kv_bshd;
   p.nq = (d->seq_q + kTile - 1) / kTile;
   p.nkv = d->seq_kv / d->s2;
   p.qblk = d->causal ? (d->seq_kv - d->seq_q) / kTile : 0;
@@ -559,6 +590,33 @@ static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const
   const uint8_t* hk = reinterpret_cast<const uint8_t*>(k);
   const uint8_t* hv = reinterpret_cast<const uint8_t*>(v);
   uint8_t* ho = reinterpret_cast<uint8_t*>(o);
+  if (d->layout == 1) {
+    // BSHD: a unit's rows are not contiguous, so no pieces -- one copy-in, compute, copy-out
+    cudaEvent_t ev_in = cache.ev[1][0], ev_done = cache.ev[2][0];
+    const cudaStream_t sc = s_comp[0];
+    e = cudaMemcpyAsync(dq, hq, nq, cudaMemcpyHostToDevice, s_in);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dk, hk, nk, cudaMemcpyHostToDevice, s_in);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dv, hv, nk, cudaMemcpyHostToDevice, s_in);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_in, s_in);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sc, ev_in, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+    if (pasa) {
+      if ((rc = pasa_b200_preprocess(d, dk, dv, dkp, dvp, dvmax, sc))) return rc;
+      rc = launch_forward(d, kModePasa, dq, dkp, dvp, dvmax, dout, sc, ddiag);
+    } else {
+      rc = launch_forward(d, kModeFa16, dq, dk, dv, nullptr, dout, sc, ddiag);
+    }
+    if (rc) return rc;
+    e = cudaEventRecord(ev_done, sc);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, ev_done, 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ho, dout, nq, cudaMemcpyDeviceToHost, s_out);
+    if (e == cudaSuccess && hdiag)
+      e = cudaMemcpyAsync(hdiag, ddiag, sizeof(pasa_b200_diag), cudaMemcpyDeviceToHost, s_out);
+    if (e == cudaSuccess && hdiag) e = cudaFreeAsync(ddiag, s_out);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s_out);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H copy / kernel");
+    return PASA_B200_OK;
+  }
   int piece = 0, kvc = 0;
   cudaEvent_t last_dep = nullptr;  // the last unit's K/V (FA16) or pre-pass (PASA) event
   // PASA_B200_HOST_TRACE=1 (diagnostic): per-piece H2D / compute / D2H completion times

@@ -409,8 +409,10 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         if (!tl[t].valid) continue;
         mbar_expect_tx(q_full + 8 * (t), Cfg::TILE_BYTES);
         for (int bx = 0; bx < Cfg::NBOX; ++bx)
+          // BHSD (c, s, b Hq + h); BSHD (h D + c, s, b) on the {Hq D, S1, B} map
           tma_load_3d(sb + Cfg::SMEM_Q + t * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_q,
-                      q_full + 8 * (t), bx * 64, tl[t].i * kTile, b * p.Hq + tl[t].hq);
+                      q_full + 8 * (t), (p.q_bshd ? tl[t].hq * D : 0) + bx * 64, tl[t].i * kTile,
+                      p.q_bshd ? b : b * p.Hq + tl[t].hq);
       }
       for (int j = 0; j < nmax; ++j) {
         const int ks = j % KS, vs = j % VS;
@@ -418,7 +420,8 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         mbar_expect_tx(k_full + 8 * (ks), Cfg::NBOX * 128 * (p.s2 + (kTcSum ? 2 : 0)));
         for (int bx = 0; bx < Cfg::NBOX; ++bx) {
           tma_load_3d(sb + Cfg::SMEM_K + ks * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_kp,
-                      k_full + 8 * (ks), bx * 64, j * p.s2, b * p.Hkv + hkv);
+                      k_full + 8 * (ks), (p.kv_bshd ? hkv * D : 0) + bx * 64, j * p.s2,
+                      p.kv_bshd ? b : b * p.Hkv + hkv);
           if (kTcSum)
             tma_load_3d(sb + Cfg::SMEM_KS + (ks * Cfg::NBOX + bx) * Cfg::KS_BOX, &tm_ks,
                         k_full + 8 * (ks), bx * 64, 2 * j, b * p.Hkv + hkv);
@@ -427,7 +430,8 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         mbar_expect_tx(v_full + 8 * (vs), Cfg::NBOX * 128 * p.s2);
         for (int bx = 0; bx < Cfg::NBOX; ++bx)
           tma_load_3d(sb + Cfg::SMEM_V + vs * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_v,
-                      v_full + 8 * (vs), bx * 64, j * p.s2, b * p.Hkv + hkv);
+                      v_full + 8 * (vs), (p.kv_bshd ? hkv * D : 0) + bx * 64, j * p.s2,
+                      p.kv_bshd ? b : b * p.Hkv + hkv);
       }
     }
   } else if (kSplitIssue ? warp <= NT : warp == 1) {
@@ -798,8 +802,10 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       const float l_tot = h == 0 ? __fadd_rn(l_run, lo_other) : __fadd_rn(lo_other, l_run);
       const float inv_l = __fmul_rn(__frcp_rn(l_tot), ldexpf(1.0f, c0));  // exact 2^c0
       const bool row_ok = ti.i * kTile + row < p.S1;  // ragged last query tile
-      uint16_t* dst = p.out + ((static_cast<size_t>(b) * p.Hq + ti.hq) * p.S1 +
-                               static_cast<size_t>(ti.i) * kTile + row) * D + (D / 2) * h;
+      const size_t orow = static_cast<size_t>(ti.i) * kTile + row;
+      uint16_t* dst = p.out + (p.q_bshd ? (static_cast<size_t>(b) * p.S1 + orow) * p.Hq + ti.hq
+                                        : (static_cast<size_t>(b) * p.Hq + ti.hq) * p.S1 + orow) * D +
+                      (D / 2) * h;
 #pragma unroll
       for (int i = 0; i < D / 4; i += 4) {
         uint32_t w[4];

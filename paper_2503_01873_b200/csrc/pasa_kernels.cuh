@@ -20,7 +20,20 @@ struct KprepParams {
   float off;           // fl16(-beta/(alpha*s2))        (pasa.cpp:27)
   float lscale;        // 1 reproduces the reference; log2(e)/2 for the fused kernel
   int rank1;           // fused path: K' = (diag-off) K + off colsum (pasa_kprep_rank1_kernel)
+  // input K / V element (b, h, s, t) at b in_bs + h in_hs + s in_ss + t (BHSD or BSHD; the
+  // rank-1 kernels only -- the output K' is always BHSD, (b Hkv + h) S2 D + s D + t)
+  int Hkv;
+  long long in_bs, in_hs, in_ss;
 };
+
+// element strides (batch, head, seq) of a (B, H, S, D) tensor stored BHSD (layout 0) or BSHD
+struct Strides3 {
+  long long bs, hs, ss;
+};
+__host__ __device__ inline Strides3 layout_strides(int layout, int H, int S, int D) {
+  return layout == 1 ? Strides3{static_cast<long long>(S) * H * D, D, static_cast<long long>(H) * D}
+                     : Strides3{static_cast<long long>(H) * S * D, static_cast<long long>(S) * D, D};
+}
 
 // O-bounding exponent c0 >= 0: the smallest integer with
 // S2 * max|V| <= 2^14 * 2^c0, computed identically on host and device.  The
@@ -35,12 +48,14 @@ __host__ __device__ inline int pasa_inflation(int S2, float vmax) {
 
 // V' = V * 2^-c0 per (b, kv head), written by the pre-pass for the fused kernel.
 struct VscaleParams {
-  const uint16_t* v;   // (B, Hkv, S2, D) fp16
-  uint16_t* vp;        // (B, Hkv, S2, D) fp16
+  const uint16_t* v;   // (B, Hkv, S2, D) fp16, BHSD or BSHD (in_*: element strides)
+  uint16_t* vp;        // (B, Hkv, S2, D) fp16, BHSD
   const float* vmax;   // (B * Hkv)
   long long per_head;  // S2 * D
   long long total;     // B * Hkv * S2 * D
   int S2;
+  int D, Hkv;
+  long long in_bs, in_hs, in_ss;
 };
 
 // Fused forward.  PASA mode: scores live in the log2 domain (K' carries log2 e).
@@ -62,6 +77,8 @@ struct FwdParams {
   int qblk;               // causal: (S2 - S1) / 128, the bottom-right alignment offset
   int s2;                 // KV block (shifting-matrix size), <= 128; < 128 masks columns
   float inv_s2;           // fl32(1/s2): the block mean S'bar = sum * inv_s2
+  int q_bshd;             // Q and O stored BSHD (TMA coordinates, output address)
+  int kv_bshd;            // the K / V operands stored BSHD (FA16 mode's raw K, V)
   int tiles_per_kv;       // group * nq
   float inva;             // beta / (1 - beta)       (pasa.cpp:85)
   float qk_scale;         // FA16 mode only: log2(e) / alpha applied after the FP16 store

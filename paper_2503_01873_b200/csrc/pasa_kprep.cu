@@ -130,13 +130,17 @@ __global__ void __launch_bounds__(256) pasa_kprep_rank1_kernel(const KprepParams
   __shared__ float red[NT / 32];
   const int j = blockIdx.y, bh = blockIdx.x, tid = threadIdx.x;
   const size_t base = (static_cast<size_t>(bh) * p.S2 + static_cast<size_t>(j) * S2) * D;
-  const uint4* kg = reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(p.k) + base);
-  const uint4* vg = reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(p.v) + base);
+  // the input block: rows j S2 .. j S2 + S2 - 1 of head (b, h), row stride in_ss
+  const long long ibase = (bh / p.Hkv) * p.in_bs + (bh % p.Hkv) * p.in_hs +
+                          static_cast<long long>(j) * S2 * p.in_ss;
+  const __half* kin0 = reinterpret_cast<const __half*>(p.k) + ibase;
+  const __half* vin0 = reinterpret_cast<const __half*>(p.v) + ibase;
   float vm = 0.f;
 #pragma unroll 4
   for (int e = tid; e < S2 * D / 8; e += NT) {
-    reinterpret_cast<uint4*>(kb)[e] = kg[e];
-    const uint4 w = vg[e];
+    const long long off = (e / (D / 8)) * p.in_ss + (e % (D / 8)) * 8;
+    reinterpret_cast<uint4*>(kb)[e] = *reinterpret_cast<const uint4*>(kin0 + off);
+    const uint4 w = *reinterpret_cast<const uint4*>(vin0 + off);
     const __half2* h = reinterpret_cast<const __half2*>(&w);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -220,8 +224,12 @@ __global__ void __launch_bounds__(256) pasa_kprep_rank1_small_kernel(const Kprep
   const int nkv = p.S2 / p.s2, s2 = p.s2;
   const int bh = blk / nkv, j = blk % nkv;
   const size_t base = (static_cast<size_t>(bh) * p.S2 + static_cast<size_t>(j) * s2) * D;
-  const __half2* kg = reinterpret_cast<const __half2*>(reinterpret_cast<const __half*>(p.k) + base);
-  const __half2* vg = reinterpret_cast<const __half2*>(reinterpret_cast<const __half*>(p.v) + base);
+  const long long ibase = (bh / p.Hkv) * p.in_bs + (bh % p.Hkv) * p.in_hs +
+                          static_cast<long long>(j) * s2 * p.in_ss;
+  // input rows (strided by in_ss), as half2: row c at kg + c * RS2
+  const __half2* kg = reinterpret_cast<const __half2*>(reinterpret_cast<const __half*>(p.k) + ibase);
+  const __half2* vg = reinterpret_cast<const __half2*>(reinterpret_cast<const __half*>(p.v) + ibase);
+  const long long RS2 = p.in_ss / 2;
   float2 cs[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) cs[u] = make_float2(0.f, 0.f);
@@ -229,10 +237,10 @@ __global__ void __launch_bounds__(256) pasa_kprep_rank1_small_kernel(const Kprep
   for (int c = 0; c < s2; ++c) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const float2 k2 = __half22float2(kg[c * (D / 2) + lane + 32 * u]);
+      const float2 k2 = __half22float2(kg[c * RS2 + lane + 32 * u]);
       cs[u].x = __fadd_rn(cs[u].x, k2.x);
       cs[u].y = __fadd_rn(cs[u].y, k2.y);
-      const float2 v2 = __half22float2(__habs2(vg[c * (D / 2) + lane + 32 * u]));
+      const float2 v2 = __half22float2(__habs2(vg[c * RS2 + lane + 32 * u]));
       vm = fmaxf(vm, fmaxf(v2.x, v2.y));  // NaN ignored
     }
   }
@@ -247,7 +255,7 @@ __global__ void __launch_bounds__(256) pasa_kprep_rank1_small_kernel(const Kprep
   for (int c = 0; c < s2; ++c) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const float2 k2 = __half22float2(kg[c * (D / 2) + lane + 32 * u]);
+      const float2 k2 = __half22float2(kg[c * RS2 + lane + 32 * u]);
       const float a = __fmul_rn(__fmaf_rn(dm, k2.x, os[u].x), p.lscale);
       const float b = __fmul_rn(__fmaf_rn(dm, k2.y, os[u].y), p.lscale);
       out[c * (D / 2) + lane + 32 * u] = __floats2half2_rn(a, b);
@@ -263,7 +271,10 @@ __global__ void __launch_bounds__(256) pasa_vscale_kernel(const VscaleParams p) 
     const int bh = static_cast<int>((i * 8) / p.per_head);
     const int c0 = pasa_inflation(p.S2, p.vmax[bh]);
     const __half2 sc = __half2half2(__float2half_rn(ldexpf(1.0f, -c0)));
-    uint4 w = reinterpret_cast<const uint4*>(p.v)[i];
+    // output (BHSD) element i * 8 = ((bh S2) + s) D + t; the input by its layout strides
+    const long long r = (i * 8) % p.per_head, s = r / p.D, t = r % p.D;
+    const long long in = (bh / p.Hkv) * p.in_bs + (bh % p.Hkv) * p.in_hs + s * p.in_ss + t;
+    uint4 w = *reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(p.v) + in);
     __half2* h = reinterpret_cast<__half2*>(&w);
 #pragma unroll
     for (int k = 0; k < 4; ++k) h[k] = __hmul2(h[k], sc);

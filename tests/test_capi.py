@@ -38,7 +38,7 @@ def test_library_is_sm100a_only():
 
 def _desc(**kw):
     base = dict(batch=1, heads_q=2, heads_kv=2, seq_q=1024, seq_kv=1024, head_dim=128, s1=128,
-                s2=128, causal=0, reserved=0, beta=BETA_STAR, alpha=math.sqrt(128.0))
+                s2=128, causal=0, layout=0, beta=BETA_STAR, alpha=math.sqrt(128.0))
     base.update(kw)
     return _lib.Desc(**base)
 

@@ -415,6 +415,34 @@ def test_fwd_batch_beyond_grid_limit(dev):
     assert torch.equal(o, torch.cat([o1, o2]))
 
 
+@pytest.mark.parametrize("B,Hq,Hkv,S1,S2,D,causal", [
+    (2, 4, 2, 256, 256, 128, False),
+    (1, 7, 1, 384, 512, 128, True),    # GQA group 7, causal bottom-right (S1 < S2)
+    (2, 2, 2, 200, 256, 64, False),    # ragged S1
+])
+def test_bshd_layout_bit_identical(dev, B, Hq, Hkv, S1, S2, D, causal):
+    """layout = BSHD ((B, S, H, d) tensors): TMA on the {H d, S, B} view, strided pre-pass,
+    BSHD output -- bit-identical to the BHSD path for PASA and FA16, device and host."""
+    from paper_2503_01873_b200 import _lib, flash_fp16_fwd, pasa_attention_fwd
+    g = torch.Generator(device=dev).manual_seed(Hq * 100 + S1)
+    q = (torch.randn(B, Hq, S1, D, device=dev, generator=g) * 2).half()
+    k = (torch.randn(B, Hkv, S2, D, device=dev, generator=g) * 2 + 1).half()
+    v = torch.randn(B, Hkv, S2, D, device=dev, generator=g).half()
+    qs, ks, vs = (t.transpose(1, 2).contiguous() for t in (q, k, v))
+    s1 = 128 if S1 % 128 == 0 else S1
+    for fn in (pasa_attention_fwd, flash_fp16_fwd):
+        want = fn(q, k, v, causal=causal, s1=s1)
+        got = fn(qs, ks, vs, causal=causal, layout="bshd", s1=s1)
+        assert torch.equal(got.transpose(1, 2), want), fn.__name__
+    L = _lib.load()
+    desc = _lib.Desc(B, Hq, Hkv, S1, S2, D, s1, 128, int(causal), 1, BETA_STAR, math.sqrt(D))
+    qh, kh, vh = (t.cpu().pin_memory() for t in (qs, ks, vs))
+    oh = torch.empty_like(qh).pin_memory()
+    _lib.check(L.pasa_b200_attention_host(C.byref(desc), qh.data_ptr(), kh.data_ptr(),
+                                          vh.data_ptr(), oh.data_ptr()))
+    assert torch.equal(oh.transpose(1, 2), pasa_attention_fwd(q, k, v, causal=causal, s1=s1).cpu())
+
+
 def test_fa16_ragged(dev, orc):
     from paper_2503_01873_b200 import flash_fp16_fwd
     q, k, v = orc.generate("hybrid", 0.0, 10.0, 14, 1, 2, 160, 64)
