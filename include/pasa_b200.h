@@ -174,6 +174,15 @@ PASA_B200_API int pasa_b200_attention_host_diag(const pasa_b200_desc* desc, cons
                                                 const uint16_t* k, const uint16_t* v, uint16_t* o,
                                                 pasa_b200_diag* diag);
 
+/* pasa_b200_attention_host over several GPUs of one process: the
+ * (batch, kv head) units are split evenly over `devices` (n_devices entries; a device
+ * may repeat), one host thread per device runs the pipelined host path on its share;
+ * no exchange between devices.  The output is bit-identical to the single-device call.
+ * BHSD only.  Blocks until every share is back in `o`. */
+PASA_B200_API int pasa_b200_attention_host_multi(const pasa_b200_desc* desc, const uint16_t* q,
+                                                 const uint16_t* k, const uint16_t* v, uint16_t* o,
+                                                 const int32_t* devices, int32_t n_devices);
+
 /* Device-side input generator: elements [start,
  * start + n) of tensor `tensor_id` (0 = Q, 1 = K, 2 = V) of the reference's
  * generate() (bench.cpp:28-72, rng.hpp:14-40) as binary16 into device memory:

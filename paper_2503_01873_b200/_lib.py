@@ -73,6 +73,7 @@ def load(path: str = SO) -> C.CDLL:
     L.pasa_b200_attention_fwd_prepped.argtypes = [dp, vp, vp, vp, vp, vp, vp]
     L.pasa_b200_preprocess.argtypes = [dp, vp, vp, vp, vp, vp, vp]
     L.pasa_b200_attention_host.argtypes = [dp, vp, vp, vp, vp]
+    L.pasa_b200_attention_host_multi.argtypes = [dp, vp, vp, vp, vp, vp, C.c_int32]
     L.pasa_b200_flash_fp16_fwd.argtypes = [dp, vp, vp, vp, vp, vp]
     L.pasa_b200_preprocess_keys_host.argtypes = [dp, vp, vp, C.c_double, C.c_double]
     L.pasa_b200_diag_reset.argtypes = [vp, vp]

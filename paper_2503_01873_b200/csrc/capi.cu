@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/pasa_b200.h"
@@ -485,6 +486,54 @@ int pasa_b200_attention_host_diag(const pasa_b200_desc* d, const uint16_t* q, co
     return fail(PASA_B200_EINVAL, "attention_host_diag: NULL diag");
   }
   return attention_host_impl(d, q, k, v, o, diag);
+}
+
+int pasa_b200_attention_host_multi(const pasa_b200_desc* d, const uint16_t* q, const uint16_t* k,
+                                   const uint16_t* v, uint16_t* o, const int32_t* devices,
+                                   int32_t n_devices) {
+  g_last_error.clear();
+  int rc = check_desc(d);
+  if (rc) return rc;
+  if (!q || !k || !v || !o || !devices || n_devices <= 0)
+    return fail(PASA_B200_EINVAL, "attention_host_multi: NULL buffer or empty device list");
+  if (d->layout != 0)
+    return fail(PASA_B200_EUNSUPPORTED, "attention_host_multi: BHSD only (units must be contiguous)");
+  // The (batch, kv head) units, contiguous in BHSD, are split evenly across the devices
+  // (no exchange -- each device computes its units' whole output); one host
+  // thread per device runs the pipelined host entry point on its share.
+  const int units = d->batch * d->heads_kv, group = d->heads_q / d->heads_kv;
+  const int n = n_devices < units ? n_devices : units;
+  const size_t q_unit = static_cast<size_t>(group) * d->seq_q * d->head_dim;  // halves
+  const size_t k_unit = static_cast<size_t>(d->seq_kv) * d->head_dim;
+  std::vector<int> rcs(n, PASA_B200_OK);
+  std::vector<std::string> errs(n);
+  std::vector<std::thread> pool;
+  for (int r = 0; r < n; ++r) {
+    const int u0 = static_cast<int>(static_cast<long long>(units) * r / n);
+    const int u1 = static_cast<int>(static_cast<long long>(units) * (r + 1) / n);
+    pool.emplace_back([&, r, u0, u1] {
+      cudaError_t e = cudaSetDevice(devices[r]);
+      if (e != cudaSuccess) {
+        rcs[r] = PASA_B200_ENODEV;
+        errs[r] = "attention_host_multi: cudaSetDevice failed";
+        return;
+      }
+      pasa_b200_desc sd = *d;  // the share as one batch of (u1 - u0) kv heads (BHSD)
+      sd.batch = 1;
+      sd.heads_kv = u1 - u0;
+      sd.heads_q = (u1 - u0) * group;
+      rcs[r] = attention_host_impl(&sd, q + q_unit * u0, k + k_unit * u0, v + k_unit * u0,
+                                   o + q_unit * u0, nullptr);
+      if (rcs[r]) errs[r] = g_last_error;
+    });
+  }
+  for (auto& th : pool) th.join();
+  for (int r = 0; r < n; ++r)
+    if (rcs[r]) {
+      g_last_error = errs[r];
+      return rcs[r];
+    }
+  return PASA_B200_OK;
 }
 
 static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const uint16_t* k,

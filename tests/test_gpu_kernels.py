@@ -443,6 +443,26 @@ def test_bshd_layout_bit_identical(dev, B, Hq, Hkv, S1, S2, D, causal):
     assert torch.equal(oh.transpose(1, 2), pasa_attention_fwd(q, k, v, causal=causal, s1=s1).cpu())
 
 
+def test_host_multi_device_bit_identical(dev):
+    """pasa_b200_attention_host_multi: units split over a device list (here device 0 three
+    times, one host thread each) -- bit-identical to the single-device host call."""
+    from paper_2503_01873_b200 import _lib
+    B, Hq, Hkv, S, D = 2, 8, 4, 384, 128
+    g = torch.Generator().manual_seed(9)
+    q = (torch.randn(B, Hq, S, D, generator=g) * 2).half().pin_memory()
+    k = (torch.randn(B, Hkv, S, D, generator=g) * 2).half().pin_memory()
+    v = torch.randn(B, Hkv, S, D, generator=g).half().pin_memory()
+    L = _lib.load()
+    desc = _lib.Desc(B, Hq, Hkv, S, S, D, 128, 128, 1, 0, BETA_STAR, math.sqrt(D))
+    o1, o3 = torch.empty_like(q).pin_memory(), torch.empty_like(q).pin_memory()
+    _lib.check(L.pasa_b200_attention_host(C.byref(desc), q.data_ptr(), k.data_ptr(),
+                                          v.data_ptr(), o1.data_ptr()))
+    devs = (C.c_int32 * 3)(0, 0, 0)
+    _lib.check(L.pasa_b200_attention_host_multi(C.byref(desc), q.data_ptr(), k.data_ptr(),
+                                                v.data_ptr(), o3.data_ptr(), devs, 3))
+    assert torch.isfinite(o1.float()).all() and torch.equal(o1, o3)
+
+
 def test_fa16_ragged(dev, orc):
     from paper_2503_01873_b200 import flash_fp16_fwd
     q, k, v = orc.generate("hybrid", 0.0, 10.0, 14, 1, 2, 160, 64)
