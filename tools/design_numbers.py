@@ -33,7 +33,7 @@ pipeline (Î² = 0) runs at {fa:.0f} TFLOP/s, so PASA's shift and recovery cost â‰
 â€” and on the Qwen-like biased inputs that baseline returns
 {b['fa16_baseline']['nonfinite_outputs'] / 1e6:.1f} M non-finite outputs while PASA returns 0 (on uniform(30, 0.5): FA16 100 % NaN,
 PASA RMSE {b['accuracy_uniform30']['rmse_vs_fp64']:.1e}).  End-to-end through the host C-ABI with pinned buffers
-(copy-in, compute and copy-out pipelined over chunks): {b['e2e']['value']:.0f} TFLOP/s; the reference's own CPU
+(copy-in, compute and copy-out pipelined over query-head pieces): {b['e2e']['value']:.0f} TFLOP/s; the reference's own CPU
 PASA on the box's {b['cpu_baseline']['cores']} host cores: {b['cpu_baseline']['value']:.3f} TFLOP/s.  ncu
 (`profiles/r01_ncu_pasa_fwd_summary.txt`): tensor pipe active {tensor:.0f} % of the kernel's cycles,
 issue active {issue:.0f} %, DRAM {dram:.0f} MB per launch.
