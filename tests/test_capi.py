@@ -71,10 +71,28 @@ def test_check_accepts_config1_and_qwen(lib):
     (dict(s2=256, s1=256), _lib.EUNSUPPORTED, "s2 must be <= 128"),
     (dict(causal=1, seq_q=1024, seq_kv=512), _lib.EUNSUPPORTED, "causal requires S1 <= S2"),
     (dict(causal=1, s2=64), _lib.EUNSUPPORTED, "causal requires S1 <= S2"),
+    (dict(layout=2), _lib.EINVAL, "layout must be 0 (BHSD) or 1 (BSHD)"),
 ])
 def test_check_rejects(lib, kw, code, msg):
     rc, err = _check(lib, **kw)
     assert rc == code and msg in err, (rc, err)
+
+
+def test_check_accepts_bshd(lib):
+    assert _check(lib, layout=1)[0] == 0
+    assert _check(lib, layout=1, heads_q=28, heads_kv=4, seq_q=16384, seq_kv=16384, causal=1)[0] == 0
+
+
+def test_host_multi_argument_errors(lib):
+    """pasa_b200_attention_host_multi validates before touching a device (CPU test)."""
+    buf = (C.c_uint16 * 8)()
+    devs = (C.c_int32 * 2)(0, 1)
+    d = _desc(layout=1)
+    assert lib.pasa_b200_attention_host_multi(C.byref(d), buf, buf, buf, buf, devs, 2) == \
+        _lib.EUNSUPPORTED
+    assert "BHSD only" in lib.pasa_b200_last_error().decode()
+    d = _desc()
+    assert lib.pasa_b200_attention_host_multi(C.byref(d), buf, buf, buf, buf, devs, 0) == _lib.EINVAL
 
 
 def test_errors_map_to_reference_exception_types(lib):
