@@ -139,10 +139,8 @@ int check_desc(const pasa_b200_desc* d) {
   if (d->head_dim != 64 && d->head_dim != 128)
     return fail(PASA_B200_EUNSUPPORTED, "head_dim must be 64 or 128");
   if (d->s2 > kTile) return fail(PASA_B200_EUNSUPPORTED, "s2 must be <= 128");
-  if (d->causal && (d->seq_q > d->seq_kv || d->s2 != kTile || d->seq_q % kTile != 0 ||
-                    (d->seq_kv - d->seq_q) % kTile != 0))
-    return fail(PASA_B200_EUNSUPPORTED,
-                "causal requires S1 <= S2, s2 == 128, S1 and S2 - S1 multiples of 128");
+  if (d->causal && (d->seq_q > d->seq_kv || d->s2 != kTile))
+    return fail(PASA_B200_EUNSUPPORTED, "causal requires S1 <= S2 and s2 == 128");
   return PASA_B200_OK;
 }
 
@@ -378,7 +376,7 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
   p.kv_bshd = kv_bshd;
   p.nq = (d->seq_q + kTile - 1) / kTile;
   p.nkv = d->seq_kv / d->s2;
-  p.qblk = d->causal ? (d->seq_kv - d->seq_q) / kTile : 0;
+  p.qoff = d->causal ? d->seq_kv - d->seq_q : 0;
   p.s2 = d->s2;
   p.inv_s2 = static_cast<float>(1.0 / d->s2);
   p.group = d->heads_q / d->heads_kv;

@@ -164,8 +164,11 @@ __device__ __forceinline__ TileInfo tile_info(const FwdParams& p, int hkv, int i
   ti.valid = idx < p.tiles_per_kv;
   ti.i = p.nq - 1 - idx / p.group;  // longest (causal) tiles first
   ti.hq = hkv * p.group + idx % p.group;
-  // causal, bottom-right aligned: query row r sees keys <= r + (S2 - S1) (qblk = (S2-S1)/128)
-  ti.nblk = ti.valid ? (causal ? min(ti.i + 1 + p.qblk, p.nkv) : p.nkv) : 0;
+  // causal, bottom-right aligned: query row r sees keys <= r + (S2 - S1); the tile runs the
+  // blocks up to the one holding its last valid row's last key (blocks masked for every
+  // row of the tile are skipped; a row may still see a block of the tile fully masked)
+  const int last = min(p.S1, (ti.i + 1) * kTile) - 1;
+  ti.nblk = ti.valid ? (causal ? min((last + p.qoff) / kTile + 1, p.nkv) : p.nkv) : 0;
   return ti;
 }
 
@@ -687,9 +690,12 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         tmem_wait_ld();
         if (tr) PASA_TR(t, j, 2);
         // masked columns: causal diagonal block (c > row) or a short KV block (c >= s2)
-        const bool cdiag = CAUSAL && (j == ti.nblk - 1);
+        // causal: block j shows row r of the tile its first vis0 + r keys (any S2 - S1: up
+        // to two blocks per tile are partial)
+        const int vis0 = ti.i * kTile + p.qoff - j * kTile + 1;
+        const bool cdiag = CAUSAL && vis0 < kTile;
         const bool diag = cdiag || p.s2 < kTile;
-        const int lim = cdiag ? row + 1 : p.s2;
+        const int lim = cdiag ? vis0 + row : p.s2;
         if (DIAGNOSE) track_store_block<NP>(s, lim, NP * h, diag, dslot);
         constexpr bool kSum = MODE == kModePasa && !kTcSum;
         float mh, sh = 0.f;

@@ -74,7 +74,7 @@ struct FwdParams {
   int S2_bound;           // key count the pre-pass's O bound c0 was computed for (>= S2 when a
                           // launch covers a prefix of the keys, e.g. the host pipeline's pieces)
   int nq, nkv, group;     // ceil(S1/128), S2/s2, Hq/Hkv
-  int qblk;               // causal: (S2 - S1) / 128, the bottom-right alignment offset
+  int qoff;               // causal: S2 - S1, the bottom-right alignment offset (any value)
   int s2;                 // KV block (shifting-matrix size), <= 128; < 128 masks columns
   float inv_s2;           // fl32(1/s2): the block mean S'bar = sum * inv_s2
   int q_bshd;             // Q and O stored BSHD (TMA coordinates, output address)

@@ -590,17 +590,22 @@ def test_run_diagnostics_match_reference(dev, orc, ref):
         d1.store_finite_min, d1.store_finite_max, d1.out_total)
 
 
-@pytest.mark.parametrize("S1,S2,D", [(256, 640, 128), (128, 512, 64)])
+@pytest.mark.parametrize("S1,S2,D", [(256, 640, 128), (128, 512, 64),
+                                     (192, 256, 128),   # S2 - S1 = 64: two partial blocks
+                                     (200, 512, 64),    # ragged S1, S2 - S1 = 312
+                                     (136, 640, 128)])  # ragged S1, S2 - S1 = 504
 def test_fwd_causal_bottom_right(dev, orc, S1, S2, D):
-    """Causal with S1 < S2 (a query chunk after S2 - S1 cached keys): row r sees keys
-    <= r + S2 - S1; against the model with q_offset and the masked FP64 golden."""
+    """Causal with S1 < S2 (a query chunk after S2 - S1 cached keys, any offset, ragged S1):
+    row r sees keys <= r + S2 - S1; against the model with q_offset and the masked FP64
+    golden."""
     from paper_2503_01873_b200 import pasa_attention_fwd
     from paper_2503_01873_b200 import bench_api as ba
     q = orc.generate("hybrid", 0.0, 10.0, 51, 1, 2, S1, D, tensor_ids=(0,))[0]
     k, v = orc.generate("hybrid", 0.0, 10.0, 52, 1, 2, S2, D, tensor_ids=(1, 2))
-    pb = Problem(q, k, v, causal=True, q_offset=S2 - S1)
+    s1 = 128 if S1 % 128 == 0 else S1  # ragged S1: the kernel still runs 128-row tiles
+    pb = Problem(q, k, v, s1=s1, causal=True, q_offset=S2 - S1)
     qt, kt, vt = (torch.from_numpy(x).half().to(dev) for x in (q, k, v))
-    o = pasa_attention_fwd(qt, kt, vt, causal=True).double().cpu().numpy()
+    o = pasa_attention_fwd(qt, kt, vt, causal=True, s1=s1).double().cpu().numpy()
     gold = orc.golden(pb)
     gold_dev = ba.golden_attention(qt, kt, vt, causal=True).cpu().numpy()
     assert np.abs(gold_dev - gold).max() <= 1e-12  # the device golden's alignment agrees
