@@ -435,6 +435,8 @@ def run_b200(args):
                       "rmse_b200_vs_fp64": ba.rmse(o_new, gold),
                       "rmse_reference_vs_fp64": ba.rmse(o_rt, gold),
                       "rmse_b200_vs_reference": ba.rmse(o_new, o_rt),
+                      "maxabs_rel_b200_vs_reference": float((o_new - o_rt).abs().max() /
+                                                            o_rt.abs().max()),
                       "nan_pct_b200": ba.nan_stats(o_new), "nan_pct_reference": ba.nan_stats(o_rt),
                       "note": "FP16 scores of this biased data carry |S'| ~ 3e2 after the shift, "
                               "so every FP16 pipeline loses accuracy; the reference loses more"}

@@ -62,6 +62,8 @@ def main():
             row["ref_pasa_nonfinite_pct"] = ba.nan_stats(rt)
             finite = torch.isfinite(rt).all().item()
             row["b200_vs_ref_rmse"] = ba.rmse(o.cpu().double(), rt) if finite else math.nan
+            row["b200_vs_ref_maxabs_rel"] = (float((o.cpu().double() - rt).abs().max() / rt.abs().max())
+                                             if finite else math.nan)
         rows.append(row)
         print(json.dumps(row), flush=True)
         del gi, gold, o, of
