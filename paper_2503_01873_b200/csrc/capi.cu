@@ -486,6 +486,35 @@ int pasa_b200_attention_host_diag(const pasa_b200_desc* d, const uint16_t* q, co
   return attention_host_impl(d, q, k, v, o, diag);
 }
 
+// The host entry point's device buffers, streams and events, cached per host thread (and
+// re-created when the thread switches device).  release() frees them: the multi-device
+// entry point's worker threads call it before they exit.
+struct HostCache {
+  static constexpr int kComp = 4, kRing = 64;
+  int dev = -1;
+  uint8_t* buf = nullptr;
+  size_t bytes = 0;
+  cudaStream_t st[3 + kComp] = {};
+  cudaEvent_t ev[3][kRing] = {};  // kv copied / piece copied in / piece computed
+  cudaEvent_t prep[kRing] = {}, comp_done[kComp] = {};
+  void release() {
+    if (buf) cudaFree(buf);
+    buf = nullptr;
+    bytes = 0;
+    for (auto& x : st)
+      if (x) cudaStreamDestroy(x), x = nullptr;
+    for (auto& row : ev)
+      for (auto& x : row)
+        if (x) cudaEventDestroy(x), x = nullptr;
+    for (auto& x : prep)
+      if (x) cudaEventDestroy(x), x = nullptr;
+    for (auto& x : comp_done)
+      if (x) cudaEventDestroy(x), x = nullptr;
+    dev = -1;
+  }
+};
+static thread_local HostCache g_host_cache;
+
 int pasa_b200_attention_host_multi(const pasa_b200_desc* d, const uint16_t* q, const uint16_t* k,
                                    const uint16_t* v, uint16_t* o, const int32_t* devices,
                                    int32_t n_devices) {
@@ -523,6 +552,8 @@ int pasa_b200_attention_host_multi(const pasa_b200_desc* d, const uint16_t* q, c
       rcs[r] = attention_host_impl(&sd, q + q_unit * u0, k + k_unit * u0, v + k_unit * u0,
                                    o + q_unit * u0, nullptr);
       if (rcs[r]) errs[r] = g_last_error;
+      cudaDeviceSynchronize();  // nothing of this share may still use the buffers
+      g_host_cache.release();   // the worker thread ends: free its cached buffers
     });
   }
   for (auto& th : pool) th.join();
@@ -550,16 +581,8 @@ static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const
   // Small pieces keep the pipeline's fill (the first piece's H2D) and drain (the last
   // piece's kernel and D2H) short; the whole call is then bound by the H2D copy
   // (tools/pcie_probe.py).  Device buffers, streams and events are cached per thread and device.
-  constexpr int kTargetPieces = 32, kComp = 4, kRing = 64;
-  struct Cache {
-    int dev = -1;
-    uint8_t* buf = nullptr;
-    size_t bytes = 0;
-    cudaStream_t st[3 + kComp] = {};
-    cudaEvent_t ev[3][kRing] = {};  // kv copied / piece copied in / piece computed
-    cudaEvent_t prep[kRing] = {}, comp_done[kComp] = {};
-  };
-  thread_local Cache cache;
+  constexpr int kTargetPieces = 32, kComp = HostCache::kComp, kRing = HostCache::kRing;
+  HostCache& cache = g_host_cache;
   const int group = d->heads_q / d->heads_kv;
   const int units = d->batch * d->heads_kv;
   const size_t q_head = static_cast<size_t>(d->seq_q) * d->head_dim * 2;
