@@ -565,8 +565,29 @@ int pasa_b200_attention_host_multi(const pasa_b200_desc* d, const uint16_t* q, c
   return PASA_B200_OK;
 }
 
+static int attention_host_run(const pasa_b200_desc* d, const uint16_t* q, const uint16_t* k,
+                              const uint16_t* v, uint16_t* o, pasa_b200_diag* hdiag,
+                              pasa_b200_diag** ddiag_out);
+
+// A failed call returns only after everything it enqueued has finished: no copy may still
+// read the caller's buffers (or write the cached device buffers) once it has returned.
 static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const uint16_t* k,
                                const uint16_t* v, uint16_t* o, pasa_b200_diag* hdiag) {
+  pasa_b200_diag* ddiag = nullptr;
+  const int rc = attention_host_run(d, q, k, v, o, hdiag, &ddiag);
+  if (rc != PASA_B200_OK) {
+    const std::string err = g_last_error;
+    for (auto st : g_host_cache.st)
+      if (st) cudaStreamSynchronize(st);
+    if (ddiag) cudaFree(ddiag);
+    g_last_error = err;
+  }
+  return rc;
+}
+
+static int attention_host_run(const pasa_b200_desc* d, const uint16_t* q, const uint16_t* k,
+                              const uint16_t* v, uint16_t* o, pasa_b200_diag* hdiag,
+                              pasa_b200_diag** ddiag_out) {
   g_last_error.clear();
   int rc = check_desc(d);
   if (rc) return rc;
@@ -651,6 +672,7 @@ static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const
     if ((e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&ddiag), sizeof(pasa_b200_diag), pool,
                                      s_prep)))
       return cuda_fail(e, "cudaMallocFromPoolAsync");
+    *ddiag_out = ddiag;  // freed on s_out on success, by the caller on failure
     if ((rc = pasa_b200_diag_reset(ddiag, s_prep))) return rc;
     if ((e = cudaEventRecord(cache.prep[0], s_prep)) != cudaSuccess) return cuda_fail(e, "event");
     for (int c = 0; c < kComp; ++c)
@@ -682,7 +704,8 @@ static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const
     if (e == cudaSuccess) e = cudaMemcpyAsync(ho, dout, nq, cudaMemcpyDeviceToHost, s_out);
     if (e == cudaSuccess && hdiag)
       e = cudaMemcpyAsync(hdiag, ddiag, sizeof(pasa_b200_diag), cudaMemcpyDeviceToHost, s_out);
-    if (e == cudaSuccess && hdiag) e = cudaFreeAsync(ddiag, s_out);
+    if (e == cudaSuccess && hdiag && (e = cudaFreeAsync(ddiag, s_out)) == cudaSuccess)
+      *ddiag_out = nullptr;
     if (e == cudaSuccess) e = cudaStreamSynchronize(s_out);
     if (e != cudaSuccess) return cuda_fail(e, "D2H copy / kernel");
     return PASA_B200_OK;
@@ -775,7 +798,7 @@ static int attention_host_impl(const pasa_b200_desc* d, const uint16_t* q, const
       if (e != cudaSuccess) return cuda_fail(e, "event");
     }
     e = cudaMemcpyAsync(hdiag, ddiag, sizeof(pasa_b200_diag), cudaMemcpyDeviceToHost, s_out);
-    if (e == cudaSuccess) e = cudaFreeAsync(ddiag, s_out);
+    if (e == cudaSuccess && (e = cudaFreeAsync(ddiag, s_out)) == cudaSuccess) *ddiag_out = nullptr;
     if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
   }
   // every compute stream's last kernel precedes a D2H on s_out, so s_out completes last
