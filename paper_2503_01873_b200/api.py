@@ -238,6 +238,22 @@ def _desc(q: torch.Tensor, k: torch.Tensor, s1: int, s2: int, beta: float, alpha
     return _lib.Desc(B, Hq, Hkv, S1, S2, d, s1, s2, int(causal), _LAYOUTS[layout], beta, alpha)
 
 
+def _check_device_tensors(fn: str, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                          out: torch.Tensor | None) -> None:
+    """The C-ABI takes raw fp16 device pointers: reject what it would misread."""
+    if not (q.is_cuda and k.is_cuda and v.is_cuda):
+        raise ValueError(f"{fn} expects CUDA tensors; use pasa_attention for host data")
+    for name, t in (("q", q), ("k", k), ("v", v), ("out", out)):
+        if t is None:
+            continue
+        if t.dtype != torch.float16:
+            raise ValueError(f"{fn}: {name} must be float16, got {t.dtype}")
+        if t.device != q.device:
+            raise ValueError(f"{fn}: {name} is on {t.device}, q on {q.device}")
+    if out is not None and (tuple(out.shape) != tuple(q.shape) or not out.is_contiguous()):
+        raise ValueError(f"{fn}: out must be a contiguous tensor of q's shape {tuple(q.shape)}")
+
+
 _WS: dict[int, torch.Tensor] = {}
 
 
@@ -264,23 +280,26 @@ def pasa_attention_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, beta: 
     RunDiagnostics of this call (the diagnostic kernel instantiation; synchronises the
     stream)."""
     L = _lib.load()
-    if not (q.is_cuda and k.is_cuda and v.is_cuda):
-        raise ValueError("pasa_attention_fwd expects CUDA tensors; use pasa_attention for host data")
+    _check_device_tensors("pasa_attention_fwd", q, k, v, out)
+    if workspace is not None and (not workspace.is_cuda or workspace.device != q.device):
+        raise ValueError("pasa_attention_fwd: workspace must be on q's device")
     q, k, v = (t if t.is_contiguous() else t.contiguous() for t in (q, k, v))
     desc = _desc(q, k, s1, s2, beta, math.sqrt(float(q.shape[-1])), causal, layout)
     _lib.check(L.pasa_b200_check(C.byref(desc)))
-    if out is None:
-        out = torch.empty_like(q)
-    if workspace is None:
-        workspace = workspace_for(desc, q.device)
-    st = (stream or torch.cuda.current_stream(q.device)).cuda_stream
-    dbuf = None
-    if diag is not None:
-        dbuf = torch.empty(C.sizeof(_lib.Diag), dtype=torch.uint8, device=q.device)
-        _lib.check(L.pasa_b200_diag_reset(dbuf.data_ptr(), st))
-    _lib.check(L.pasa_b200_attention_fwd(C.byref(desc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
-                                         out.data_ptr(), workspace.data_ptr(), workspace.numel(),
-                                         dbuf.data_ptr() if dbuf is not None else None, st))
+    with torch.cuda.device(q.device):  # the library launches on the current device
+        if out is None:
+            out = torch.empty_like(q)
+        if workspace is None:
+            workspace = workspace_for(desc, q.device)
+        st = (stream or torch.cuda.current_stream(q.device)).cuda_stream
+        dbuf = None
+        if diag is not None:
+            dbuf = torch.empty(C.sizeof(_lib.Diag), dtype=torch.uint8, device=q.device)
+            _lib.check(L.pasa_b200_diag_reset(dbuf.data_ptr(), st))
+        _lib.check(L.pasa_b200_attention_fwd(C.byref(desc), q.data_ptr(), k.data_ptr(),
+                                             v.data_ptr(), out.data_ptr(), workspace.data_ptr(),
+                                             workspace.numel() * workspace.element_size(),
+                                             dbuf.data_ptr() if dbuf is not None else None, st))
     if dbuf is not None:
         torch.cuda.current_stream(q.device).synchronize() if stream is None else stream.synchronize()
         host = _lib.Diag.from_buffer_copy(bytes(dbuf.cpu().numpy()))
@@ -295,14 +314,16 @@ def flash_fp16_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: bo
     semantics of flash_attention, attention.cpp:92-180): scale after the FP16 score
     store, so inputs whose |QK^T| exceeds 65504 produce NaN -- the failure PASA removes."""
     L = _lib.load()
+    _check_device_tensors("flash_fp16_fwd", q, k, v, out)
     q, k, v = (t if t.is_contiguous() else t.contiguous() for t in (q, k, v))
     desc = _desc(q, k, s1, s2, 0.0, math.sqrt(float(q.shape[-1])), causal, layout)
     _lib.check(L.pasa_b200_check(C.byref(desc)))
     if out is None:
         out = torch.empty_like(q)
-    st = (stream or torch.cuda.current_stream(q.device)).cuda_stream
-    _lib.check(L.pasa_b200_flash_fp16_fwd(C.byref(desc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
-                                          out.data_ptr(), st))
+    with torch.cuda.device(q.device):
+        st = (stream or torch.cuda.current_stream(q.device)).cuda_stream
+        _lib.check(L.pasa_b200_flash_fp16_fwd(C.byref(desc), q.data_ptr(), k.data_ptr(),
+                                              v.data_ptr(), out.data_ptr(), st))
     return out
 
 
@@ -333,14 +354,18 @@ def preprocess_keys(k: torch.Tensor, params: PasaParams, lscale: float = 1.0,
     Returns (kp, vmax) with kp in the K-major layout kp[b,h,j*s2+c,t] = K'_j[t][c];
     ``lscale=1`` reproduces the reference's bits."""
     L = _lib.load()
+    _check_device_tensors("preprocess_keys", k, k, k if v is None else v, None)
+    k = k.contiguous()
+    v = v.contiguous() if v is not None else None
     B, H, S2, d = k.shape
     desc = _lib.Desc(B, H, H, S2, S2, d, params.s2, params.s2, 0, 0, params.beta, params.alpha)
     kp = torch.empty_like(k)
     vmax = torch.zeros(B * H, dtype=torch.float32, device=k.device)
-    st = torch.cuda.current_stream(k.device).cuda_stream
-    _lib.check(L.pasa_b200_preprocess_keys(C.byref(desc), k.data_ptr(),
-                                           v.data_ptr() if v is not None else None,
-                                           kp.data_ptr(), vmax.data_ptr(), lscale, st))
+    with torch.cuda.device(k.device):
+        st = torch.cuda.current_stream(k.device).cuda_stream
+        _lib.check(L.pasa_b200_preprocess_keys(C.byref(desc), k.data_ptr(),
+                                               v.data_ptr() if v is not None else None,
+                                               kp.data_ptr(), vmax.data_ptr(), lscale, st))
     return kp, vmax
 
 

@@ -167,3 +167,22 @@ def test_cli_sweep_gate_and_run(dev, tmp_path):
     assert row[0] == "PASA_FP16" and row[1] == "file" and float(row[12]) == 0.0
     assert float(row[11]) < 0.05 and row[13] != ""  # rmse vs the device golden; ranges filled
     assert np.load(f"{d}/o.npy").shape == (1, 2, 256, 128)
+
+
+def test_device_api_rejects_misread_tensors(dev):
+    """The C-ABI takes raw fp16 pointers: the Python entry points reject wrong dtypes,
+    host/device mixes and mis-shaped outputs before launching, and take the workspace
+    size in bytes whatever its dtype."""
+    from paper_2503_01873_b200 import flash_fp16_fwd, pasa_attention_fwd
+    q = torch.randn(1, 2, 256, 64, device=dev).half()
+    with pytest.raises(ValueError, match="must be float16"):
+        pasa_attention_fwd(q.float(), q, q)
+    with pytest.raises(ValueError, match="must be float16"):
+        flash_fp16_fwd(q, q.float(), q)
+    with pytest.raises(ValueError, match="CUDA tensors"):
+        flash_fp16_fwd(q, q.cpu(), q)
+    with pytest.raises(ValueError, match="out must be"):
+        pasa_attention_fwd(q, q, q, out=torch.empty(1, 2, 128, 64, device=dev, dtype=torch.float16))
+    ref = pasa_attention_fwd(q, q, q)
+    ws = torch.empty(1 << 20, dtype=torch.float32, device=dev)  # 4 MiB as floats
+    assert torch.equal(pasa_attention_fwd(q, q, q, workspace=ws), ref)
