@@ -628,7 +628,10 @@ def test_full_size_properties(dev, cfg):
         the visible V (the prefix for causal rows, checked on the whole V here);
     (2) V -> 2 V doubles O bit for bit (2^-c0 absorbs the exact power of two) outside the
         FP16 subnormal range;
-    (3) the run is deterministic."""
+    (3) the run is deterministic;
+    (4) causal: new keys in the last KV block leave every earlier query tile bit-identical
+        (K'_j depends on block j only, the pseudo-average on blocks <= j); non-causal: rows are
+        independent, so permuting the query rows permutes the output rows bit for bit."""
     from paper_2503_01873_b200 import bench_api as ba, pasa_attention_fwd
     B, Hq, Hkv, S, D, causal = cfg
     gi = ba.generate(ba.DistributionSpec(ba.DistKind.HYBRID, 0.0, 10.0, 0.001, 3, B, Hq, S, D,
@@ -649,6 +652,16 @@ def test_full_size_properties(dev, cfg):
     assert float((o2.float() - 2 * o.float())[~normal].abs().max().item() if (~normal).any()
                  else 0.0) <= 2.0 ** -23
     assert torch.equal(pasa_attention_fwd(q, k, v, causal=causal), o)
+    if causal:
+        k2 = k.clone()
+        k2[:, :, -128:] = torch.flip(k[:, :, -128:], dims=[3]) * 0.5 + 1.0
+        o3 = pasa_attention_fwd(q, k2, v, causal=causal)
+        assert torch.equal(o3[:, :, :-128], o[:, :, :-128])
+        assert not torch.equal(o3[:, :, -128:], o[:, :, -128:])
+    else:
+        perm = torch.randperm(S, generator=torch.Generator().manual_seed(7)).to(dev)
+        o3 = pasa_attention_fwd(q[:, :, perm].contiguous(), k, v, causal=causal)
+        assert torch.equal(o3, o[:, :, perm])
 
 
 def _random_cases(n=16, seed=2025):
