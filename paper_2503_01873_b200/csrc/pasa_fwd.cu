@@ -391,6 +391,9 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // Everything above touches only this CTA's shared memory, TMEM and the kernel
+  // parameters; the inputs (Q, K', V', max|V|) may come from the previous grid.
+  pdl_wait();
   // A 512-column allocation is the whole TMEM of the SM, so it starts at lane 0, column 0:
   // the base is the constant 0 (no per-thread register, no spill, uniform addressing).
   static_assert(Cfg::TMEM_COLS == 512, "tmem_base = 0 needs the full allocation");
@@ -874,8 +877,17 @@ cudaError_t launch_fwd_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
   if (e != cudaSuccess) return e;
   const int units = (p.tiles_per_kv + Cfg::NT - 1) / Cfg::NT;
   const dim3 grid = CAUSAL ? dim3(p.B * p.Hkv, units) : dim3(units, p.B * p.Hkv);
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(tq, tk, tv, tks, p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tks, p);
 }
 
 cudaError_t launch_fwd(int D, bool causal, int mode, const CUtensorMap& tq, const CUtensorMap& tk,

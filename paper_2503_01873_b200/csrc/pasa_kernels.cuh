@@ -1,5 +1,6 @@
 // pasa_kernels.cuh -- shared parameter blocks for the PASA B200 kernels.
 #pragma once
+#include <cstdlib>
 #include <cstdint>
 
 namespace pasa_b200 {
@@ -44,6 +45,14 @@ __host__ __device__ inline int pasa_inflation(int S2, float vmax) {
   if (!(need > 1.0f)) return 0;
   const int e = ilogbf(need);  // floor(log2 need), exact
   return ldexpf(1.0f, e) == need ? e : e + 1;
+}
+
+// Programmatic dependent launch for the kernels that follow another of the path's kernels
+// in a stream (V scale after the K' pre-pass, the forward after the pre-pass): their launch
+// and prologue overlap the previous kernel's tail.  PASA_B200_NO_PDL=1 turns it off.
+inline bool pdl_enabled() {
+  static const bool on = std::getenv("PASA_B200_NO_PDL") == nullptr;
+  return on;
 }
 
 // V' = V * 2^-c0 per (b, kv head), written by the pre-pass for the fused kernel.

@@ -17,6 +17,7 @@
 #include <cuda_fp16.h>
 
 #include "pasa_kernels.cuh"
+#include "sm100.cuh"
 
 namespace pasa_b200 {
 
@@ -129,6 +130,7 @@ __global__ void __launch_bounds__(256) pasa_kprep_rank1_kernel(const KprepParams
   __shared__ float os[D];
   __shared__ float red[NT / 32];
   const int j = blockIdx.y, bh = blockIdx.x, tid = threadIdx.x;
+  sm100::pdl_trigger();  // the V scale may launch now (it waits for this grid before reading)
   const size_t base = (static_cast<size_t>(bh) * p.S2 + static_cast<size_t>(j) * S2) * D;
   // the input block: rows j S2 .. j S2 + S2 - 1 of head (b, h), row stride in_ss
   const long long ibase = (bh / p.Hkv) * p.in_bs + (bh % p.Hkv) * p.in_hs +
@@ -271,6 +273,8 @@ template <int D>
 __global__ void __launch_bounds__(256) pasa_vscale_kernel(const VscaleParams p) {
   constexpr int C8 = D / 8, U = 4, NT = 256;  // 16-byte words per row, per thread, threads
   const int bh = blockIdx.x;
+  sm100::pdl_trigger();  // the forward may launch now (it waits for this grid before reading)
+  sm100::pdl_wait();     // max|V| comes from the pre-pass grid
   const int c0 = pasa_inflation(p.S2, p.vmax[bh]);
   const __half2 sc = __half2half2(__float2half_rn(ldexpf(1.0f, -c0)));
   const int n8 = p.S2 * C8;  // 16-byte words per head
@@ -303,10 +307,18 @@ cudaError_t launch_vscale(const VscaleParams& p, cudaStream_t stream) {
   const long long bh = p.total / p.per_head;
   const long long chunks = (p.per_head / 8 + 1023) / 1024;
   const dim3 grid(static_cast<unsigned>(bh), static_cast<unsigned>(chunks < 65535 ? chunks : 65535));
-  if (p.D == 128) pasa_vscale_kernel<128><<<grid, 256, 0, stream>>>(p);
-  else if (p.D == 64) pasa_vscale_kernel<64><<<grid, 256, 0, stream>>>(p);
-  else return cudaErrorInvalidValue;
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  if (p.D == 128) return cudaLaunchKernelEx(&cfg, pasa_vscale_kernel<128>, p);
+  if (p.D == 64) return cudaLaunchKernelEx(&cfg, pasa_vscale_kernel<64>, p);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stream) {

@@ -96,6 +96,13 @@ __device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads)
 }
 
 // ---------------------------------------------------------------- TMA
+// Programmatic dependent launch: a grid launched with the PDL attribute may start while
+// the previous grid of its stream still runs; pdl_wait() returns once that grid has
+// completed and its memory is visible (a no-op without the attribute).  pdl_trigger()
+// lets the next PDL-launched grid start once every block of this one has triggered.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void tma_prefetch(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
