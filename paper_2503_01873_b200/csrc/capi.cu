@@ -8,6 +8,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -715,20 +716,25 @@ static int attention_host_run(const pasa_b200_desc* d, const uint16_t* q, const 
   // PASA_B200_HOST_TRACE=1 (diagnostic): per-piece H2D / compute / D2H completion times
   static const bool trace = getenv("PASA_B200_HOST_TRACE") != nullptr;
   std::vector<cudaEvent_t> tev;
+  std::vector<double> thost;  // host time (ms after the first mark) when each piece was enqueued
+  const auto h0 = std::chrono::steady_clock::now();
   auto tmark = [&](cudaStream_t st) {
     if (!trace) return;
     cudaEvent_t x;
     cudaEventCreate(&x);
     cudaEventRecord(x, st);
     tev.push_back(x);
+    if (st == s_out)
+      thost.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
   };
   tmark(s_in);
   // one piece: query rows [r0, r0 + nr) of heads [g0, g0 + nh) of units [u0, u0 + nu) on
   // keys [0, skv) (row pieces of a causal head stay bit-identical to the whole head; V's O
   // bound keeps the full key count).  Pieces are whole heads today: cutting the last
-  // unit's causal heads by rows (cheap early rows last) did not shorten the drain, and
-  // cutting every head doubled the pieces and made the host's enqueueing (~50 us per
-  // piece) the bottleneck (PASA_B200_HOST_TRACE timelines).
+  // unit's causal heads by rows (cheap early rows last) did not shorten the drain (a
+  // late-row piece keeps a 128-block CTA chain), and cutting every head doubled the copy
+  // chunks, whose per-copy DMA overhead cost more (PASA_B200_HOST_TRACE timelines,
+  // tools/pcie_probe.py).
   auto run_piece = [&](int u0, int nu, int g0, int nh, int r0, int nr, int skv,
                        cudaEvent_t dep) -> int {
     const size_t ok = k_unit * u0;
@@ -809,7 +815,8 @@ static int attention_host_run(const pasa_b200_desc* d, const uint16_t* q, const 
       cudaEventElapsedTime(&a, tev[0], tev[i]);
       cudaEventElapsedTime(&b, tev[0], tev[i + 1]);
       cudaEventElapsedTime(&c, tev[0], tev[i + 2]);
-      fprintf(stderr, "piece %2zu  in %.3f  comp %.3f  out %.3f\n", i / 3, a, b, c);
+      fprintf(stderr, "piece %2zu  in %.3f  comp %.3f  out %.3f  enqueued %.3f\n", i / 3, a, b, c,
+              thost[i / 3]);
     }
     for (auto x : tev) cudaEventDestroy(x);
   }

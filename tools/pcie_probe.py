@@ -49,7 +49,24 @@ def main():
         with torch.cuda.stream(s2):
             for hq in range(HQ):
                 oh[:, hq].copy_(od[:, hq], non_blocking=True)
+    sin = [torch.cuda.Stream() for _ in range(3)]
+    sout = [torch.cuda.Stream() for _ in range(2)]
+
+    def chunked_multi(n_in, n_out):  # the same chunks spread round-robin over several streams
+        c = 0
+        for hk in range(HKV):
+            for src, dst in [(kh[:, hk], kd[:, hk]), (vh[:, hk], vd[:, hk])] + \
+                    [(qh[:, hk * (HQ // HKV) + g], qd[:, hk * (HQ // HKV) + g]) for g in range(HQ // HKV)]:
+                with torch.cuda.stream(sin[c % n_in]):
+                    dst.copy_(src, non_blocking=True)
+                c += 1
+        for hq in range(HQ):
+            with torch.cuda.stream(sout[hq % n_out]):
+                oh[:, hq].copy_(od[:, hq], non_blocking=True)
     th, td, tb, tc = t(h2d), t(d2h), t(lambda: (h2d(), d2h())), t(chunked)
+    for n_in, n_out in [(1, 1), (2, 1), (2, 2), (3, 2)]:
+        tm = t(lambda: chunked_multi(n_in, n_out))
+        print(f"chunked over {n_in} H2D + {n_out} D2H streams: {tm*1e3:.3f} ms")
     L = _lib.load()
     desc = _lib.Desc(1, HQ, HKV, S, S, D, 128, 128, 1, 0, 0.984497, math.sqrt(D))
     te = t(lambda: _lib.check(L.pasa_b200_attention_host(C.byref(desc), qh.data_ptr(), kh.data_ptr(),
