@@ -53,7 +53,7 @@ typedef struct pasa_b200_desc {
   int32_t s1;        /* query block; numerically irrelevant (any divisor of S1) */
   int32_t s2;        /* KV block = shifting-matrix size, <= 128 (128 is fastest)*/
   int32_t causal;    /* 0: reference semantics; 1: causal, bottom-right aligned: query
-                        row r sees keys <= r + S2 - S1 (S1 <= S2, s2 = 128, any offset) */
+                        row r sees keys <= r + S2 - S1 (S1 <= S2, any s2 and offset) */
   int32_t layout;    /* Q, K, V, O memory order: 0 = BHSD (the reference's Tensor4D,
                         tensor.hpp:27-29), 1 = BSHD ((B, S, H, d) row-major, as most model
                         code stores activations); the workspace (K', V') is always BHSD.

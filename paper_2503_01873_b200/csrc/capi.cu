@@ -140,8 +140,8 @@ int check_desc(const pasa_b200_desc* d) {
   if (d->head_dim != 64 && d->head_dim != 128)
     return fail(PASA_B200_EUNSUPPORTED, "head_dim must be 64 or 128");
   if (d->s2 > kTile) return fail(PASA_B200_EUNSUPPORTED, "s2 must be <= 128");
-  if (d->causal && (d->seq_q > d->seq_kv || d->s2 != kTile))
-    return fail(PASA_B200_EUNSUPPORTED, "causal requires S1 <= S2 and s2 == 128");
+  if (d->causal && d->seq_q > d->seq_kv)
+    return fail(PASA_B200_EUNSUPPORTED, "causal requires S1 <= S2");
   return PASA_B200_OK;
 }
 

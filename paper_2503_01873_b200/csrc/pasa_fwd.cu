@@ -168,7 +168,8 @@ __device__ __forceinline__ TileInfo tile_info(const FwdParams& p, int hkv, int i
   // blocks up to the one holding its last valid row's last key (blocks masked for every
   // row of the tile are skipped; a row may still see a block of the tile fully masked)
   const int last = min(p.S1, (ti.i + 1) * kTile) - 1;
-  ti.nblk = ti.valid ? (causal ? min((last + p.qoff) / kTile + 1, p.nkv) : p.nkv) : 0;
+  const int kb = p.s2 == kTile ? (last + p.qoff) / kTile : (last + p.qoff) / p.s2;
+  ti.nblk = ti.valid ? (causal ? min(kb + 1, p.nkv) : p.nkv) : 0;
   return ti;
 }
 
@@ -693,12 +694,13 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         tmem_wait_ld();
         if (tr) PASA_TR(t, j, 2);
         // masked columns: causal diagonal block (c > row) or a short KV block (c >= s2)
-        // causal: block j shows row r of the tile its first vis0 + r keys (any S2 - S1: up
-        // to two blocks per tile are partial)
-        const int vis0 = ti.i * kTile + p.qoff - j * kTile + 1;
-        const bool cdiag = CAUSAL && vis0 < kTile;
-        const bool diag = cdiag || p.s2 < kTile;
-        const int lim = cdiag ? vis0 + row : p.s2;
+        // causal: block j (s2 keys) shows row r of the tile its first vis0 + r keys (any
+        // S2 - S1 and s2: the tile's last blocks are partial, some fully masked for a row)
+        const bool short_blk = p.s2 < kTile;
+        const int vis0 = ti.i * kTile + p.qoff - j * (short_blk ? p.s2 : kTile) + 1;
+        const bool cdiag = CAUSAL && vis0 < (short_blk ? p.s2 : kTile);
+        const bool diag = cdiag || short_blk;
+        const int lim = cdiag ? (short_blk ? min(vis0 + row, p.s2) : vis0 + row) : p.s2;
         if (DIAGNOSE) track_store_block<NP>(s, lim, NP * h, diag, dslot);
         constexpr bool kSum = MODE == kModePasa && !kTcSum;
         float mh, sh = 0.f;

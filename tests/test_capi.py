@@ -57,6 +57,7 @@ def test_check_accepts_config1_and_qwen(lib):
     assert _check(lib, seq_q=200, seq_kv=256, s1=200, s2=64)[0] == 0
     assert _check(lib, heads_q=28, heads_kv=4, seq_q=16384, seq_kv=16384, causal=1)[0] == 0
     assert _check(lib, seq_q=512, seq_kv=1024, causal=1)[0] == 0  # bottom-right aligned
+    assert _check(lib, seq_q=256, seq_kv=320, s2=64, causal=1)[0] == 0  # causal, short KV blocks
     assert _check(lib, head_dim=64, alpha=8.0)[0] == 0
 
 
@@ -70,7 +71,6 @@ def test_check_accepts_config1_and_qwen(lib):
     (dict(head_dim=96, alpha=math.sqrt(96.0)), _lib.EUNSUPPORTED, "head_dim"),
     (dict(s2=256, s1=256), _lib.EUNSUPPORTED, "s2 must be <= 128"),
     (dict(causal=1, seq_q=1024, seq_kv=512), _lib.EUNSUPPORTED, "causal requires S1 <= S2"),
-    (dict(causal=1, s2=64), _lib.EUNSUPPORTED, "causal requires S1 <= S2"),
     (dict(layout=2), _lib.EINVAL, "layout must be 0 (BHSD) or 1 (BSHD)"),
 ])
 def test_check_rejects(lib, kw, code, msg):

@@ -532,13 +532,14 @@ def test_fused_prepass_rank1_bitexact(dev, orc, D, s2, nblk):
         assert np.array_equal(vp[0, h].double().cpu().numpy(), orc.f16(v[0, h] * 2.0 ** -c0))
 
 
-@pytest.mark.parametrize("B,Hq,Hkv,S,D,causal,beta", [
-    (1, 28, 4, 512, 128, True, BETA_STAR),   # 28 pieces of one query head (GQA units split)
-    (5, 14, 2, 256, 64, True, BETA_STAR),    # pieces of 3, 3, 1 query heads per unit
-    (3, 20, 20, 256, 64, False, BETA_STAR),  # runs of two whole units per piece
-    (2, 8, 2, 384, 128, True, 0.0),          # beta = 0: FA16, no pre-pass
+@pytest.mark.parametrize("B,Hq,Hkv,S,D,causal,beta,s2", [
+    (1, 28, 4, 512, 128, True, BETA_STAR, 128),   # 28 pieces of one query head (GQA units split)
+    (5, 14, 2, 256, 64, True, BETA_STAR, 128),    # pieces of 3, 3, 1 query heads per unit
+    (3, 20, 20, 256, 64, False, BETA_STAR, 128),  # runs of two whole units per piece
+    (2, 8, 2, 384, 128, True, 0.0, 128),          # beta = 0: FA16, no pre-pass
+    (2, 6, 2, 384, 128, True, BETA_STAR, 64),     # causal with short KV blocks
 ])
-def test_host_pipeline_pieces_bit_identical(dev, B, Hq, Hkv, S, D, causal, beta):
+def test_host_pipeline_pieces_bit_identical(dev, B, Hq, Hkv, S, D, causal, beta, s2):
     """pasa_b200_attention_host (pieces of query heads over H2D / pre-pass / four compute /
     D2H streams) returns exactly the device path's output for every piece layout."""
     from paper_2503_01873_b200 import _lib, flash_fp16_fwd, pasa_attention_fwd
@@ -547,10 +548,10 @@ def test_host_pipeline_pieces_bit_identical(dev, B, Hq, Hkv, S, D, causal, beta)
     k = (torch.randn(B, Hkv, S, D, generator=g) * 3).half()
     v = torch.randn(B, Hkv, S, D, generator=g).half()
     qd, kd, vd = (x.to(dev) for x in (q, k, v))
-    want = (pasa_attention_fwd(qd, kd, vd, beta, causal=causal) if beta
-            else flash_fp16_fwd(qd, kd, vd, causal=causal)).cpu()
+    want = (pasa_attention_fwd(qd, kd, vd, beta, causal=causal, s2=s2) if beta
+            else flash_fp16_fwd(qd, kd, vd, causal=causal, s2=s2)).cpu()
     L = _lib.load()
-    desc = _lib.Desc(B, Hq, Hkv, S, S, D, 128, 128, int(causal), 0, beta, math.sqrt(D))
+    desc = _lib.Desc(B, Hq, Hkv, S, S, D, 128, s2, int(causal), 0, beta, math.sqrt(D))
     qh, kh, vh = (x.pin_memory() for x in (q, k, v))
     oh = torch.empty_like(qh).pin_memory()
     for _ in range(2):  # second call reuses the cached buffers, streams and events
@@ -593,11 +594,14 @@ def test_run_diagnostics_match_reference(dev, orc, ref):
         d1.store_finite_min, d1.store_finite_max, d1.out_total)
 
 
-@pytest.mark.parametrize("S1,S2,D", [(256, 640, 128), (128, 512, 64),
-                                     (192, 256, 128),   # S2 - S1 = 64: two partial blocks
-                                     (200, 512, 64),    # ragged S1, S2 - S1 = 312
-                                     (136, 640, 128)])  # ragged S1, S2 - S1 = 504
-def test_fwd_causal_bottom_right(dev, orc, S1, S2, D):
+@pytest.mark.parametrize("S1,S2,D,s2", [(256, 640, 128, 128), (128, 512, 64, 128),
+                                        (192, 256, 128, 128),  # S2 - S1 = 64: two partial blocks
+                                        (200, 512, 64, 128),   # ragged S1, S2 - S1 = 312
+                                        (136, 640, 128, 128),  # ragged S1, S2 - S1 = 504
+                                        (256, 256, 128, 64),   # short KV blocks: two per tile row
+                                        (256, 320, 64, 32),    # S2 - S1 = 64, s2 = 32
+                                        (128, 200, 128, 25)])  # s2 = 25, offset 72
+def test_fwd_causal_bottom_right(dev, orc, S1, S2, D, s2):
     """Causal with S1 < S2 (a query chunk after S2 - S1 cached keys, any offset, ragged S1):
     row r sees keys <= r + S2 - S1; against the model with q_offset and the masked FP64
     golden."""
@@ -606,9 +610,9 @@ def test_fwd_causal_bottom_right(dev, orc, S1, S2, D):
     q = orc.generate("hybrid", 0.0, 10.0, 51, 1, 2, S1, D, tensor_ids=(0,))[0]
     k, v = orc.generate("hybrid", 0.0, 10.0, 52, 1, 2, S2, D, tensor_ids=(1, 2))
     s1 = 128 if S1 % 128 == 0 else S1  # ragged S1: the kernel still runs 128-row tiles
-    pb = Problem(q, k, v, s1=s1, causal=True, q_offset=S2 - S1)
+    pb = Problem(q, k, v, s1=s1, s2=s2, causal=True, q_offset=S2 - S1)
     qt, kt, vt = (torch.from_numpy(x).half().to(dev) for x in (q, k, v))
-    o = pasa_attention_fwd(qt, kt, vt, causal=True, s1=s1).double().cpu().numpy()
+    o = pasa_attention_fwd(qt, kt, vt, causal=True, s1=s1, s2=s2).double().cpu().numpy()
     gold = orc.golden(pb)
     gold_dev = ba.golden_attention(qt, kt, vt, causal=True).cpu().numpy()
     assert np.abs(gold_dev - gold).max() <= 1e-12  # the device golden's alignment agrees
@@ -678,6 +682,9 @@ def _random_cases(n=16, seed=2025):
             s2 = 128
             S2 = 128 * int(rng.integers(1, 6))
             S1 = 128 * int(rng.integers(1, S2 // 128 + 1))
+            if rng.random() < 0.4:  # short KV blocks under the causal mask
+                s2 = int(rng.choice([64, 32, 25]))
+                S2 = s2 * (S2 // s2)
         else:
             s2 = int(rng.choice([128, 128, 64, 32, 25]))
             S2 = s2 * int(rng.integers(1, 8))
