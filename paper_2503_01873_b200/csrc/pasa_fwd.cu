@@ -54,7 +54,7 @@ constexpr bool kPingPong = (D == 64 ? PASA_PINGPONG_D64 : PASA_PINGPONG) != 0;
 // balances MUFU against issue slots at 6 (5-7 within noise, +2-3 % over 4 once P is
 // released in parts and the tiles' exp passes overlap); at d = 64 the FMA pipe and the
 // issue slots are shared with twice the softmax work per FLOP and MUFU-only wins
-// (measured: tools/variants.py, +6 % at d = 64).
+// (measured: tools/variants.py, +6 % at d = 64 over 1/4; 1/8 and 1/16 lose 9-10 %).
 #ifndef PASA_POLY_EVERY
 #define PASA_POLY_EVERY 6
 #endif
