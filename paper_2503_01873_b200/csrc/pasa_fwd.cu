@@ -120,11 +120,16 @@ static_assert(128 * PASA_WG0_REGS + 512 * PASA_SM_REGS <= 61440, "register pool"
   } while (0)
 #endif
 
+// K'/V' pipeline stages at d = 64 (d = 128 fills shared memory at two); 3 or 4 at d = 64
+// measured 1.5 % slower than 2 (tools/variants.py): the loads are not what the tiles wait on
+#ifndef PASA_STAGES_D64
+#define PASA_STAGES_D64 2
+#endif
 template <int D>
 struct FwdCfg {
   static constexpr int NT = 2;
-  static constexpr int KS = 2;
-  static constexpr int VS = 2;
+  static constexpr int KS = D == 64 ? PASA_STAGES_D64 : 2;
+  static constexpr int VS = D == 64 ? PASA_STAGES_D64 : 2;
   static constexpr int NBOX = D / 64;                     // 128-byte swizzle boxes per row
   static constexpr int BOX_BYTES = kTile * 128;           // 128 rows x 64 halves
   static constexpr int TILE_BYTES = NBOX * BOX_BYTES;     // one 128 x D fp16 tile
