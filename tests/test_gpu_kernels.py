@@ -714,3 +714,32 @@ def test_fwd_random_shapes_vs_model(dev, orc, case):
     # near-flat softmax (e.g. uniform(0, 0.5)) sums thousands of P ~ 1 terms, where the tensor
     # core's accumulation order alone moves the result by about the model's own error
     assert orc.rmse(o, model) <= 1.5 * r_model + 2e-4
+
+
+def test_pdl_off_bit_identical(dev, tmp_path):
+    """Programmatic dependent launch only moves when the next grid's CTAs become resident:
+    the pre-pass + forward with PASA_B200_NO_PDL=1 (read once per process, so in a
+    subprocess) return the same bits."""
+    import subprocess
+    import sys
+    from paper_2503_01873_b200 import pasa_attention_fwd
+    script = (
+        "import sys, torch, numpy as np; sys.path.insert(0, %r)\n"
+        "from paper_2503_01873_b200 import pasa_attention_fwd\n"
+        "g = torch.Generator().manual_seed(11)\n"
+        "q = (torch.randn(1, 4, 640, 128, generator=g) * 4).half().cuda()\n"
+        "k = (torch.randn(1, 2, 640, 128, generator=g) * 4).half().cuda()\n"
+        "v = torch.randn(1, 2, 640, 128, generator=g).half().cuda()\n"
+        "o = pasa_attention_fwd(q, k, v, causal=True)\n"
+        "np.save(sys.argv[1], o.cpu().view(torch.int16).numpy())\n") % \
+        os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "o.npy")
+    env = dict(os.environ, PASA_B200_NO_PDL="1")
+    r = subprocess.run([sys.executable, "-c", script, out], env=env, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    g = torch.Generator().manual_seed(11)
+    q = (torch.randn(1, 4, 640, 128, generator=g) * 4).half().to(dev)
+    k = (torch.randn(1, 2, 640, 128, generator=g) * 4).half().to(dev)
+    v = torch.randn(1, 2, 640, 128, generator=g).half().to(dev)
+    o = pasa_attention_fwd(q, k, v, causal=True).cpu().view(torch.int16).numpy()
+    assert np.array_equal(np.load(out), o)
