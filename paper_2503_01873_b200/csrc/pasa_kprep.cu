@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(128) pasa_kprep_small_kernel(const KprepParams
 // as the temporal attention's N = 25): one warp per block, each lane owns D/64 head-dim
 // pairs; FP32 column sums over the s2 keys ascending, then one FMA per element -- the same
 // arithmetic as pasa_kprep_rank1_kernel (orc_preprocess_keys, p_acc = PR1) -- and max|V|.
-template <int D>
+template <int D, int MAXR>
 __global__ void __launch_bounds__(256) pasa_kprep_rank1_small_kernel(const KprepParams p,
                                                                       int nblk_total) {
   constexpr int U = D / 64;  // half2 columns per lane
@@ -236,6 +236,50 @@ __global__ void __launch_bounds__(256) pasa_kprep_rank1_small_kernel(const Kprep
 #pragma unroll
   for (int u = 0; u < U; ++u) cs[u] = make_float2(0.f, 0.f);
   float vm = 0.f;
+  if (MAXR > 0 && s2 <= MAXR) {
+    // short blocks (e.g. the SVD temporal N = 25): every row's K and V loads are issued
+    // before the first is used (the row loop below waits a memory latency per row), and the
+    // K values stay in registers for the output pass; same sums in the same order.
+    __half2 kr[MAXR > 0 ? MAXR : 1][U], vr[MAXR > 0 ? MAXR : 1][U];
+#pragma unroll
+    for (int c = 0; c < MAXR; ++c)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        kr[c][u] = c < s2 ? kg[c * RS2 + lane + 32 * u] : __half2{};
+        vr[c][u] = c < s2 ? vg[c * RS2 + lane + 32 * u] : __half2{};
+      }
+#pragma unroll
+    for (int c = 0; c < MAXR; ++c)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (c < s2) {
+          const float2 k2 = __half22float2(kr[c][u]);
+          cs[u].x = __fadd_rn(cs[u].x, k2.x);
+          cs[u].y = __fadd_rn(cs[u].y, k2.y);
+        }
+        const float2 v2 = __half22float2(__habs2(vr[c][u]));  // padded rows are 0
+        vm = fmaxf(vm, fmaxf(v2.x, v2.y));
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) vm = fmaxf(vm, __shfl_xor_sync(0xffffffffu, vm, o));
+    if (lane == 0) atomicMax(reinterpret_cast<int*>(p.vmax) + bh, __float_as_int(vm));  // vm >= 0
+    const float dm = p.diag - p.off;
+    float2 os[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) os[u] = make_float2(__fmul_rn(p.off, cs[u].x), __fmul_rn(p.off, cs[u].y));
+    __half2* out = reinterpret_cast<__half2*>(reinterpret_cast<__half*>(p.kp) + base);
+#pragma unroll
+    for (int c = 0; c < MAXR; ++c)
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c < s2) {
+          const float2 k2 = __half22float2(kr[c][u]);
+          const float a = __fmul_rn(__fmaf_rn(dm, k2.x, os[u].x), p.lscale);
+          const float b = __fmul_rn(__fmaf_rn(dm, k2.y, os[u].y), p.lscale);
+          out[c * (D / 2) + lane + 32 * u] = __floats2half2_rn(a, b);
+        }
+    return;
+  }
   for (int c = 0; c < s2; ++c) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -303,10 +347,41 @@ __global__ void __launch_bounds__(256) pasa_vscale_kernel(const VscaleParams p) 
   }
 }
 
+// Short heads (fewer than 1024 16-byte words, e.g. the SVD temporal N = 25 with 46080
+// heads): one block per head would leave most threads idle and make block scheduling the
+// cost, so the words of all heads are walked flat, head = word / words-per-head.
+template <int D>
+__global__ void __launch_bounds__(256) pasa_vscale_flat_kernel(const VscaleParams p, int n8,
+                                                               int total8) {
+  constexpr int C8 = D / 8;
+  sm100::pdl_trigger();
+  sm100::pdl_wait();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total8; i += gridDim.x * blockDim.x) {
+    const int bh = i / n8, r = i - bh * n8;
+    const int c0 = pasa_inflation(p.S2, p.vmax[bh]);
+    const __half2 sc = __half2half2(__float2half_rn(ldexpf(1.0f, -c0)));
+    const __half* vin = reinterpret_cast<const __half*>(p.v) + (bh / p.Hkv) * p.in_bs +
+                        (bh % p.Hkv) * p.in_hs + static_cast<long long>(r / C8) * p.in_ss +
+                        (r % C8) * 8;
+    uint4 w = *reinterpret_cast<const uint4*>(vin);
+    __half2* h = reinterpret_cast<__half2*>(&w);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = __hmul2(h[k], sc);
+    reinterpret_cast<uint4*>(p.vp)[i] = w;
+  }
+}
+
 cudaError_t launch_vscale(const VscaleParams& p, cudaStream_t stream) {
   const long long bh = p.total / p.per_head;
   const long long chunks = (p.per_head / 8 + 1023) / 1024;
-  const dim3 grid(static_cast<unsigned>(bh), static_cast<unsigned>(chunks < 65535 ? chunks : 65535));
+  const bool flat = p.per_head / 8 < 1024 && p.total / 8 < (1LL << 31);
+  dim3 grid(static_cast<unsigned>(bh), static_cast<unsigned>(chunks < 65535 ? chunks : 65535));
+  if (flat) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const long long blocks = (p.total / 8 + 255) / 256;
+    grid = dim3(static_cast<unsigned>(blocks < 16LL * sms ? blocks : 16LL * sms));
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(256);
@@ -316,6 +391,9 @@ cudaError_t launch_vscale(const VscaleParams& p, cudaStream_t stream) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const int n8 = static_cast<int>(p.per_head / 8), total8 = static_cast<int>(p.total / 8);
+  if (flat && p.D == 128) return cudaLaunchKernelEx(&cfg, pasa_vscale_flat_kernel<128>, p, n8, total8);
+  if (flat && p.D == 64) return cudaLaunchKernelEx(&cfg, pasa_vscale_flat_kernel<64>, p, n8, total8);
   if (p.D == 128) return cudaLaunchKernelEx(&cfg, pasa_vscale_kernel<128>, p);
   if (p.D == 64) return cudaLaunchKernelEx(&cfg, pasa_vscale_kernel<64>, p);
   return cudaErrorInvalidValue;
@@ -325,8 +403,13 @@ cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stre
   if (p.s2 != kTile && p.rank1 && p.v && (p.D == 64 || p.D == 128)) {
     const int total = (p.S2 / p.s2) * B * Hkv;
     const int grid = (total + 7) / 8;
-    if (p.D == 64) pasa_kprep_rank1_small_kernel<64><<<grid, 256, 0, stream>>>(p, total);
-    else pasa_kprep_rank1_small_kernel<128><<<grid, 256, 0, stream>>>(p, total);
+    if (p.D == 64) {
+      if (p.s2 <= 32) pasa_kprep_rank1_small_kernel<64, 32><<<grid, 256, 0, stream>>>(p, total);
+      else pasa_kprep_rank1_small_kernel<64, 0><<<grid, 256, 0, stream>>>(p, total);
+    } else {
+      if (p.s2 <= 32) pasa_kprep_rank1_small_kernel<128, 32><<<grid, 256, 0, stream>>>(p, total);
+      else pasa_kprep_rank1_small_kernel<128, 0><<<grid, 256, 0, stream>>>(p, total);
+    }
     return cudaGetLastError();
   }
   if (p.s2 != kTile) {
