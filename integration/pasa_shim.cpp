@@ -11,13 +11,16 @@
 // Semantics follow the reference: same validation and exception types
 // (pasa.cpp:200-211), inputs are FP16-exact doubles (tensor.hpp:19-20), output
 // is tagged with the policy's vector precision (pasa.cpp:242).  Only the
-// PASA_FP16 policy is offloaded; anything else throws (no CPU fallback).
+// PASA_FP16 policy is offloaded; pasa_attention with any other policy throws (no CPU
+// fallback); preprocess_keys under a non-PASA policy is the reference's FP64 range
+// diagnostic and keeps the reference's own gemm.
 #include <cmath>
 #include <cstring>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "pasa/matrix.hpp"
 #include "pasa/pasa.hpp"
 #include "pasa_b200.h"
 
@@ -88,10 +91,14 @@ PasaParams PasaParams::make(size_t s2, double beta, double alpha, Prec prec) {
 }
 
 // K^T * M on the device (bit-exact with the reference's FP32 sequential GEMM).
+//
+// Other policies are the reference's own diagnostics, not the offloaded path: range_report
+// (bench.cpp:136, run by sweep() when SweepOptions::diagnose is set) asks for the FP64 K'
+// ranges with the GoldenFp64 policy.  Those go to the reference's gemm (matrix.o, in the
+// link set) exactly as pasa.cpp:53-56 does, so the drop-in keeps every pasa.o feature.
 Matrix2D preprocess_keys(const Matrix2D& k_block, const Matrix2D& m,
                          const PrecisionPolicy& policy) {
-  if (!is_pasa_fp16(policy))
-    throw std::invalid_argument("pasa_b200 preprocess_keys offloads the PASA_FP16 policy only");
+  if (!is_pasa_fp16(policy)) return gemm(transpose(k_block), m, false, policy);
   const size_t s2 = k_block.rows, d = k_block.cols;
   if (m.rows != s2 || m.cols != s2) throw std::invalid_argument("gemm: inner dimensions disagree");
   // Recover (beta, alpha) from the two distinct entries: diag - off = 1/alpha.

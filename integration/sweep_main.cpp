@@ -2,7 +2,8 @@
 // (pasa::sweep, bench.cpp:170-247) with pasa.o replaced by pasa_shim.o, so
 // every PASA_FP16 cell runs on the B200 while FA_PARTIAL_FP16 stays on the
 // reference CPU path.  Prints the reference's CSV report (bench.hpp:105-107).
-// Usage: ref_sweep_b200 [heads] [seq]
+// Usage: ref_sweep_b200 [heads] [seq] [diagnose 0|1]  (diagnose: the reference's FP64 range
+// report, whose K' pre-pass under GoldenFp64 stays on the reference's gemm)
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -31,6 +32,7 @@ int main(int argc, char** argv) {
     specs.push_back(s);
   }
   pasa::SweepOptions opts;
+  opts.diagnose = argc > 3 && std::strtoul(argv[3], nullptr, 10) != 0;
   opts.policies = {pasa::PolicyId::PasaFp16, pasa::PolicyId::FaPartialFp16};
   const auto rows = pasa::sweep(specs, opts);
   std::fputs(pasa::report_csv(rows).c_str(), stdout);

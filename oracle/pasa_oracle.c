@@ -595,7 +595,7 @@ typedef struct {
 ORC_API double orc_model_inflation(double vmax, size_t S2, double lscale) {
   (void)lscale;
   const float need = (float)S2 * (float)vmax * (1.0f / 16384.0f);
-  if (!(need > 1.0f)) return 0.0;
+  if (!(need > 1.0f) || !(need < 3.0e38f)) return 0.0; /* non-finite V: c0 = 0 */
   int e = ilogbf(need); /* floor(log2 need), exact */
   return (double)(ldexpf(1.0f, e) == need ? e : e + 1);
 }

@@ -27,10 +27,6 @@ class Desc(C.Structure):
     ]
 
 
-class Diag(C.Structure):
-    _fields_ = [("out_nonfinite", C.c_ulonglong), ("out_total", C.c_ulonglong)]
-
-
 _LIB = None
 
 

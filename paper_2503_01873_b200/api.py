@@ -254,20 +254,47 @@ def _check_device_tensors(fn: str, q: torch.Tensor, k: torch.Tensor, v: torch.Te
         raise ValueError(f"{fn}: out must be a contiguous tensor of q's shape {tuple(q.shape)}")
 
 
-_WS: dict[int, torch.Tensor] = {}
+_WS: dict[tuple[int, int], torch.Tensor] = {}
 
 
-def workspace_for(desc: _lib.Desc, device: torch.device) -> torch.Tensor:
-    """One cached workspace per device, grown to the largest request (the caching
-    allocator keeps reuse stream-ordered on the current stream; pass ``workspace=``
-    explicitly when launching on several streams at once)."""
+def workspace_for(desc: _lib.Desc, device: torch.device,
+                  stream: "torch.cuda.Stream | None" = None) -> torch.Tensor:
+    """The cached K'/V' workspace of (device, stream), grown to the largest request.
+
+    Each stream gets its own buffer, allocated while that stream is current, so torch's
+    caching allocator only hands its memory out again in that stream's order: two calls on
+    different streams never share a workspace, and a buffer replaced by a larger one cannot
+    be reused while a kernel on its stream may still read it."""
     n = _lib.load().pasa_b200_workspace_size(C.byref(desc))
-    key = device.index if device.index is not None else torch.cuda.current_device()
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    s = stream if stream is not None else torch.cuda.current_stream(idx)
+    key = (idx, s.cuda_stream)
     ws = _WS.get(key)
     if ws is None or ws.numel() < n:
-        ws = torch.empty(n, dtype=torch.uint8, device=device)
+        with torch.cuda.device(idx), torch.cuda.stream(s):
+            ws = torch.empty(n, dtype=torch.uint8, device=device)
         _WS[key] = ws
     return ws[:n]
+
+
+def _launch_stream(dev: torch.device, stream: "torch.cuda.Stream | None"):
+    """(launch stream, current stream).  A launch on another stream first waits for the
+    current one, where the inputs (and any contiguous copies made here) were produced."""
+    cur = torch.cuda.current_stream(dev)
+    s = stream if stream is not None else cur
+    if s != cur:
+        s.wait_stream(cur)
+    return s, cur
+
+
+def _hold_for(s: "torch.cuda.Stream", cur: "torch.cuda.Stream", *tensors) -> None:
+    """Keep tensors allocated on other streams alive until the launch stream is done with
+    them (torch's allocator otherwise only tracks their allocation stream)."""
+    if s == cur:
+        return
+    for t in tensors:
+        if t is not None:
+            t.record_stream(s)
 
 
 def pasa_attention_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, beta: float = BETA_STAR,
@@ -276,9 +303,10 @@ def pasa_attention_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, beta: 
                        stream: torch.cuda.Stream | None = None,
                        diag: "RunDiagnostics | None" = None, layout: str = "bhsd") -> torch.Tensor:
     """Device entry point: fp16 CUDA tensors (BHSD, or BSHD with ``layout="bshd"``),
-    asynchronous on ``stream``.  ``diag`` (optional) is merged with the device
-    RunDiagnostics of this call (the diagnostic kernel instantiation; synchronises the
-    stream)."""
+    asynchronous on ``stream`` (default: the current stream; another stream first waits
+    for the current one, and everything it reads or writes stays allocated until it is
+    done).  ``diag`` (optional) is merged with the device RunDiagnostics of this call (the
+    diagnostic kernel instantiation; synchronises the stream)."""
     L = _lib.load()
     _check_device_tensors("pasa_attention_fwd", q, k, v, out)
     if workspace is not None and (not workspace.is_cuda or workspace.device != q.device):
@@ -287,21 +315,24 @@ def pasa_attention_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, beta: 
     desc = _desc(q, k, s1, s2, beta, math.sqrt(float(q.shape[-1])), causal, layout)
     _lib.check(L.pasa_b200_check(C.byref(desc)))
     with torch.cuda.device(q.device):  # the library launches on the current device
-        if out is None:
-            out = torch.empty_like(q)
-        if workspace is None:
-            workspace = workspace_for(desc, q.device)
-        st = (stream or torch.cuda.current_stream(q.device)).cuda_stream
-        dbuf = None
-        if diag is not None:
-            dbuf = torch.empty(C.sizeof(_lib.Diag), dtype=torch.uint8, device=q.device)
-            _lib.check(L.pasa_b200_diag_reset(dbuf.data_ptr(), st))
-        _lib.check(L.pasa_b200_attention_fwd(C.byref(desc), q.data_ptr(), k.data_ptr(),
-                                             v.data_ptr(), out.data_ptr(), workspace.data_ptr(),
-                                             workspace.numel() * workspace.element_size(),
-                                             dbuf.data_ptr() if dbuf is not None else None, st))
+        s, cur = _launch_stream(q.device, stream)
+        with torch.cuda.stream(s):  # out / workspace / diag are allocated in s's order
+            if out is None:
+                out = torch.empty_like(q)
+            if workspace is None:
+                workspace = workspace_for(desc, q.device, s)
+            dbuf = None
+            if diag is not None:
+                dbuf = torch.empty(C.sizeof(_lib.Diag), dtype=torch.uint8, device=q.device)
+                _lib.check(L.pasa_b200_diag_reset(dbuf.data_ptr(), s.cuda_stream))
+            _lib.check(L.pasa_b200_attention_fwd(C.byref(desc), q.data_ptr(), k.data_ptr(),
+                                                 v.data_ptr(), out.data_ptr(), workspace.data_ptr(),
+                                                 workspace.numel() * workspace.element_size(),
+                                                 dbuf.data_ptr() if dbuf is not None else None,
+                                                 s.cuda_stream))
+        _hold_for(s, cur, q, k, v, out, workspace)
     if dbuf is not None:
-        torch.cuda.current_stream(q.device).synchronize() if stream is None else stream.synchronize()
+        s.synchronize()
         host = _lib.Diag.from_buffer_copy(bytes(dbuf.cpu().numpy()))
         diag.merge(RunDiagnostics.from_c(host))
     return out
@@ -312,18 +343,21 @@ def flash_fp16_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, causal: bo
                    stream: torch.cuda.Stream | None = None, layout: str = "bhsd") -> torch.Tensor:
     """The naive FP16 FlashAttention baseline on the same pipeline (FA_PARTIAL_FP16
     semantics of flash_attention, attention.cpp:92-180): scale after the FP16 score
-    store, so inputs whose |QK^T| exceeds 65504 produce NaN -- the failure PASA removes."""
+    store, so inputs whose |QK^T| exceeds 65504 produce NaN -- the failure PASA removes.
+    Stream semantics as pasa_attention_fwd."""
     L = _lib.load()
     _check_device_tensors("flash_fp16_fwd", q, k, v, out)
     q, k, v = (t if t.is_contiguous() else t.contiguous() for t in (q, k, v))
     desc = _desc(q, k, s1, s2, 0.0, math.sqrt(float(q.shape[-1])), causal, layout)
     _lib.check(L.pasa_b200_check(C.byref(desc)))
-    if out is None:
-        out = torch.empty_like(q)
     with torch.cuda.device(q.device):
-        st = (stream or torch.cuda.current_stream(q.device)).cuda_stream
-        _lib.check(L.pasa_b200_flash_fp16_fwd(C.byref(desc), q.data_ptr(), k.data_ptr(),
-                                              v.data_ptr(), out.data_ptr(), st))
+        s, cur = _launch_stream(q.device, stream)
+        with torch.cuda.stream(s):
+            if out is None:
+                out = torch.empty_like(q)
+            _lib.check(L.pasa_b200_flash_fp16_fwd(C.byref(desc), q.data_ptr(), k.data_ptr(),
+                                                  v.data_ptr(), out.data_ptr(), s.cuda_stream))
+        _hold_for(s, cur, q, k, v, out)
     return out
 
 

@@ -769,6 +769,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(p_part + 8 * (q * NT + t));
+          if (q == 0 && tr) PASA_TR(t, j, 9);  // first P part released
         };
         float lsum;
         if (MODE == kModeFa16 || fast2)

@@ -21,8 +21,17 @@
 //
 // Persistent CTAs walk the tiles; 6 warps: warp 0 loads (TMA, a two-stage ring, so the next
 // tile's loads overlap this one's compute), warp 1 issues the MMAs, warps 2-5 run the
-// softmax with one thread per row (TMEM lane quadrant = warp % 4).  256 TMEM columns (S'/P
-// at +0, T at +128), so two CTAs share an SM at d = 64.
+// softmax with one thread per row (TMEM lane quadrant = warp % 4).  TMEM: S'/P at +0, T at
+// +128, T_clean at +128 + D (256 columns at d = 64, so two CTAs share an SM; 512 at d = 128).
+//
+// Non-finite V: the tile's P V' also multiplies each row's zero P entries by the other
+// sequences' V' rows, and 0 x Inf = NaN would leak one sequence's Inf/NaN into its
+// neighbours (the unpacked kernel keeps heads apart).  So the MMA warp scans the tile's V'
+// rows while S' runs; for a tile with a non-finite V' row it issues P V' twice -- into T
+// (the poisoned sequences read it: exactly what they get alone) and, after zeroing the
+// poisoned sequences' V' rows in shared memory, into T_clean (everyone else reads it).
+// The zeroed rows stay zero until TMA refills them, so the stale slots of a ragged last
+// tile are clean too.  Clean tiles pay only the scan.
 #include <cuda.h>
 #include <cuda_fp16.h>
 
@@ -43,7 +52,10 @@ struct PackedCfg {
   static constexpr int STAGES = 2;
   static constexpr int SMEM_BAR = STAGES * STAGE_BYTES;
   static constexpr int SMEM_BYTES = SMEM_BAR + 128 + 1024;
+  static constexpr int NUM_BARS = 2 * STAGES + 6;  // in_full/empty, s/p/t_full, t_empty, aux, mask
   static constexpr int THREADS = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 softmax
+  static constexpr uint32_t TMEM_COLS = D == 64 ? 256 : 512;
+  static constexpr uint32_t T_CLEAN = 128 + D;  // P V' over zeroed poisoned rows
 };
 
 __device__ __forceinline__ float lo_f(uint32_t u) { return __low2float(u32_as_h2(u)); }
@@ -74,7 +86,11 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
   const uint32_t in_empty = in_full + 8 * ST;   // [ST]: the stage's MMAs are done
   const uint32_t s_full = in_empty + 8 * ST, p_full = s_full + 8, t_full = p_full + 8,
                  t_empty = t_full + 8;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Cfg::SMEM_BAR + 8 * (2 * ST + 4));
+  const uint32_t aux = t_empty + 8;       // the first P V' of a poisoned tile is done
+  const uint32_t mask_full = aux + 8;     // the tile's poisoned-slot mask is published
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Cfg::SMEM_BAR + 8 * Cfg::NUM_BARS);
+  // [it % 2]: bit s = slot s of tile it holds a non-finite V' row
+  volatile uint32_t* bad_mask = tmem_holder + 2;
   const int warp = static_cast<int>(warp_id());
   const int lane = threadIdx.x & 31;
   const int W = p.W;                                // slot stride (rows / keys)
@@ -89,6 +105,8 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
     mbar_init(p_full, 4);
     mbar_init(t_full, 1);
     mbar_init(t_empty, 4);
+    mbar_init(aux, 1);
+    mbar_init(mask_full, 1);
     fence_barrier_init();
   }
   {  // V' rows outside the sequences' N-row slots must read as zero (P = 0 there, and 0 x
@@ -99,7 +117,7 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
-  if (warp == 0) tmem_alloc<256>(tmem_holder);
+  if (warp == 0) tmem_alloc<Cfg::TMEM_COLS>(tmem_holder);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -129,18 +147,20 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer
-    if (elect_one()) {
-      constexpr uint32_t kIdS = idesc_f16(128, 128, 0, 0, 0);
-      constexpr uint32_t kIdPV = idesc_f16(128, D, 0, 0, 1);
-      int it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int st = it % ST;
-        const uint32_t base = sb + st * Cfg::STAGE_BYTES;
-        mbar_wait(in_full + 8 * st, (it / ST) & 1);
-        tc_fence_after();
-        // S' = Q K'^T (SS, F16 accumulator) into columns [0, 128); in-order after the
-        // previous tile's PV, so its P columns are free
+    // ---- MMA issuer (one elected lane); the whole warp scans V' for non-finite rows
+    const bool leader = elect_one();
+    constexpr uint32_t kIdS = idesc_f16(128, 128, 0, 0, 0);
+    constexpr uint32_t kIdPV = idesc_f16(128, D, 0, 0, 1);
+    int it = 0, npois = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int st = it % ST, nseq = min(p.P, p.BH - tile * p.P);
+      const uint32_t base = sb + st * Cfg::STAGE_BYTES;
+      const uint32_t vbase = base + 2 * Cfg::TILE_BYTES;
+      mbar_wait(in_full + 8 * st, (it / ST) & 1);
+      tc_fence_after();
+      // S' = Q K'^T (SS, F16 accumulator) into columns [0, 128); in-order after the
+      // previous tile's PV, so its P columns are free
+      if (leader) {
 #pragma unroll
         for (int s = 0; s < D / 16; ++s) {
           const uint32_t off = (s / 4) * Cfg::BOX_BYTES + (s % 4) * 32;
@@ -148,19 +168,67 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
                   smem_desc_sw128(base + Cfg::TILE_BYTES + off, 16, 1024), kIdS, s > 0);
         }
         tc_commit(s_full);
-        // T = P V' (TS: P packed in columns [0, 64), V' MN-major) into [128, 128 + D), once
-        // the softmax has stored P and read the previous tile's T
-        mbar_wait(p_full, it & 1);
-        mbar_wait(t_empty, (it & 1) ^ 1);
-        tc_fence_after();
+      }
+      // while S' runs: which slots' V' rows hold Inf / NaN?  0 x v is NaN exactly for a
+      // non-finite v, so one HFMA2 per pair accumulates the verdict.
+      uint32_t bad = 0;
+      for (int r = lane; r < nseq * W; r += 32) {
+        if (r % W >= p.N) continue;  // gap rows are zero
+        __half2 acc = __float2half2_rn(0.f);
+#pragma unroll
+        for (int bx = 0; bx < Cfg::NBOX; ++bx) {
+          const uint4* row = reinterpret_cast<const uint4*>(smem + (vbase - sb) + bx * Cfg::BOX_BYTES + r * 128);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint4 x = row[c];
+            acc = __hfma2(u32_as_h2(x.x), __float2half2_rn(0.f), acc);
+            acc = __hfma2(u32_as_h2(x.y), __float2half2_rn(0.f), acc);
+            acc = __hfma2(u32_as_h2(x.z), __float2half2_rn(0.f), acc);
+            acc = __hfma2(u32_as_h2(x.w), __float2half2_rn(0.f), acc);
+          }
+        }
+        if (__hisnan(__low2half(acc)) || __hisnan(__high2half(acc))) bad |= 1u << (r / W);
+      }
+      bad = __reduce_or_sync(0xffffffffu, bad);
+      // T = P V' (TS: P packed in columns [0, 64), V' MN-major) into [128, 128 + D), once
+      // the softmax has stored P and read the previous tile's T
+      mbar_wait(p_full, it & 1);
+      // publish the mask (release) only now: the softmax has finished tile it - 1 (p_full),
+      // so mask_full is never two phases ahead of its reader and slot it & 1 is free
+      if (leader) {
+        bad_mask[it & 1] = bad;
+        mbar_arrive(mask_full);
+      }
+      mbar_wait(t_empty, (it & 1) ^ 1);
+      tc_fence_after();
+      auto issue_pv = [&](uint32_t dcol) {
 #pragma unroll
         for (int s = 0; s < 8; ++s)
-          umma_ts(tmem_base + 128, tmem_base + s * 8,
-                  smem_desc_sw128(base + 2 * Cfg::TILE_BYTES + s * 2048, Cfg::BOX_BYTES, 1024),
-                  kIdPV, s > 0);
+          umma_ts(tmem_base + dcol, tmem_base + s * 8,
+                  smem_desc_sw128(vbase + s * 2048, Cfg::BOX_BYTES, 1024), kIdPV, s > 0);
+      };
+      if (leader) issue_pv(128);
+      if (bad) {
+        // the poisoned sequences keep T; the rest get T_clean over zeroed poisoned rows
+        if (leader) tc_commit(aux);
+        mbar_wait(aux, npois & 1);
+        ++npois;
+        for (int e = lane; e < nseq * W * Cfg::NBOX * 8; e += 32) {
+          const int r = e / (Cfg::NBOX * 8), bx = (e / 8) % Cfg::NBOX, c = e % 8;
+          if ((bad >> (r / W)) & 1u)
+            *reinterpret_cast<uint4*>(smem + (vbase - sb) + bx * Cfg::BOX_BYTES + r * 128 + c * 16) =
+                make_uint4(0, 0, 0, 0);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        tc_fence_after();
+        if (leader) issue_pv(Cfg::T_CLEAN);
+      }
+      if (leader) {
         tc_commit(t_full);
         tc_commit(in_empty + 8 * st);
       }
+      __syncwarp();
     }
   } else {
     // ---- softmax: one thread per row
@@ -231,11 +299,26 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
       // epilogue: O = T 2^c0 / l (global recovering, pasa.cpp:184-194)
       const int c0 = MODE == kModePasa && row_ok ? pasa_inflation(p.N, p.vmax[seq0 + sl]) : 0;
       const float inv_l = __fmul_rn(__frcp_rn(l), ldexpf(1.0f, c0));
+      mbar_wait(mask_full, it & 1);
+      const uint32_t bad = bad_mask[it & 1];
+      // a poisoned tile: this row's own sequence poisoned -> T, else T_clean (warp-uniform
+      // column choice per load: rows of a warp may sit in different slots)
+      const bool clean = bad != 0 && !((bad >> sl) & 1u);
       mbar_wait(t_full, it & 1);
       tc_fence_after();
       uint32_t tv[D / 2];
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) tmem_ld_32cols_pack16(t_s + 128 + 32 * c, tv + 16 * c);
+      if (__any_sync(0xffffffffu, clean)) {  // rare: 16 extra registers at a time
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t tc[16];
+          tmem_ld_32cols_pack16(t_s + Cfg::T_CLEAN + 32 * c, tc);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) tv[16 * c + i] = clean ? tc[i] : tv[16 * c + i];
+        }
+      }
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
@@ -257,7 +340,7 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 0) tmem_dealloc<256>(tmem_base);
+  if (warp == 0) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
 }
 
 template <int D, int MODE>
@@ -269,8 +352,7 @@ static cudaError_t launch_packed_t(const CUtensorMap& tq, const CUtensorMap& tk,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int tiles = (p.BH + p.P - 1) / p.P;  // p.P = 128 / p.W sequences per tile
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int sms = current_sm_count();  // the launching (current) device
   const int per_sm = D == 64 ? 2 : 1;  // shared memory: 2 x 98 KB (d = 64), 194 KB (d = 128)
   const int grid = tiles < per_sm * sms ? tiles : per_sm * sms;
   pasa_fwd_packed_kernel<D, MODE><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(tq, tk, tv, p);

@@ -90,9 +90,7 @@ __global__ void gen_resonance_kernel(ResonanceParams p, __half* __restrict__ out
 }
 
 int grid_for(uint64_t n) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = current_sm_count();
   const uint64_t want = (n + 255) / 256;
   const uint64_t cap = static_cast<uint64_t>(sms) * 16;  // grid-stride beyond 16 CTAs per SM
   return static_cast<int>(want < cap ? (want ? want : 1) : cap);

@@ -1,5 +1,8 @@
 // pasa_kernels.cuh -- shared parameter blocks for the PASA B200 kernels.
 #pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
 #include <cstdlib>
 #include <cstdint>
 
@@ -40,9 +43,11 @@ __host__ __device__ inline Strides3 layout_strides(int layout, int H, int S, int
 // S2 * max|V| <= 2^14 * 2^c0, computed identically on host and device.  The
 // pre-pass scales V by the exact power of two 2^-c0, so T = P V and the FP16 O
 // stay below 2^14 while P keeps its full (0, 1] range (no subnormal P).
+// A head whose V holds an infinity (vmax = inf) gets c0 = 0: its output is non-finite
+// whatever the scale, and V' = V keeps the other values intact.
 __host__ __device__ inline int pasa_inflation(int S2, float vmax) {
   const float need = static_cast<float>(S2) * vmax * (1.0f / 16384.0f);
-  if (!(need > 1.0f)) return 0;
+  if (!(need > 1.0f) || !(need < 3.0e38f)) return 0;
   const int e = ilogbf(need);  // floor(log2 need), exact
   return ldexpf(1.0f, e) == need ? e : e + 1;
 }
@@ -53,6 +58,22 @@ __host__ __device__ inline int pasa_inflation(int S2, float vmax) {
 inline bool pdl_enabled() {
   static const bool on = std::getenv("PASA_B200_NO_PDL") == nullptr;
   return on;
+}
+
+// SM count of the CURRENT device (grid sizing), cached per device ordinal.
+inline int current_sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return 148;
+  if (dev < 64) {
+    const int c = cache[dev].load(std::memory_order_relaxed);
+    if (c > 0) return c;
+  }
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+    return 148;
+  if (dev < 64) cache[dev].store(sms, std::memory_order_relaxed);
+  return sms;
 }
 
 // V' = V * 2^-c0 per (b, kv head), written by the pre-pass for the fused kernel.

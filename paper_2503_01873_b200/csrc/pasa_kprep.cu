@@ -377,8 +377,7 @@ cudaError_t launch_vscale(const VscaleParams& p, cudaStream_t stream) {
   const bool flat = p.per_head / 8 < 1024 && p.total / 8 < (1LL << 31);
   dim3 grid(static_cast<unsigned>(bh), static_cast<unsigned>(chunks < 65535 ? chunks : 65535));
   if (flat) {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int sms = current_sm_count();  // the launching (current) device
     const long long blocks = (p.total / 8 + 255) / 256;
     grid = dim3(static_cast<unsigned>(blocks < 16LL * sms ? blocks : 16LL * sms));
   }

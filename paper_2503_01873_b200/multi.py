@@ -39,24 +39,35 @@ def partition(batch: int, heads_kv: int, world: int) -> list[Shard]:
     return out
 
 
-def _unit_slices(q, k, v, unit: int):
+def _shard_views(q, k, v, start: int, stop: int):
+    """The shard's units [start, stop) as ONE problem: in BHSD the flat (b, kv head) units
+    are contiguous, so Q is a (1, (stop - start) * g, S1, d) view and K, V are
+    (1, stop - start, S2, d) views -- one launch per shard, whatever the unit count."""
     B, Hq, S1, d = q.shape
-    Hkv = k.shape[1]
+    Hkv, S2 = k.shape[1], k.shape[2]
     g = Hq // Hkv
-    b, h = divmod(unit, Hkv)
-    return (q[b:b + 1, h * g:(h + 1) * g], k[b:b + 1, h:h + 1], v[b:b + 1, h:h + 1])
+    n = stop - start
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    return (q.reshape(B * Hkv, g, S1, d)[start:stop].reshape(1, n * g, S1, d),
+            k.reshape(B * Hkv, 1, S2, d)[start:stop].reshape(1, n, S2, d),
+            v.reshape(B * Hkv, 1, S2, d)[start:stop].reshape(1, n, S2, d))
 
 
 def _default_compute(q, k, v, **kw):
     from .api import pasa_attention_fwd
-    return pasa_attention_fwd(q.contiguous(), k.contiguous(), v.contiguous(), **kw)
+    return pasa_attention_fwd(q, k, v, **kw)
 
 
 def shard_forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, shard: Shard,
                   compute: Callable | None = None, **kw) -> list[tuple[int, torch.Tensor]]:
-    """Run this rank's units; returns [(unit, O_unit)] with O_unit (1, Hq/Hkv, S1, d)."""
+    """Run this rank's units in one call; returns [(unit, O_unit)] with O_unit
+    (1, Hq/Hkv, S1, d), views of the shard's output."""
     compute = compute or _default_compute
-    return [(u, compute(*_unit_slices(q, k, v, u), **kw)) for u in shard.units()]
+    if shard.stop <= shard.start:
+        return []
+    g = q.shape[1] // k.shape[1]
+    o = compute(*_shard_views(q, k, v, shard.start, shard.stop), **kw)
+    return [(u, o[:, i * g:(i + 1) * g]) for i, u in enumerate(shard.units())]
 
 
 def pasa_attention_sharded(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,

@@ -239,17 +239,20 @@ def test_host_entry_point_matches_device(dev, orc):
     assert diag.out_total == o_host.numel() and diag.out_nonfinite == 0
 
 
-def test_reference_harness_on_b200(dev):
+@pytest.mark.parametrize("diagnose", [0, 1])
+def test_reference_harness_on_b200(dev, diagnose):
     """The reference's own sweep (bench.cpp:170-247) linked against the B200
     drop-in (integration/pasa_shim.cpp instead of pasa.o): PASA_FP16 cells run
-    on the GPU, FA_PARTIAL_FP16 on the reference CPU path, same CSV schema."""
+    on the GPU, FA_PARTIAL_FP16 on the reference CPU path, same CSV schema.  With
+    SweepOptions::diagnose the reference's range report (bench.cpp:108-168) calls
+    preprocess_keys under GoldenFp64, which the drop-in must keep serving."""
     import csv
     import io
     import subprocess
     exe = os.path.join(os.path.dirname(HERE), "integration", "_build", "ref_sweep_b200")
     if not os.path.exists(exe):
         pytest.skip("integration binary not built")
-    r = subprocess.run([exe, "2", "1280"], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([exe, "2", "1280", str(diagnose)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr
     rows = list(csv.DictReader(io.StringIO(r.stdout)))
     pasa_rows = [x for x in rows if x["policy"] == "PASA_FP16"]
@@ -261,6 +264,14 @@ def test_reference_harness_on_b200(dev):
         assert float(row["nan_pct"]) == 0.0
         assert float(row["rmse"]) <= 1.25 * rr + 1e-3, (row, rr)
     assert float(fa_rows[0]["nan_pct"]) == 100.0 and float(fa_rows[3]["nan_pct"]) == 100.0
+    cols = ("s_min_before", "s_max_before", "s_min_after", "s_max_after")
+    for row in pasa_rows + fa_rows:  # (a cell error would have failed the run: rc != 0)
+        if diagnose:  # FP64 score ranges before / after the shift: PASA narrows them
+            lo_b, hi_b, lo_a, hi_a = (float(row[c]) for c in cols)
+            assert all(math.isfinite(x) for x in (lo_b, hi_b, lo_a, hi_a)), row
+            assert max(abs(lo_a), abs(hi_a)) < max(abs(lo_b), abs(hi_b)), row
+        else:
+            assert all(row[c] == "" for c in cols), row
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
@@ -743,3 +754,63 @@ def test_pdl_off_bit_identical(dev, tmp_path):
     v = torch.randn(1, 2, 640, 128, generator=g).half().to(dev)
     o = pasa_attention_fwd(q, k, v, causal=True).cpu().view(torch.int16).numpy()
     assert np.array_equal(np.load(out), o)
+
+
+def _same_bits_nan_aware(a, b):
+    """Equal bit for bit where finite-or-inf; NaN exactly where the other is NaN."""
+    na, nb = torch.isnan(a), torch.isnan(b)
+    return torch.equal(na, nb) and torch.equal(a[~na].view(torch.int16), b[~nb].view(torch.int16))
+
+
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("mode", ["pasa", "fa16"])
+def test_packed_nonfinite_v_stays_in_its_sequence(dev, D, mode):
+    """in the packed short-sequence kernel a tile's P V' multiplies each row's
+    zero P entries by the other sequences' V' rows; an Inf/NaN in one sequence's V must
+    not reach its neighbours (0 x Inf = NaN).  B*H = 2498 sequences of N = 25 (4 per tile,
+    625 tiles, ragged last tile) so persistent CTAs reuse each shared-memory stage and the
+    ragged last tile sees a stage whose previous tile was poisoned."""
+    from paper_2503_01873_b200 import flash_fp16_fwd, pasa_attention_fwd
+    B, H, N = 1, 2498, 25
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    q, k, v = (torch.randn(B, H, N, D, device=dev, generator=g).half() for _ in range(3))
+    run = (lambda q_, k_, v_: pasa_attention_fwd(q_, k_, v_, causal=False, s1=N, s2=N)) \
+        if mode == "pasa" else (lambda q_, k_, v_: flash_fp16_fwd(q_, k_, v_, s1=N, s2=N))
+    clean = run(q, k, v)
+    vp = v.clone()
+    # seq 2 (+inf), 6 (nan, another tile), 131 = tile 32 slot 3 (-inf; tile 32's CTA later
+    # runs the ragged last tile 624 on the same stage, whose slot 3 is then stale)
+    poisoned = {2: float("inf"), 6: float("nan"), 131: float("-inf"), 2497: float("nan")}
+    for sq, val in poisoned.items():
+        vp[0, sq, 7, 3] = val
+    got = run(q, k, vp)
+    torch.cuda.synchronize()
+    keep = torch.ones(H, dtype=torch.bool, device=dev)
+    keep[list(poisoned)] = False
+    assert torch.equal(got[0, keep].view(torch.int16), clean[0, keep].view(torch.int16))
+    for sq in poisoned:  # a poisoned sequence gets exactly what it gets alone
+        alone = run(q[:, sq:sq + 1], k[:, sq:sq + 1], vp[:, sq:sq + 1])
+        assert _same_bits_nan_aware(got[:, sq:sq + 1], alone), sq
+        assert not torch.isfinite(got[:, sq]).all()
+
+
+def test_two_streams_own_workspaces(dev):
+    """calls on different streams must not share a K'/V' workspace, and a
+    launch on a side stream is ordered after the inputs' producer on the current stream."""
+    from paper_2503_01873_b200 import pasa_attention_fwd
+    g = torch.Generator(device=dev)
+    g.manual_seed(9)
+    shapes = [(1, 4, 2048, 128), (1, 4, 4096, 128)]
+    ins = [tuple(torch.randn(*sh, device=dev, generator=g).half() for _ in range(3)) for sh in shapes]
+    want = [pasa_attention_fwd(*x, causal=True) for x in ins]
+    torch.cuda.synchronize()
+    s_a, s_b = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    for _ in range(3):
+        outs = []
+        for x, s in zip(ins, (s_a, s_b)):
+            xs = tuple(t * 1 for t in x)  # produced on the current stream just before
+            outs.append(pasa_attention_fwd(*xs, causal=True, stream=s))
+        torch.cuda.synchronize()
+        for o, w in zip(outs, want):
+            assert torch.equal(o.view(torch.int16), w.view(torch.int16))

@@ -59,3 +59,26 @@ def test_sharded_equals_single_process(tmp_path, orc):
     mp.spawn(_worker, args=(2, _free_port(), q, k, v, out), nprocs=2, join=True)
     sharded = torch.load(out)
     assert torch.equal(sharded, single)
+
+
+def test_shard_forward_one_call_per_shard():
+    """a shard is ONE compute call over its contiguous (b, kv head) units (views,
+    no per-unit launches), and the per-unit outputs it returns are that call's slices."""
+    from paper_2503_01873_b200.multi import Shard, shard_forward
+    B, Hq, Hkv, S, d = 2, 6, 3, 8, 4
+    q = torch.arange(B * Hq * S * d, dtype=torch.float32).reshape(B, Hq, S, d)
+    k = -torch.arange(B * Hkv * S * d, dtype=torch.float32).reshape(B, Hkv, S, d)
+    v = k * 2
+    calls = []
+
+    def compute(qs, ks, vs, **kw):
+        calls.append((qs.shape, ks.shape, vs.shape, kw))
+        return qs * 10  # stand-in: any per-row function of the shard's Q
+    out = shard_forward(q, k, v, Shard(0, 1, 5), compute=compute, causal=True)
+    assert len(calls) == 1
+    assert calls[0][0] == (1, 8, S, d) and calls[0][1] == (1, 4, S, d) and calls[0][3] == {"causal": True}
+    assert [u for u, _ in out] == [1, 2, 3, 4]
+    for u, o in out:
+        b, h = divmod(u, Hkv)
+        assert torch.equal(o, q[b:b + 1, 2 * h:2 * h + 2] * 10)
+    assert shard_forward(q, k, v, Shard(1, 3, 3), compute=compute) == [] and len(calls) == 1

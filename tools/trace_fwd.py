@@ -30,10 +30,12 @@ def main():
     ap.add_argument("--hkv", type=int, default=4)
     ap.add_argument("--causal", type=int, default=1)
     ap.add_argument("--d", type=int, default=128)
+    ap.add_argument("--lib", default="libpasa_b200_trace.so",
+                    help="trace build in paper_2503_01873_b200/_build (tools/build_variant.py NAME -DPASA_TRACE ...)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "trace.json"))
     a = ap.parse_args()
     from paper_2503_01873_b200 import _lib
-    lib = _lib.load(os.path.join(ROOT, "paper_2503_01873_b200", "_build", "libpasa_b200_trace.so"))
+    lib = _lib.load(os.path.join(ROOT, "paper_2503_01873_b200", "_build", a.lib))
     lib.pasa_b200_debug_set_trace.argtypes = [C.c_void_p]
     dev = torch.device("cuda:0")
     S, D = a.seq, a.d
@@ -43,7 +45,7 @@ def main():
     o = torch.empty_like(q)
     desc = _lib.Desc(1, a.hq, a.hkv, S, S, D, 128, 128, a.causal, 0, 0.984497, math.sqrt(D))
     ws = torch.empty(lib.pasa_b200_workspace_size(C.byref(desc)), dtype=torch.uint8, device=dev)
-    tr = torch.zeros(CTAS * ROLES * ITERS * EVENTS, dtype=torch.int64, device=dev)
+    tr = torch.zeros(CTAS * ROLES * ITERS * EVENTS + 512 * 8, dtype=torch.int64, device=dev)  # + the PASA_STATE row-state area
     st = torch.cuda.current_stream().cuda_stream
     for it in range(3):
         lib.pasa_b200_debug_set_trace(tr.data_ptr() if it == 2 else None)
@@ -51,14 +53,15 @@ def main():
                                                v.data_ptr(), o.data_ptr(), ws.data_ptr(),
                                                ws.numel(), None, st))
     torch.cuda.synchronize()
-    t = tr.cpu().numpy().reshape(CTAS, ROLES, ITERS, EVENTS).astype(np.int64)
+    n = CTAS * ROLES * ITERS * EVENTS
+    t = tr[:n].cpu().numpy().reshape(CTAS, ROLES, ITERS, EVENTS).astype(np.int64)
     res = {}
     for c in range(CTAS):
         base = t[c][t[c] > 0].min() if (t[c] > 0).any() else 0
         rel = np.where(t[c] > 0, t[c] - base, -1)
         res[c] = rel.tolist()
         print(f"=== CTA y={c}")
-        print(" j | WG0: waitS  ldS p1+sc ppwait exp  stP  waitT  ldT  O   | WG1: waitS  ldS p1+sc ppwait exp  stP  waitT  ldT  O | period0 period1")
+        print(" j | WG0: waitS  ldS p1+sc ppwait exp  stP  waitT  ldT  O   | WG1: waitS  ldS p1+sc ppwait exp  stP  waitT  ldT  O | period0 period1 | part0: WG0 WG1")
         for j in range(1, ITERS - 1):
             row = []
             for w in range(2):
@@ -71,7 +74,8 @@ def main():
                                                          e[8] - e[3], e[7] - e[8], e[4] - e[7], e[5] - e[4],
                                                          e[6] - e[5], (nxt - e[6]) if nxt > 0 else -1]))
             per = [rel[w, j + 1][0] - rel[w, j][0] if rel[w, j + 1][0] > 0 else -1 for w in range(2)]
-            print(f"{j:2d} | {row[0]} | {row[1]} | {per[0]:6d} {per[1]:6d}")
+            p0 = [rel[w, j][9] - rel[w, j][8] if rel[w, j][9] > 0 else -1 for w in range(2)]
+            print(f"{j:2d} | {row[0]} | {row[1]} | {per[0]:6d} {per[1]:6d} | {p0[0]:5d} {p0[1]:5d}")
         m = rel[2]
         print(" MMA: j | t0: waitP issuePV issueS | t1: waitP issuePV issueS")
         for j in range(1, 12):

@@ -71,8 +71,9 @@ def main():
         for _ in range(a.rounds):
             for so, L, x in zip(a.libs, libs, args):
                 ts[so].append(time_once(L, x))
-        for so in a.libs:
-            res[so].append(f"{name} {fl / statistics.median(ts[so]) / 1e9:7.1f}")
+        for so, x in zip(a.libs, args):
+            same = torch.equal(x[5].view(torch.int16), args[0][5].view(torch.int16))
+            res[so].append(f"{name} {fl / statistics.median(ts[so]) / 1e9:7.1f}{'' if same else '(DIFF)'}")
         del args
         torch.cuda.empty_cache()
     for so in a.libs:
