@@ -61,7 +61,7 @@ class ModelParams(C.Structure):
     _fields_ = [
         ("beta", C.c_double), ("diag", C.c_double), ("off", C.c_double),
         ("lscale", C.c_double), ("tc_mode", C.c_int), ("c0", C.c_double),
-        ("xscale", C.c_double),
+        ("xscale", C.c_double), ("rowsum", C.c_int),
     ]
 
 
@@ -233,15 +233,20 @@ class Oracle:
 
     def model_pasa(self, pb: Problem, beta: float = BETA_STAR, lscale: float = LOG2E / 2,
                    tc_mode: int = 1, c0: float = -1.0, threads: int = 0,
-                   xscale: float | None = None) -> np.ndarray:
+                   xscale: float | None = None, rowsum: int | None = None) -> np.ndarray:
         """The kernel's numerics: scores stored in units of lscale
         (log2(e)/2 on the device), exp argument xscale*fl16(S' - c_j) with
-        xscale = log2(e)/lscale rounded to the power of two (2 by default)."""
+        xscale = log2(e)/lscale rounded to the power of two (2 by default).
+        ``rowsum``: the pseudo-average's row sum -- 1: tensor core, q.hi and q.lo added in
+        FP32 (the kernel at d = 64); 2: one FP32 accumulator over [q|q].[hi|lo] (d = 128);
+        0: the CUDA-core FP32 chains (d = 128 default build); None: the kernel's choice."""
         d = pb.q.shape[-1]
+        if rowsum is None:  # d = 64: per-block tensor-core sums; d = 128: CUDA cores
+            rowsum = 1 if 128 + d + 16 <= 256 else 0
         diag, off = self.shift_entries(pb.s2, beta, float(np.sqrt(d)), P16)
         if xscale is None:
             xscale = 2.0 if lscale == LOG2E / 2 else 1.0
-        mp = ModelParams(beta, diag, off, lscale, tc_mode, c0, xscale)
+        mp = ModelParams(beta, diag, off, lscale, tc_mode, c0, xscale, rowsum)
         o = np.empty(pb.q.shape)
         sh = pb.shape()
         rc = self.lib.orc_model_pasa(C.byref(sh), _f64(pb.q), _f64(pb.k), _f64(pb.v), o,

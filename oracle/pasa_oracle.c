@@ -586,6 +586,11 @@ typedef struct {
                     xscale*fl16(S' - c_j) (the kernel: lscale = log2(e)/2,
                     xscale = 2, so the FP16 S' store holds 1/ln 2 / 2 = 0.72 x the
                     reference's scores and overflows later than the reference) */
+  int rowsum;    /* the pseudo-average's row sum: 1 = tensor core, q . hi and q . lo (the
+                    K' block sums split into FP16 hi + lo) in two FP32 accumulators, then
+                    added (the kernel at d = 64, per block); 2 = one FP32 accumulator over
+                    [q | q] . [hi | lo] (d = 128, the prologue GEMM); 0 = the CUDA-core
+                    FP32 chains over the stored FP16 scores (PASA_PRO_SUM=0 builds) */
 } orc_model_params;
 
 /* The kernel's O-bounding exponent (pasa_kernels.cuh: pasa_inflation): the
@@ -638,7 +643,7 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
     float* fbar = calloc(s1, sizeof(float));
     double* oacc = calloc(s1 * d, sizeof(double));
     double* S = malloc(sizeof(double) * s2);
-    const int tcsum = (128 + d + 16 <= 256); /* the kernel's pasa_tc_rowsum(d) */
+    const int tcsum = mp->rowsum != 0;
     double* ksh = malloc(sizeof(double) * d); /* K' block sums, hi / lo parts */
     double* ksl = malloc(sizeof(double) * d);
     size_t jc = 0; /* consumed blocks */
@@ -664,8 +669,8 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
         const double* qr = row_ptr(q, sh->Hq, sh->S1, d, b, h, i * s1 + r);
         const size_t pos = row0 + r;
         for (size_t c = 0; c < s2; ++c) S[c] = tc_dot(qr, 1, kpj + c * d, 1, d, mp->tc_mode);
-        /* Pseudo-average.  D <= 112 (pasa_tc_rowsum): from the tensor core,
-         * sum_c S'_c = q . ksum_j with the
+        /* Pseudo-average.  From the tensor core (rowsum = 1; per block at d = 64, from
+         * the prologue GEMM at d = 128): sum_c S'_c = q . ksum_j with the
          * block's K' column sums split as (hi, lo) FP16 (the K'-sum kernel), each
          * product exact, accumulated to FP32 (modelled as FP64 then one rounding),
          * columns hi and lo added in FP32. */
@@ -676,9 +681,10 @@ ORC_API int orc_model_pasa(const orc_shape* sh, const double* q,
             ghi += qr[t] * ksh[t];
             glo += qr[t] * ksl[t];
           }
-          ssum = (float)ghi + (float)glo;
+          ssum = mp->rowsum == 2 ? (float)(ghi + glo) /* one FP32 accumulator over K = 2 d */
+                                 : (float)ghi + (float)glo;
         } else {
-          /* D = 128 (no free TMEM columns): two threads per row (tile columns [0, 64)
+          /* rowsum = 0 (CUDA cores): two threads per row (tile columns [0, 64)
            * and [64, 128)); in each half eight FP32 chains: column c -> chain
            * 2*((c/2)%4) + c%2 (the kernel's pair-register order), combined
            * ((t0+t1)+(t2+t3)), t_r = a_2r + a_2r+1; the row total is half0 + half1. */

@@ -64,6 +64,37 @@ static cudaMemPool_t scratch_pool() {
 
 namespace {
 
+__global__ void nsmid_kernel(int* out) {
+  uint32_t n;
+  asm volatile("mov.u32 %0, %%nsmid;" : "=r"(n));
+  *out = static_cast<int>(n);
+}
+
+// %nsmid of the current device (SM ids are < it; they need not be contiguous), queried once
+// per device on a private stream; falls back to twice the SM count.
+int device_nsmid() {
+  static std::mutex mu;
+  static int cache[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 2 * current_sm_count();
+  std::lock_guard<std::mutex> lock(mu);
+  if (cache[dev] > 0) return cache[dev];
+  int n = 0;
+  int* d = nullptr;
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
+      cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(int), st) == cudaSuccess) {
+    nsmid_kernel<<<1, 1, 0, st>>>(d);
+    if (cudaMemcpyAsync(&n, d, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess) n = 0;
+    cudaFreeAsync(d, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) n = 0;
+  }
+  if (st) cudaStreamDestroy(st);
+  cudaGetLastError();
+  cache[dev] = n > 0 ? n : 2 * current_sm_count();
+  return cache[dev];
+}
+
 thread_local std::string g_last_error;
 long long* g_trace = nullptr;  // PASA_TRACE builds: clock64 timeline buffer
 
@@ -114,6 +145,24 @@ int make_tmap(CUtensorMap* m, const void* base, int d, int seq, int bh, int rows
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(PASA_B200_ECUDA, "cuTensorMapEncodeTiled failed");
+  return PASA_B200_OK;
+}
+
+// 4-D view {d, 2, nblk, bh} of the K'-sum buffer [bh][nblk][hi, lo][d] (pasa_ksum_kernel):
+// box {64, 1, rows, 1} -- the hi (or lo) rows of `rows` consecutive blocks, 128B swizzle.
+int make_tmap_ks4(CUtensorMap* m, const void* base, int d, int nblk, int bh, int rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return fail(PASA_B200_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t row = static_cast<cuuint64_t>(d) * 2;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(d), 2, static_cast<cuuint64_t>(nblk),
+                        static_cast<cuuint64_t>(bh)};
+  cuuint64_t strides[3] = {row, 2 * row, 2 * row * static_cast<cuuint64_t>(nblk)};
+  cuuint32_t box[4] = {64, 1, static_cast<cuuint32_t>(rows), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PASA_B200_ECUDA, "cuTensorMapEncodeTiled (K' sums) failed");
   return PASA_B200_OK;
 }
 
@@ -393,23 +442,41 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
   // PASA at D = 64: the S' row sums come from the tensor core (pseudo-average GEMM
   // against the block sums of K', pasa_tc_rowsum); the sums are a stream-ordered scratch
   // of B Hkv (S2 / s2) 2 D halves (1.6 % of K' at s2 = 128) from the library's pool.
+  //
+  // PASA at D = 128: the same K' block sums feed the fused kernel's prologue GEMM (256-row
+  // boxes, 128 blocks per chunk); its per-row results go to an L2-resident scratch of one
+  // slot per SM id (%nsmid x 2 tiles x blocks x 128 rows FP32), also from the pool.
   CUtensorMap tks = tk;
   void* ks = nullptr;
+  void* gs = nullptr;
   cudaError_t e = cudaSuccess;
-  if (mode == kModePasa && pasa_tc_rowsum(d->head_dim)) {
+  if (mode == kModePasa && (pasa_tc_rowsum(d->head_dim) || pasa_prologue_rowsum(d->head_dim))) {
     const int bh = d->batch * d->heads_kv, nblk = d->seq_kv / d->s2;
+    const bool pro = pasa_prologue_rowsum(d->head_dim);
     cudaMemPool_t pool = scratch_pool();
     if (!pool) return fail(PASA_B200_ECUDA, "cudaMemPoolCreate failed");
     e = cudaMallocFromPoolAsync(&ks, static_cast<size_t>(bh) * nblk * 2 * d->head_dim * 2, pool, st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMallocFromPoolAsync");
-    if ((rc = make_tmap(&tks, ks, d->head_dim, 2 * nblk, bh, 2))) {
+    p.ks_rows = pro ? (nblk < 128 ? nblk : 128) : 2;
+    if ((rc = pro ? make_tmap_ks4(&tks, ks, d->head_dim, nblk, bh, p.ks_rows)
+                  : make_tmap(&tks, ks, d->head_dim, 2 * nblk, bh, p.ks_rows))) {
       cudaFreeAsync(ks, st);
       return rc;
+    }
+    if (pro) {
+      p.gslots = device_nsmid();
+      e = cudaMallocFromPoolAsync(&gs, static_cast<size_t>(p.gslots) * 2 * nblk * kTile * 4, pool, st);
+      if (e != cudaSuccess) {
+        cudaFreeAsync(ks, st);
+        return cuda_fail(e, "cudaMallocFromPoolAsync");
+      }
+      p.gsum = static_cast<float*>(gs);
     }
     e = launch_ksum(keys, ks, bh, d->seq_kv, d->s2, d->head_dim, st);
   }
   if (e == cudaSuccess) e = launch_fwd(d->head_dim, d->causal != 0, mode, tq, tk, tv, tks, p, st);
   if (ks) cudaFreeAsync(ks, st);
+  if (gs) cudaFreeAsync(gs, st);
   if (e != cudaSuccess) return cuda_fail(e, "pasa_fwd launch");
   return PASA_B200_OK;
 }

@@ -120,6 +120,17 @@ static_assert(128 * PASA_WG0_REGS + 512 * PASA_SM_REGS <= 61440, "register pool"
   } while (0)
 #endif
 
+// d = 128 (no free TMEM columns in the loop): the pseudo-average from the tensor core in a
+// PROLOGUE -- G_t[r][j] = q_r . (K'sum_j hi + K'sum_j lo) as ONE GEMM over K = 2 D,
+// A = [Q_t | Q_t], B row j = [hi_j | lo_j], FP32 accumulator, up to 128 blocks per GEMM
+// (N <= 128) in tile t's T columns, so S'(0) runs beside it in the S' columns -- read out
+// to an L2-resident scratch slot of this SM and read back one float per row and block,
+// instead of 64 FP32 adds per thread and block in pass 1.  Off by default (PASA_PRO_SUM in
+// pasa_kernels.cuh): the exact mean cuts the RMSE by a quarter (uniform(30, 0.5) at Qwen 16K:
+// 1.07e-3 -> 7.9e-4), but the prologue's 128 KB of scratch stores per CTA cost 2-5 % of
+// throughput, and the pass-1 adds it removes are not what sets the block period.
+constexpr int kGChunk = 128;  // blocks per prologue GEMM (N = 128 FP32 columns = a T region)
+
 // K'/V' pipeline stages at d = 64 (d = 128 fills shared memory at two); 3 or 4 at d = 64
 // measured 1.5 % slower than 2 (tools/variants.py): the loads are not what the tiles wait on
 #ifndef PASA_STAGES_D64
@@ -142,7 +153,7 @@ struct FwdCfg {
   static constexpr int KS_BOX = 2048;
   static constexpr int SMEM_KS = SMEM_V + VS * TILE_BYTES;
   static constexpr int SMEM_BAR = SMEM_KS + (TCSUM ? KS * NBOX * KS_BOX : 0);
-  static constexpr int NUM_BARS = NT + 2 * KS + 2 * VS + (3 + kPParts<D>) * NT;
+  static constexpr int NUM_BARS = NT + 2 * KS + 2 * VS + (3 + kPParts<D>) * NT + 3 + NT;
   static constexpr int HALVES = 2;  // threads per row: each owns 64 S' columns, D/2 outputs
   static constexpr int SMEM_XCH = SMEM_BAR + NUM_BARS * 8 + 16;  // row max/sum exchange
   static constexpr int XCH_BYTES = 2 * NT * HALVES * kTile * 8;  // [j&1][t][half][row] float2
@@ -323,6 +334,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
                     const __grid_constant__ CUtensorMap tm_v,
                     const __grid_constant__ CUtensorMap tm_ks, const FwdParams p) {
   constexpr bool kTcSum = FwdCfg<D>::TCSUM && MODE == kModePasa;
+  constexpr bool kProSum = pasa_prologue_rowsum(D) && MODE == kModePasa;
   // MMA issue: one warp for both tiles (PV of the first-ready tile, then its S'(j+1);
   // best at D = 128, where an S' MMA queued ahead of the other tile's PV stalls it) or,
   // at D = 64, one warp per tile (+5 %, tools/variants.py).
@@ -343,6 +355,9 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
   const uint32_t t_full = s_full + 8 * NT;
   const uint32_t t_empty = t_full + 8 * NT;
   const uint32_t p_part = t_empty + 8 * NT;  // [q][t]: P of part q stored (pass 2 in kPParts parts)
+  // prologue pseudo-average (kProSum): K'-sum chunk loaded / consumed, G in TMEM / read out
+  const uint32_t ks_full = p_part + 8 * kPParts<D> * NT;
+  const uint32_t ks_empty = ks_full + 8, g_free = ks_full + 16, g_full = ks_full + 24;  // g_full[t]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Cfg::SMEM_BAR + 8 * Cfg::NUM_BARS);
 
   const int warp = static_cast<int>(warp_id());
@@ -360,6 +375,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
   int nmax = 0;
 #pragma unroll
   for (int t = 0; t < NT; ++t) nmax = max(nmax, tl[t].nblk);
+  const int nch = kProSum ? (nmax + kGChunk - 1) / kGChunk : 0;  // prologue G chunks
 
   if (threadIdx.x == 0) {
     for (int t = 0; t < NT; ++t) {
@@ -377,6 +393,10 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       mbar_init(v_full + 8 * (s), 1);
       mbar_init(v_empty + 8 * (s), kSplitIssue ? NT : 1);
     }
+    mbar_init(ks_full, 1);
+    mbar_init(ks_empty, 1);
+    for (int t = 0; t < NT; ++t) mbar_init(g_full + 8 * t, 1);
+    mbar_init(g_free, 4 * Cfg::HALVES * NT);  // every softmax warp, every chunk
     fence_barrier_init();
   }
   if (kTcSum) {  // rows 2-15 of the K'-sum boxes read as zero (TMA writes rows 0-1)
@@ -416,7 +436,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       tma_prefetch(&tm_q);
       tma_prefetch(&tm_kp);
       tma_prefetch(&tm_v);
-      if (kTcSum) tma_prefetch(&tm_ks);
+      if (kTcSum || kProSum) tma_prefetch(&tm_ks);
       for (int t = 0; t < NT; ++t) {
         if (!tl[t].valid) continue;
         mbar_expect_tx(q_full + 8 * (t), Cfg::TILE_BYTES);
@@ -425,6 +445,17 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
           tma_load_3d(sb + Cfg::SMEM_Q + t * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_q,
                       q_full + 8 * (t), (p.q_bshd ? tl[t].hq * D : 0) + bx * 64, tl[t].i * kTile,
                       p.q_bshd ? b : b * p.Hq + tl[t].hq);
+      }
+      // Prologue (kProSum): the head's K' block sums, 128 blocks at a time, into the V'
+      // stages (free until the first V' load): box (hl, bx) = the hi (hl = 0) or lo rows,
+      // columns [64 bx, 64 bx + 64), 128 blocks x 128 B (SW128, K-major like K').
+      for (int c = 0; c < nch; ++c) {
+        mbar_wait(ks_empty, (c & 1) ^ 1);
+        mbar_expect_tx(ks_full, 2 * Cfg::NBOX * 128 * p.ks_rows);  // whole boxes (OOB rows = 0)
+        for (int hl = 0; hl < 2; ++hl)
+          for (int bx = 0; bx < Cfg::NBOX; ++bx)
+            tma_load_4d(sb + Cfg::SMEM_V + (hl * Cfg::NBOX + bx) * Cfg::BOX_BYTES, &tm_ks, ks_full,
+                        bx * 64, hl, c * kGChunk, b * p.Hkv + hkv);
       }
       for (int j = 0; j < nmax; ++j) {
         const int ks = j % KS, vs = j % VS;
@@ -438,6 +469,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
             tma_load_3d(sb + Cfg::SMEM_KS + (ks * Cfg::NBOX + bx) * Cfg::KS_BOX, &tm_ks,
                         k_full + 8 * (ks), bx * 64, 2 * j, b * p.Hkv + hkv);
         }
+        if (kProSum && j == 0 && nch > 0) mbar_wait(ks_empty, (nch - 1) & 1);  // V area free
         mbar_wait(v_empty + 8 * (vs), ((j / VS) & 1) ^ 1);
         mbar_expect_tx(v_full + 8 * (vs), Cfg::NBOX * 128 * p.s2);
         for (int bx = 0; bx < Cfg::NBOX; ++bx)
@@ -585,6 +617,31 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       };
       for (int t = 0; t < NT; ++t)
         if (tl[t].valid) mbar_wait(q_full + 8 * (t), 0);
+      // Prologue (kProSum): G_t = [Q_t | Q_t] [hi | lo]^T (K = 2 D) for 128 blocks at a
+      // time into tile t's T columns [256 t + 128, 256 t + 128 + nb) (FP32), read out by the
+      // softmax warps (g_free); S'(0) is issued after the last chunk's GEMMs, into the S'
+      // columns, and runs while the last chunk is read out.
+      for (int c = 0; c < nch; ++c) {
+        mbar_wait(ks_full, c & 1);
+        if (c > 0) mbar_wait(g_free, (c - 1) & 1);
+        tc_fence_after();
+        for (int t = 0; t < NT; ++t) {
+          const int nb = min(kGChunk, tl[t].nblk - c * kGChunk);
+          if (nb <= 0) continue;
+          const uint32_t idg = idesc_f16(128, 16 * ((nb + 15) / 16), 1, 0, 0);
+          const uint32_t qa = sb + Cfg::SMEM_Q + t * Cfg::TILE_BYTES;
+#pragma unroll
+          for (int s = 0; s < 2 * D / 16; ++s)
+            umma_ss(tmem_base + t * Cfg::TMEM_TILE + 128,
+                    smem_desc_sw128(qa + ((s % (D / 16)) / 4) * Cfg::BOX_BYTES + (s % 4) * 32, 16, 1024),
+                    smem_desc_sw128(sb + Cfg::SMEM_V + (s / 4) * Cfg::BOX_BYTES + (s % 4) * 32, 16, 1024),
+                    idg, s > 0);
+          tc_commit(g_full + 8 * t);  // tile t's softmax reads out while tile t + 1's GEMM runs
+        }
+        for (int t = 0; t < NT; ++t)  // a tile without blocks in this chunk: nothing to wait for
+          if (min(kGChunk, tl[t].nblk - c * kGChunk) <= 0) mbar_arrive(g_full + 8 * t);
+        tc_commit(ks_empty);
+      }
       if (nmax > 0) {
         mbar_wait(k_full + 8 * (0), 0);
         tc_fence_after();
@@ -598,6 +655,10 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       for (int j = 0; j < nmax; ++j) {
         const int vs = j % VS;
         mbar_wait(v_full + 8 * (vs), (j / VS) & 1);
+        if (j == 0 && nch > 0) {  // PV(0) overwrites the last chunk's G columns
+          mbar_wait(g_free, (nch - 1) & 1);
+          tc_fence_after();
+        }
         bool k_next = false;
         // Serve the tile whose first P part is ready first (no head-of-line blocking
         // when the two tiles' exp passes overlap).
@@ -671,6 +732,52 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       dslot[1] = __int_as_float(0xff800000);  // -inf
       dslot[2] = dslot[3] = dslot[4] = 0.f;
     }
+    // kProSum: this row's S' sums, G[j] at grow[128 j] in this SM's scratch slot (written
+    // below from the prologue GEMM, read back one block ahead of use)
+    const float* grow = nullptr;
+    float gnext = 0.f;
+#ifdef PASA_TRACE
+    const long long tp0 = clock64();
+    long long tp1 = tp0;
+#endif
+    if (kProSum) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      if (smid >= static_cast<uint32_t>(p.gslots)) asm volatile("trap;");
+      float* gw = p.gsum + (static_cast<size_t>(smid * NT + t) * p.nkv) * kTile + row;
+      for (int c = 0; c < nch; ++c) {
+        mbar_wait(g_full + 8 * t, c & 1);
+#ifdef PASA_TRACE
+        if (c == 0) tp1 = clock64();
+#endif
+        tc_fence_after();
+        const int nb = min(kGChunk, ti.nblk - c * kGChunk);  // tile-uniform
+#pragma unroll
+        for (int q2 = 0; q2 < 2; ++q2) {
+          const int jb = 64 * h + 32 * q2;  // this half's 64 blocks, 32 at a time
+          if (jb >= nb) break;
+          uint32_t g[32];
+          tmem_ld_32cols_b32(t_s + 128 + jb, g);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (jb + i < nb) gw[static_cast<size_t>(c * kGChunk + jb + i) * kTile] = __uint_as_float(g[i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(g_free);
+      }
+      named_bar_sync(xbar, 64);  // the row's other half wrote the other blocks' sums
+      grow = gw;
+      if (ti.nblk > 0) gnext = grow[0];
+    }
+#ifdef PASA_TRACE  // prologue: kernel start -> G ready -> G stored (CTA x = 0, y < kTraceCtas)
+    if (p.trace && blockIdx.x == 0 && blockIdx.y < kTraceCtas && h == 0 && quad == 0 && lane == 0) {
+      float* st = reinterpret_cast<float*>(p.trace + kTraceStateOffset) + kStateIters * 8;
+      st[(blockIdx.y * NT + t) * 2] = static_cast<float>(tp1 - tp0);
+      st[(blockIdx.y * NT + t) * 2 + 1] = static_cast<float>(clock64() - tp1);
+    }
+#endif
     if (ti.nblk > 0) {
       // O-bounding exponent: V arrives pre-scaled by 2^-c0; the
       // epilogue multiplies by 2^c0.
@@ -682,11 +789,14 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       uint32_t s[NP];
       float m_run = 0.f, l_run = 0.f, fbar = 0.f;
       float rcp_j = 1.0f;  // 1/(j+1), computed off the critical path
+
       // both tiles' block counts (identical in every thread of the CTA)
       const int nmin = min(tile_info(p, hkv, unit * NT, CAUSAL).nblk,
                            tile_info(p, hkv, unit * NT + 1, CAUSAL).nblk);
       const bool pingpong = kPingPong<D>;
       for (int j = 0; j < ti.nblk; ++j) {
+        const float gcur = gnext;  // kProSum: sum_c S'_c of block j
+        if (kProSum && j + 1 < ti.nblk) gnext = grow[static_cast<size_t>(j + 1) * kTile];
         const bool tr = h == 0 && quad == 0 && lane == 0;
         if (tr) PASA_TR(t, j, 0);
         mbar_wait(s_full + 8 * (t), j & 1);
@@ -707,7 +817,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         const bool diag = cdiag || short_blk;
         const int lim = cdiag ? (short_blk ? min(vis0 + row, p.s2) : vis0 + row) : p.s2;
         if (DIAGNOSE) track_store_block<NP>(s, lim, NP * h, diag, dslot);
-        constexpr bool kSum = MODE == kModePasa && !kTcSum;
+        constexpr bool kSum = MODE == kModePasa && !kTcSum && !kProSum;
         float mh, sh = 0.f;
         if (diag) row_max_sum<true, NP, kSum>(s, lim, NP * h, mh, sh);
         else row_max_sum<false, NP, kSum>(s, lim, NP * h, mh, sh);
@@ -721,8 +831,9 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
         bool fast2 = true;  // PASA: the exp argument is one HFMA2 (see below)
         if (MODE == kModePasa) {
           // sum_c S'_c (pasa.cpp:131): the two halves' FP32 sums, or G's hi + lo columns
-          const float ssum = kTcSum ? __fadd_rn(__uint_as_float(g[0]), __uint_as_float(g[1]))
-                                    : (h == 0 ? __fadd_rn(sh, other.y) : __fadd_rn(other.y, sh));
+          const float ssum = kTcSum    ? __fadd_rn(__uint_as_float(g[0]), __uint_as_float(g[1]))
+                             : kProSum ? gcur
+                                       : (h == 0 ? __fadd_rn(sh, other.y) : __fadd_rn(other.y, sh));
           const float sbar = __fmul_rn(ssum, p.inv_s2);
           fnew = (jc == 1) ? sbar : __fadd_rn(fbar, __fmul_rn(__fsub_rn(sbar, fbar), rcp_j));
           const float dmc = __fmul_rn(p.inva, __fsub_rn(sbar, fnew));

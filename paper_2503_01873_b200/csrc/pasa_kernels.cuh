@@ -117,7 +117,21 @@ struct FwdParams {
   void* diag;             // optional device pasa_b200_diag (RunDiagnostics); nullptr = off
   float diag_scale;       // stored score -> reference units (PASA: 2/log2(e); FA16: 1)
   long long* trace;       // PASA_TRACE builds only: clock64 timeline (see pasa_fwd.cu)
+  float* gsum;            // D = 128 PASA: per-SM scratch of the prologue's S' row sums,
+                          // [smid][tile][block][row] FP32 (gslots x 2 x nkv x 128)
+  int gslots;             // SM-id slots in gsum (>= %nsmid of the device)
+  int ks_rows;            // rows of the K'-sum TMA box (d = 64: 2 = hi, lo of one block;
+                          // d = 128: blocks per prologue chunk, min(nkv, 128), per hi/lo box)
 };
+// D = 128 PASA, PASA_PRO_SUM=1 builds: the prologue pseudo-average (pasa_fwd.cu, kProSum);
+// D = 64 uses the per-block tensor-core row sum (pasa_tc_rowsum).  Both need the K' block
+// sums (pasa_ksum_kernel).  Defined here so the launcher and the kernel always agree.
+#ifndef PASA_PRO_SUM
+#define PASA_PRO_SUM 0
+#endif
+__host__ __device__ constexpr bool pasa_prologue_rowsum(int D) {
+  return PASA_PRO_SUM != 0 && !pasa_tc_rowsum(D);
+}
 
 // Packed short-sequence forward (pasa_fwd_packed.cu): B*H sequences of N <= 64 rows, each
 // a single KV block (S1 = S2 = s2 = N), in 16-aligned slots of W = 16 ceil(N/16) rows,

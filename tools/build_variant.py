@@ -31,11 +31,12 @@ flags_base = [f for f in B.FLAGS if f not in ("-Xptxas", "-v") and not f.startsw
 objs = []
 for src in B.SOURCES:
     o = os.path.join(B.OUT, src.replace(".cu", ".o"))
-    trace = "-DPASA_TRACE" in flags  # the trace hook lives in capi.cu too
-    if rev or src == "pasa_fwd.cu" or (trace and src == "capi.cu"):
+    # flags the launcher must see too: the trace hook, the prologue row sum's scratch
+    shared = [f for f in flags if f == "-DPASA_TRACE" or f.startswith("-DPASA_PRO_SUM")]
+    if rev or src == "pasa_fwd.cu" or (shared and src == "capi.cu"):
         o = os.path.join(out, src.replace(".cu", ".o"))
         subprocess.run([B.NVCC, *B.ARCH, *flags_base, f"-I{inc}", f"-I{csrc}",
-                        *(flags if src == "pasa_fwd.cu" else (["-DPASA_TRACE"] if trace else [])),
+                        *(flags if src == "pasa_fwd.cu" else shared),
                         "-c", os.path.join(csrc, src), "-o", o], check=True)
     objs.append(o)
 subprocess.run([B.NVCC, *B.ARCH, "-shared", "-cudart", "static", "-o",

@@ -45,7 +45,7 @@ def main():
     o = torch.empty_like(q)
     desc = _lib.Desc(1, a.hq, a.hkv, S, S, D, 128, 128, a.causal, 0, 0.984497, math.sqrt(D))
     ws = torch.empty(lib.pasa_b200_workspace_size(C.byref(desc)), dtype=torch.uint8, device=dev)
-    tr = torch.zeros(CTAS * ROLES * ITERS * EVENTS + 512 * 8, dtype=torch.int64, device=dev)  # + the PASA_STATE row-state area
+    tr = torch.zeros(CTAS * ROLES * ITERS * EVENTS + 512 * 8 + 64, dtype=torch.int64, device=dev)  # + the PASA_STATE row-state area
     st = torch.cuda.current_stream().cuda_stream
     for it in range(3):
         lib.pasa_b200_debug_set_trace(tr.data_ptr() if it == 2 else None)
@@ -55,6 +55,8 @@ def main():
     torch.cuda.synchronize()
     n = CTAS * ROLES * ITERS * EVENTS
     t = tr[:n].cpu().numpy().reshape(CTAS, ROLES, ITERS, EVENTS).astype(np.int64)
+    pro = tr[n:].cpu().numpy().view(np.float32)[512 * 8:512 * 8 + CTAS * 4].reshape(CTAS, 2, 2)
+    print("prologue cycles [cta][tile] (start -> G in TMEM, G -> stored):", pro.astype(int).tolist())
     res = {}
     for c in range(CTAS):
         base = t[c][t[c] > 0].min() if (t[c] > 0).any() else 0
