@@ -28,8 +28,8 @@ cudaError_t launch_ksum(const void* kp, void* ks, int BH, int S2, int s2, int D,
 cudaError_t launch_fwd_packed(int D, int mode, const CUtensorMap& tq, const CUtensorMap& tk,
                               const CUtensorMap& tv, const PackedParams& p, cudaStream_t stream);
 cudaError_t launch_fwd(int D, bool causal, int mode, const CUtensorMap& tq, const CUtensorMap& tk,
-                       const CUtensorMap& tv, const CUtensorMap& tks, const FwdParams& p,
-                       cudaStream_t stream);
+                       const CUtensorMap& tv, const CUtensorMap& tks, const CUtensorMap& to,
+                       const FwdParams& p, cudaStream_t stream);
 cudaError_t launch_generate(const GenParams& p, void* out, cudaStream_t stream);
 cudaError_t launch_generate_resonance(const ResonanceParams& p, void* out, cudaStream_t stream);
 }  // namespace pasa_b200
@@ -403,10 +403,13 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
   // hold every head's d values, so a {H d, S, B} map with coordinates (h d + c, s, b).
   // K and V are the caller's in FA16 mode, the BHSD workspace (K', V') in PASA mode.
   const bool kv_bshd = mode == kModeFa16 && d->layout == 1;
+  CUtensorMap to;  // O: Q's shape and layout (the epilogue's TMA store)
   if (d->layout == 1) {
     if ((rc = make_tmap(&tq, q, d->heads_q * d->head_dim, d->seq_q, d->batch))) return rc;
-  } else if ((rc = make_tmap(&tq, q, d->head_dim, d->seq_q, d->batch * d->heads_q))) {
-    return rc;
+    if ((rc = make_tmap(&to, o, d->heads_q * d->head_dim, d->seq_q, d->batch))) return rc;
+  } else {
+    if ((rc = make_tmap(&tq, q, d->head_dim, d->seq_q, d->batch * d->heads_q))) return rc;
+    if ((rc = make_tmap(&to, o, d->head_dim, d->seq_q, d->batch * d->heads_q))) return rc;
   }
   if (kv_bshd) {
     if ((rc = make_tmap(&tk, keys, d->heads_kv * d->head_dim, d->seq_kv, d->batch, d->s2))) return rc;
@@ -474,7 +477,7 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
     }
     e = launch_ksum(keys, ks, bh, d->seq_kv, d->s2, d->head_dim, st);
   }
-  if (e == cudaSuccess) e = launch_fwd(d->head_dim, d->causal != 0, mode, tq, tk, tv, tks, p, st);
+  if (e == cudaSuccess) e = launch_fwd(d->head_dim, d->causal != 0, mode, tq, tk, tv, tks, to, p, st);
   if (ks) cudaFreeAsync(ks, st);
   if (gs) cudaFreeAsync(gs, st);
   if (e != cudaSuccess) return cuda_fail(e, "pasa_fwd launch");
@@ -890,7 +893,7 @@ static int attention_host_run(const pasa_b200_desc* d, const uint16_t* q, const 
   return PASA_B200_OK;
 }
 
-#ifdef PASA_TRACE
+#if defined(PASA_TRACE) || defined(PASA_TRACE_CTA)
 // Profiling builds only (libpasa_b200_trace.so): device buffer of
 // kTraceCtas * 3 * 32 * 8 int64 that the fused kernel fills with clock64().
 __attribute__((visibility("default"))) int pasa_b200_debug_set_trace(void* device_buf) {

@@ -234,22 +234,16 @@ __device__ __forceinline__ void row_max_sum(const uint32_t* s, int lim, int pbas
 // Pass 2: P = 2^(S' - c_j) in place (masked -> 0) and its FP32 sum, same
 // eight-chain order as pass 1.  Three pairs in four use MUFU ex2.approx.f16x2,
 // one the FMA-pipe polynomial (sm100.cuh); both are within 1 ulp of 2^x.
-template <int D, bool DIAG, int I0, int I1, bool FMA>
+template <int D, bool DIAG, int I0, int I1>
 __device__ __forceinline__ void row_exp_range(uint32_t* s, int lim, int pbase, uint32_t cj2,
                                               uint32_t scale2, float* acc) {
 #pragma unroll
   for (int i = I0; i < I1; ++i) {
-    // FMA form: x = fl16(S * scale - c) in one HFMA2 -- FA16: scale = log2e/alpha,
-    // c = m*scale; PASA: scale = 2, c = 2 c_j (scores are stored in units of
-    // log2(e)/2, so the FP16 store holds 0.72x the reference's scores).
-    // Split form (PASA rows with |c_j| > 32752): x = 2 fl16(S' - c_j), exact doubling.
-    uint32_t x;
-    if (FMA) {
-      x = h2_as_u32(__hfma2(u32_as_h2(s[i]), u32_as_h2(scale2), u32_as_h2(cj2)));
-    } else {
-      const __half2 d = __hsub2(u32_as_h2(s[i]), u32_as_h2(cj2));
-      x = h2_as_u32(__hadd2(d, d));
-    }
+    // x = fl16(S * scale - c) in one HFMA2 -- FA16: scale = log2e/alpha, c = m*scale;
+    // PASA: scale = 2, c = 2 c_j (scores are stored in units of log2(e)/2, so the FP16
+    // store holds 0.72x the reference's scores), or -- rows with |c_j| > 32752 -- S
+    // already holds fl16(S' - c_j) and c = 0: x = 2 fl16(S' - c_j), an exact doubling.
+    const uint32_t x = h2_as_u32(__hfma2(u32_as_h2(s[i]), u32_as_h2(scale2), u32_as_h2(cj2)));
     // one pair in kPolyEvery on the FMA pipe, the rest on MUFU: balances MUFU time
     // (8 cycles / pair / SMSP) against issue slots (poly ~11 vs MUFU 3 per pair)
     constexpr int PE = kPolyEvery<D>;
@@ -266,22 +260,22 @@ __device__ __forceinline__ void row_exp_range(uint32_t* s, int lim, int pbase, u
 // Pass 2 over a half row in kPParts parts: part(q) runs after pairs [q NP/kPParts,
 // (q+1) NP/kPParts) are done -- the caller stores them to TMEM so the PV MMA can
 // start on those keys while the exp continues.
-template <int D, bool DIAG, int NP, bool FMA, int Q = 0, class Part>
+template <int D, bool DIAG, int NP, int Q = 0, class Part>
 __device__ __forceinline__ void row_exp_parts(uint32_t* s, int lim, int pbase, uint32_t cj2,
                                               uint32_t scale2, float* acc, Part&& part) {
   constexpr int W = NP / kPParts<D>;
-  row_exp_range<D, DIAG, Q * W, (Q + 1) * W, FMA>(s, lim, pbase, cj2, scale2, acc);
+  row_exp_range<D, DIAG, Q * W, (Q + 1) * W>(s, lim, pbase, cj2, scale2, acc);
   part(Q);
   if constexpr (Q + 1 < kPParts<D>)
-    row_exp_parts<D, DIAG, NP, FMA, Q + 1>(s, lim, pbase, cj2, scale2, acc, part);
+    row_exp_parts<D, DIAG, NP, Q + 1>(s, lim, pbase, cj2, scale2, acc, part);
 }
-template <int D, bool DIAG, int NP, bool FMA, class Part>
+template <int D, bool DIAG, int NP, class Part>
 __device__ __forceinline__ float row_exp_sum(uint32_t* s, int lim, int pbase, uint32_t cj2,
                                              uint32_t scale2, Part&& part) {
   float acc[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc[k] = 0.f;
-  row_exp_parts<D, DIAG, NP, FMA>(s, lim, pbase, cj2, scale2, acc, part);
+  row_exp_parts<D, DIAG, NP>(s, lim, pbase, cj2, scale2, acc, part);
   return __fadd_rn(__fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3])),
                    __fadd_rn(__fadd_rn(acc[4], acc[5]), __fadd_rn(acc[6], acc[7])));
 }
@@ -332,7 +326,8 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
     pasa_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_kp,
                     const __grid_constant__ CUtensorMap tm_v,
-                    const __grid_constant__ CUtensorMap tm_ks, const FwdParams p) {
+                    const __grid_constant__ CUtensorMap tm_ks,
+                    const __grid_constant__ CUtensorMap tm_o, const FwdParams p) {
   constexpr bool kTcSum = FwdCfg<D>::TCSUM && MODE == kModePasa;
   constexpr bool kProSum = pasa_prologue_rowsum(D) && MODE == kModePasa;
   // MMA issue: one warp for both tiles (PV of the first-ready tile, then its S'(j+1);
@@ -420,6 +415,10 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
   // Everything above touches only this CTA's shared memory, TMEM and the kernel
   // parameters; the inputs (Q, K', V', max|V|) may come from the previous grid.
   pdl_wait();
+#ifdef PASA_TRACE_CTA  // per-CTA lifetime (globaltimer ns) and SM id: p.trace[4 * linear id]
+  unsigned long long cta_t0 = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(cta_t0));
+#endif
   // A 512-column allocation is the whole TMEM of the SM, so it starts at lane 0, column 0:
   // the base is the constant 0 (no per-thread register, no spill, uniform addressing).
   static_assert(Cfg::TMEM_COLS == 512, "tmem_base = 0 needs the full allocation");
@@ -845,7 +844,7 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
           ep = (jc == 1) ? 0.f
                          : __half2float(__float2half_rn(ex2_f32(__fmul_rn(2.f, __fsub_rn(mprev, mnew)))));
           // x = fl16(2 S' - 2 c_j) in one HFMA2 while -2 c_j is representable (every
-          // row of the warp: |c_j| <= 32752); otherwise 2 fl16(S' - c_j) in two ops.
+          // row of the warp: |c_j| <= 32752); otherwise 2 fl16(S' - c_j) (below).
           fast2 = __all_sync(0xFFFFFFFFu, __habs(cj) <= __float2half_rn(32752.f));
           cj2 = fast2 ? h2_as_u32(__half2half2(__hmul(cj, __float2half_rn(-2.f))))
                       : h2_as_u32(__half2half2(cj));
@@ -882,13 +881,16 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
           if (lane == 0) mbar_arrive(p_part + 8 * (q * NT + t));
           if (q == 0 && tr) PASA_TR(t, j, 9);  // first P part released
         };
-        float lsum;
-        if (MODE == kModeFa16 || fast2)
-          lsum = diag ? row_exp_sum<D, true, NP, true>(s, lim, NP * h, cj2, scale2, mid)
-                      : row_exp_sum<D, false, NP, true>(s, lim, NP * h, cj2, scale2, mid);
-        else
-          lsum = diag ? row_exp_sum<D, true, NP, false>(s, lim, NP * h, cj2, scale2, mid)
-                      : row_exp_sum<D, false, NP, false>(s, lim, NP * h, cj2, scale2, mid);
+        if (MODE == kModePasa && !fast2) {
+          // rare (|c_j| > 32752 somewhere in the warp): the split form 2 fl16(S' - c_j) as
+          // S' <- fl16(S' - c_j) here, then the common pass with c = 0 (fl16(2 d) = 2 d
+          // exactly) -- one exp-pass instantiation instead of two (instruction cache)
+#pragma unroll
+          for (int i = 0; i < NP; ++i) s[i] = h2_as_u32(__hsub2(u32_as_h2(s[i]), u32_as_h2(cj2)));
+          cj2 = 0u;
+        }
+        const float lsum = diag ? row_exp_sum<D, true, NP>(s, lim, NP * h, cj2, scale2, mid)
+                                : row_exp_sum<D, false, NP>(s, lim, NP * h, cj2, scale2, mid);
         if (pingpong && ((t == 0 && j < nmin) || (t == 1 && j + 1 < nmin)))
           named_bar_arrive(2 - t, 512);
         PASA_STATE(j, 0, mloc);
@@ -929,11 +931,12 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       const float lo_other = ld_xch(xs_other + (ti.nblk & 1) * kXPar).x;
       const float l_tot = h == 0 ? __fadd_rn(l_run, lo_other) : __fadd_rn(lo_other, l_run);
       const float inv_l = __fmul_rn(__frcp_rn(l_tot), ldexpf(1.0f, c0));  // exact 2^c0
-      const bool row_ok = ti.i * kTile + row < p.S1;  // ragged last query tile
-      const size_t orow = static_cast<size_t>(ti.i) * kTile + row;
-      uint16_t* dst = p.out + (p.q_bshd ? (static_cast<size_t>(b) * p.S1 + orow) * p.Hq + ti.hq
-                                        : (static_cast<size_t>(b) * p.Hq + ti.hq) * p.S1 + orow) * D +
-                      (D / 2) * h;
+      // O goes out by TMA: each thread writes its D/2 outputs into tile t's Q buffer (dead:
+      // the tile's last S' MMA finished before its last T was ready), in the SW128 box
+      // layout of the O map (= Q's), then one thread stores the tile -- rows past S1 (a
+      // ragged last tile) are clipped by the map.  The threads' 16-byte stores go to smem
+      // instead of 512 STGs drained at CTA exit.
+      const uint32_t ostage = sb + Cfg::SMEM_Q + t * Cfg::TILE_BYTES;
 #pragma unroll
       for (int i = 0; i < D / 4; i += 4) {
         uint32_t w[4];
@@ -943,9 +946,23 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
           const __half c = __float2half_rn(__fmul_rn(hi_f(o[i + k]), inv_l));
           w[k] = h2_as_u32(__halves2half2(a, c));
         }
-        if (row_ok) *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(w[0], w[1], w[2], w[3]);
+        const int col = (D / 2) * h + 2 * i;  // first of these 8 output columns
+        const uint32_t a = ostage + (col / 64) * Cfg::BOX_BYTES + row * 128 +
+                           ((((col % 64) / 8) ^ (row & 7)) << 4);
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(w[0]), "r"(w[1]),
+                     "r"(w[2]), "r"(w[3])
+                     : "memory");
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      named_bar_sync(11 + t, 4 * Cfg::HALVES * 32);  // the tile's 256 softmax threads
+      if (h == 0 && quad == 0 && lane == 0) {
+        for (int bx = 0; bx < Cfg::NBOX; ++bx)
+          tma_store_3d(&tm_o, ostage + bx * Cfg::BOX_BYTES, (p.q_bshd ? ti.hq * D : 0) + bx * 64,
+                       ti.i * kTile, p.q_bshd ? b : b * p.Hq + ti.hq);
+        tma_store_commit_wait_read();  // the buffer must outlive the read before the CTA exits
       }
       if (DIAGNOSE) {  // out_nonfinite / out_total (pasa.cpp:275-286) and the store stats
+        const bool row_ok = ti.i * kTile + row < p.S1;  // ragged last query tile
         DiagAccum* g = static_cast<DiagAccum*>(p.diag);
         unsigned nf = 0;
 #pragma unroll
@@ -981,12 +998,26 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+#ifdef PASA_TRACE_CTA
+  if (threadIdx.x == 0 && p.trace) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    long long* e = p.trace + 4 * (static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x);
+    e[0] = static_cast<long long>(cta_t0);
+    e[1] = static_cast<long long>(t1);
+    e[2] = smid;
+    e[3] = nmax;
+  }
+#endif
 }
 
 // ---------------------------------------------------------------- launcher
 template <int D, bool CAUSAL, int MODE>
 cudaError_t launch_fwd_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                         const CUtensorMap& tks, const FwdParams& p, cudaStream_t stream) {
+                         const CUtensorMap& tks, const CUtensorMap& to, const FwdParams& p,
+                         cudaStream_t stream) {
   using Cfg = FwdCfg<D>;
   // RunDiagnostics is a separate instantiation so the production kernel's schedule is
   // untouched by the diagnostic code.
@@ -1006,14 +1037,14 @@ cudaError_t launch_fwd_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUt
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tks, p);
+  return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, tks, to, p);
 }
 
 cudaError_t launch_fwd(int D, bool causal, int mode, const CUtensorMap& tq, const CUtensorMap& tk,
-                       const CUtensorMap& tv, const CUtensorMap& tks, const FwdParams& p,
-                       cudaStream_t stream) {
+                       const CUtensorMap& tv, const CUtensorMap& tks, const CUtensorMap& to,
+                       const FwdParams& p, cudaStream_t stream) {
 #define PASA_LAUNCH(DD, CC, MM) \
-  if (D == DD && causal == CC && mode == MM) return launch_fwd_t<DD, CC, MM>(tq, tk, tv, tks, p, stream);
+  if (D == DD && causal == CC && mode == MM) return launch_fwd_t<DD, CC, MM>(tq, tk, tv, tks, to, p, stream);
   PASA_LAUNCH(128, false, kModePasa)
   PASA_LAUNCH(128, true, kModePasa)
   PASA_LAUNCH(64, false, kModePasa)

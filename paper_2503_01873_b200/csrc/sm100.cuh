@@ -127,6 +127,17 @@ __device__ __forceinline__ void tma_load_4d(uint32_t smem_dst, const void* tmap,
       "l"(tmap), "r"(bar), "r"(x), "r"(y), "r"(z), "r"(w)
       : "memory");
 }
+// TMA tensor store shared -> global (bulk group), and the wait until the shared memory it
+// reads may be reused (the global writes complete on their own).
+__device__ __forceinline__ void tma_store_3d(const void* tmap, uint32_t smem_src, int x, int y, int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+               ::"l"(tmap), "r"(smem_src), "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_commit_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 // 32 lanes x 32 columns, 32-bit each (32 regs).
 __device__ __forceinline__ void tmem_ld_32cols_b32(uint32_t taddr, uint32_t* r) {
   asm volatile(

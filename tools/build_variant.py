@@ -32,7 +32,7 @@ objs = []
 for src in B.SOURCES:
     o = os.path.join(B.OUT, src.replace(".cu", ".o"))
     # flags the launcher must see too: the trace hook, the prologue row sum's scratch
-    shared = [f for f in flags if f == "-DPASA_TRACE" or f.startswith("-DPASA_PRO_SUM")]
+    shared = [f for f in flags if f in ("-DPASA_TRACE", "-DPASA_TRACE_CTA") or f.startswith("-DPASA_PRO_SUM")]
     if rev or src == "pasa_fwd.cu" or (shared and src == "capi.cu"):
         o = os.path.join(out, src.replace(".cu", ".o"))
         subprocess.run([B.NVCC, *B.ARCH, *flags_base, f"-I{inc}", f"-I{csrc}",

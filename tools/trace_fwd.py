@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--hkv", type=int, default=4)
     ap.add_argument("--causal", type=int, default=1)
     ap.add_argument("--d", type=int, default=128)
+    ap.add_argument("--beta", type=float, default=0.984497, help="0 = the naive FP16 FA mode")
     ap.add_argument("--lib", default="libpasa_b200_trace.so",
                     help="trace build in paper_2503_01873_b200/_build (tools/build_variant.py NAME -DPASA_TRACE ...)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "trace.json"))
@@ -43,7 +44,7 @@ def main():
     k = torch.randn(1, a.hkv, S, D, device=dev).half()
     v = torch.randn(1, a.hkv, S, D, device=dev).half()
     o = torch.empty_like(q)
-    desc = _lib.Desc(1, a.hq, a.hkv, S, S, D, 128, 128, a.causal, 0, 0.984497, math.sqrt(D))
+    desc = _lib.Desc(1, a.hq, a.hkv, S, S, D, 128, 128, a.causal, 0, a.beta, math.sqrt(D))
     ws = torch.empty(lib.pasa_b200_workspace_size(C.byref(desc)), dtype=torch.uint8, device=dev)
     tr = torch.zeros(CTAS * ROLES * ITERS * EVENTS + 512 * 8 + 64, dtype=torch.int64, device=dev)  # + the PASA_STATE row-state area
     st = torch.cuda.current_stream().cuda_stream
