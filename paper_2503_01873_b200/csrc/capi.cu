@@ -343,9 +343,17 @@ int pasa_b200_preprocess(const pasa_b200_desc* d, const void* k, const void* v, 
 
 constexpr long long kMaxGridY = 65535;
 
+// Short sequences (one KV block each, N <= 64) run on the packed kernel (pasa_fwd_packed.cu).
+static bool packed_shape(const pasa_b200_desc* d, const pasa_b200_diag* diag, int s2_bound) {
+  return !diag && !d->causal && d->heads_q == d->heads_kv && d->layout == 0 && d->seq_q == d->seq_kv &&
+         d->seq_kv == d->s2 && d->s2 <= 64 && (s2_bound <= 0 || s2_bound == d->seq_kv);
+}
+
+// self_prep (PASA, packed shapes): keys / v are the raw K, V and the packed kernel runs the
+// pre-pass per tile in shared memory (no K', V' round trip through HBM).
 static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, const void* keys,
                           const void* v, const float* vmax, void* o, void* stream,
-                          pasa_b200_diag* diag = nullptr, int s2_bound = 0) {
+                          pasa_b200_diag* diag = nullptr, int s2_bound = 0, bool self_prep = false) {
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(keys) |
        reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(o)) & 15)
     return fail(PASA_B200_EINVAL, "attention_fwd: tensors must be 16-byte aligned");
@@ -355,8 +363,7 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
   {
     const long long units = (static_cast<long long>(d->heads_q / d->heads_kv) *
                                  ((d->seq_q + kTile - 1) / kTile) + 1) / 2;
-    const bool packed = !diag && !d->causal && d->heads_q == d->heads_kv && d->layout == 0 &&
-                        d->seq_q == d->seq_kv && d->seq_kv == d->s2 && d->s2 <= 64;
+    const bool packed = packed_shape(d, diag, 0);
     const long long ydim = d->causal ? units : static_cast<long long>(d->batch) * d->heads_kv;
     if (!packed && ydim > kMaxGridY && d->batch > 1) {
       const int per_b = d->causal ? 0 : static_cast<int>(kMaxGridY / d->heads_kv);
@@ -380,9 +387,7 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
   }
   CUtensorMap tq, tk, tv;
   // Short sequences (one KV block each, N <= 64): packed P = 128 / N per tensor-core tile
-  if (!diag && !d->causal && d->heads_q == d->heads_kv && d->layout == 0 &&
-      d->seq_q == d->seq_kv && d->seq_kv == d->s2 && d->s2 <= 64 &&
-      (s2_bound <= 0 || s2_bound == d->seq_kv)) {
+  if (packed_shape(d, diag, s2_bound)) {
     const int bh = d->batch * d->heads_q, rows = bh * d->seq_q, n = d->seq_q;
     if ((rc = make_tmap(&tq, q, d->head_dim, rows, 1, n))) return rc;
     if ((rc = make_tmap(&tk, keys, d->head_dim, rows, 1, n))) return rc;
@@ -395,6 +400,15 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
     pp.qk_scale = static_cast<float>(kLog2e / d->alpha);
     pp.vmax = vmax;
     pp.out = static_cast<uint16_t*>(o);
+    pp.trace = g_trace;
+    if (self_prep && mode == kModePasa) {
+      __half dg, of;
+      shift_scalars(d->s2, d->beta, d->alpha, &dg, &of);
+      pp.self_prep = 1;
+      pp.dm = __half2float(dg) - __half2float(of);  // exact: both are FP16 values
+      pp.off = __half2float(of);
+      pp.lscale = static_cast<float>(0.5 * kLog2e);  // the fused path's K' carries log2(e)/2
+    }
     cudaError_t e = launch_fwd_packed(d->head_dim, mode, tq, tk, tv, pp, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "pasa_fwd_packed launch");
     return PASA_B200_OK;
@@ -517,6 +531,9 @@ int pasa_b200_attention_fwd(const pasa_b200_desc* d, const void* q, const void* 
     return fail(PASA_B200_EINVAL, "attention_fwd: workspace too small");
   // beta == 0 degrades to the blocked FP16 attention (pasa.cpp:212-221)
   if (d->beta == 0.0) return launch_forward(d, kModeFa16, q, k, v, nullptr, o, stream, diag);
+  // short sequences: one packed kernel with the pre-pass fused (bit-identical to the path below)
+  if (packed_shape(d, diag, 0))
+    return launch_forward(d, kModePasa, q, k, v, nullptr, o, stream, nullptr, 0, /*self_prep=*/true);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   void* kp = ws;
   void* vp = ws + align_up(kp_bytes(d), 256);

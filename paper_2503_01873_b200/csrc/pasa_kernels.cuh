@@ -139,8 +139,14 @@ __host__ __device__ constexpr bool pasa_prologue_rowsum(int D) {
 struct PackedParams {
   int BH, N, W, P;
   float qk_scale;         // FA16 mode: log2(e) / alpha
-  const float* vmax;      // PASA: per sequence, from the pre-pass (V' = V 2^-c0)
+  const float* vmax;      // PASA, prepped inputs: per sequence, from the pre-pass (V' = V 2^-c0)
   uint16_t* out;
+  // PASA, self_prep = 1: the kernel reads raw K and V and runs the pre-pass per tile in shared
+  // memory -- K' = fl16(fl32(fma(dm, K, fl32(off colsum))) lscale) (pasa_kprep_rank1_small
+  // _kernel's arithmetic), max|V| and V' = V 2^-c0 per sequence (pasa_vscale_kernel's)
+  int self_prep;
+  float dm, off, lscale;  // diag - off, off (FP16 values), log2(e) / 2
+  long long* trace;       // PASA_TRACE builds: clock64 timeline of CTA 0 (pasa_fwd_packed.cu)
 };
 
 // Device generators (pasa_gen.cu; bench.cpp:28-56, rng.hpp).

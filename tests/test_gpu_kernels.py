@@ -814,3 +814,31 @@ def test_two_streams_own_workspaces(dev):
         torch.cuda.synchronize()
         for o, w in zip(outs, want):
             assert torch.equal(o.view(torch.int16), w.view(torch.int16))
+
+
+@pytest.mark.parametrize("N,D,vamp", [(25, 64, 1.0), (16, 64, 3e3), (32, 128, 1.0), (40, 64, 5e3),
+                                      (64, 128, 2e3), (25, 128, 1e4)])
+def test_packed_self_prep_matches_prepped(dev, N, D, vamp):
+    """Short sequences: pasa_b200_attention_fwd runs the packed kernel with the pre-pass
+    fused per tile (raw K, V in shared memory); it must equal, bit for bit, the separate
+    pre-pass (K', V', max|V|) + packed forward -- including V large enough that c0 > 0."""
+    from paper_2503_01873_b200 import _lib, pasa_attention_fwd
+    L = _lib.load()
+    g = torch.Generator(device=dev)
+    g.manual_seed(N * D)
+    B, H = 3, 37  # 111 sequences: ragged last tile
+    q = torch.randn(B, H, N, D, device=dev, generator=g).half()
+    k = (torch.randn(B, H, N, D, device=dev, generator=g) * 4).half()
+    v = (torch.randn(B, H, N, D, device=dev, generator=g) * vamp).half()
+    fused = pasa_attention_fwd(q, k, v, BETA_STAR, s1=N, s2=N)
+    desc = _lib.Desc(B, H, H, N, N, D, N, N, 0, 0, BETA_STAR, math.sqrt(D))
+    kp, vp, o = torch.empty_like(k), torch.empty_like(v), torch.empty_like(q)
+    vmax = torch.zeros(B * H, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.check(L.pasa_b200_preprocess(C.byref(desc), k.data_ptr(), v.data_ptr(), kp.data_ptr(),
+                                      vp.data_ptr(), vmax.data_ptr(), st))
+    _lib.check(L.pasa_b200_attention_fwd_prepped(C.byref(desc), q.data_ptr(), kp.data_ptr(), vp.data_ptr(),
+                                                 vmax.data_ptr(), o.data_ptr(), st))
+    torch.cuda.synchronize()
+    assert bool(torch.isfinite(fused).all())
+    assert torch.equal(fused.view(torch.int16), o.view(torch.int16))

@@ -1,5 +1,5 @@
 """SVD temporal attention (BASELINE configs[2], N = 25 frames, d = 64) throughput (tool).
-    python tools/temporal_bench.py
+    python tools/temporal_bench.py [B ...]   (default 1024 9216)
 Short sequences run on the packed kernel (csrc/pasa_fwd_packed.cu); the step is the key
 pre-pass + the forward, CUDA events, inputs from the resonance generator."""
 import math, os, sys
@@ -12,7 +12,8 @@ from paper_2503_01873_b200 import bench_api as ba  # noqa: E402
 
 def main():
     dev = torch.device("cuda:0")
-    for B in (1024, 9216):  # 9216 = the spatial token count of the SVD shape
+    bs = [int(x) for x in sys.argv[1:]] or [1024, 9216]
+    for B in bs:  # 9216 = the spatial token count of the SVD shape
         q = torch.randn(B, 5, 25, 64, device=dev).half()
         k, v = torch.randn_like(q), torch.randn_like(q)
         for _ in range(2):
