@@ -64,11 +64,20 @@ struct PackedCfg {
   static constexpr int STAGE_BYTES = 3 * TILE_BYTES;  // Q, K', V' of one tile
   static constexpr int STAGES = 2;
   static constexpr int SMEM_BAR = STAGES * STAGE_BYTES;
-  static constexpr int NUM_BARS = 3 * STAGES + 7;  // in_full/empty, s/p/t_full, t_empty, aux, mask, prep, qk_empty
+  static constexpr int NUM_BARS = 4 * STAGES + 6;  // in_full/empty, s/p/t_full, t_empty, aux, mask, prep_done, qk_empty
   // after the barriers: TMEM holder, bad-slot masks [2], per-stage slot exponents c0 [ST][8],
   // per-slot max|V| bits [8]
-  static constexpr int SMEM_BYTES = SMEM_BAR + 8 * NUM_BARS + 16 + 4 * (8 * STAGES + 16) + 1024;
-  static constexpr int THREADS = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 softmax
+  // after the barriers: TMEM holder, bad-slot masks [4], slot exponents c0 [4][8], the
+  // prep's per-slot max|V| bits and non-finite slots [9]
+  static constexpr int SMEM_BYTES = SMEM_BAR + 8 * NUM_BARS + 4 * (1 + 4 + 32 + 16) + 1024;
+  // warpgroup 0: warp 0 TMA, warp 1 MMA (2, 3 idle); 1: softmax (warps 4-7 = TMEM lane
+  // quadrants 0-3); 2: the per-tile pre-pass (self_prep)
+  static constexpr int THREADS = 384;
+  // setmaxnreg split of the launch allocation (d = 64: 2 CTAs per SM, 80 x 384 = 30720
+  // registers each; d = 128: 1 CTA, 168 x 384)
+  static constexpr int REGS_CTL = D == 64 ? 32 : 40, REGS_PREP = D == 64 ? 56 : 64,
+                       REGS_SM = D == 64 ? 152 : 232;
+  static_assert(128 * (REGS_CTL + REGS_PREP + REGS_SM) <= (D == 64 ? 80 : 168) * THREADS, "registers");
   static constexpr uint32_t TMEM_COLS = D == 64 ? 256 : 512;
   static constexpr uint32_t T_CLEAN = 128 + D;  // P V' over zeroed poisoned rows
 };
@@ -175,11 +184,11 @@ __device__ __noinline__ void self_prep_stage(uint32_t stage, const PackedParams&
   const uint32_t vt = stage + 2 * TILE;
   // (the parameters as values: through the reference every "memory"-clobbering shared
   // access below would reload them)
-  const int tid = threadIdx.x - 64, W = p.W, N = p.N;
+  const int tid = threadIdx.x - 256, W = p.W, N = p.N;
   const float dm = p.dm, off_s = p.off, lscale = p.lscale;
   if (tid < 9) vmx[tid] = 0u;  // [0, 8): slot max|V| bits, [8]: non-finite slots
   mbar_wait(in_full, parity);
-  if (threadIdx.x == 64) PK_TR(0, trit, 6);
+  if (threadIdx.x == 256) PK_TR(0, trit, 6);
   named_bar_sync(1, 128);  // vmx reset before any thread's atomicMax
   // Rows of a slot start at a multiple of 8 (W is), so row r0 + c of a batch of 8 (c0 % 8 == 0)
   // has swizzle key u = c % 8: within a batch every address is a constant offset from the
@@ -241,7 +250,7 @@ __device__ __noinline__ void self_prep_stage(uint32_t stage, const PackedParams&
   badl = __reduce_or_sync(0xffffffffu, badl);
   if ((threadIdx.x & 31) == 0 && badl) atomicOr(vmx + 8, badl);
   named_bar_sync(1, 128);  // every slot's max|V| and the non-finite slots are in
-  if (threadIdx.x == 64) PK_TR(0, trit, 7);
+  if (threadIdx.x == 256) PK_TR(0, trit, 7);
   for (int e = tid; e < nseq * (D / 2); e += 128) {
     const int sl = e / (D / 2), cp = e % (D / 2), r0 = sl * W;
     const int cz = pasa_inflation(N, __uint_as_float(vmx[sl]));
@@ -280,14 +289,15 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
                  t_empty = t_full + 8;
   const uint32_t aux = t_empty + 8;       // the first P V' of a poisoned tile is done
   const uint32_t mask_full = aux + 8;     // the tile's poisoned-slot mask is published
-  const uint32_t prep_done = mask_full + 8;  // self_prep: the stage holds K', V', c0, mask
-  const uint32_t qk_empty = prep_done + 8;   // [ST]: the stage's S' MMA has read Q and K'
+  const uint32_t prep_done = mask_full + 8;     // [ST] self_prep: the stage holds K', V', c0, mask
+  const uint32_t qk_empty = prep_done + 8 * ST;  // [ST]: the stage's S' MMA has read Q and K'
   // (in_empty: its P V' has read V' -- the Q / K' half of a stage refills a PV earlier)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Cfg::SMEM_BAR + 8 * Cfg::NUM_BARS);
   // [it % 2]: bit s = slot s of tile it holds a non-finite V' row
-  volatile uint32_t* bad_mask = tmem_holder + 2;
-  int* c0s = reinterpret_cast<int*>(tmem_holder + 4);            // [ST][8]
-  unsigned* vmx = reinterpret_cast<unsigned*>(c0s + 8 * ST);     // [9] (self_prep scratch)
+  // per tile it, slot it & 3: written up to two tiles ahead of the epilogue that reads it
+  volatile uint32_t* bad_mask = tmem_holder + 1;                 // [4]
+  int* c0s = reinterpret_cast<int*>(tmem_holder + 5);            // [4][8]
+  unsigned* vmx = reinterpret_cast<unsigned*>(c0s + 32);         // [9] (prep scratch)
   const int warp = static_cast<int>(warp_id());
   const int lane = threadIdx.x & 31;
   const int W = p.W;                                // slot stride (rows / keys)
@@ -305,7 +315,7 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
     mbar_init(t_empty, 4);
     mbar_init(aux, 1);
     mbar_init(mask_full, 1);
-    mbar_init(prep_done, 1);
+    for (int st = 0; st < ST; ++st) mbar_init(prep_done + 8 * st, 1);
     fence_barrier_init();
   }
   {  // V' rows outside the sequences' N-row slots must read as zero (P = 0 there, and 0 x
@@ -322,6 +332,9 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
+  const bool self_prep = MODE == kModePasa && p.self_prep;
+  if (warp < 4) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::REGS_CTL));
   if (warp == 0) {
     // ---- TMA producer: each sequence's N rows of Q, K', V' into its slot
     if (elect_one()) {
@@ -364,7 +377,7 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
       const uint32_t vbase = base + 2 * Cfg::TILE_BYTES;
       // self_prep: the softmax warps turn K, V into K', V' in place first (and find the
       // non-finite slots); else the stage holds the pre-pass output as loaded
-      if (p.self_prep) mbar_wait(prep_done, it & 1);
+      if (self_prep) mbar_wait(prep_done + 8 * st, (it / ST) & 1);
       else mbar_wait(in_full + 8 * st, (it / ST) & 1);
       tc_fence_after();
       // S' = Q K'^T (SS, F16 accumulator) into columns [0, 128); in-order after the
@@ -382,8 +395,8 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
       }
       // while S' runs: which slots' V' rows hold Inf / NaN?  0 x v is NaN exactly for a
       // non-finite v, so one HFMA2 per pair accumulates the verdict.
-      uint32_t bad = p.self_prep ? bad_mask[it & 1] : 0u;  // (self_prep: from the prep)
-      for (int r = lane; !p.self_prep && r < nseq * W; r += 32) {
+      uint32_t bad = self_prep ? bad_mask[it & 3] : 0u;  // (self_prep: from the prep)
+      for (int r = lane; !self_prep && r < nseq * W; r += 32) {
         if (r % W >= p.N) continue;  // gap rows are zero
         __half2 acc = __float2half2_rn(0.f);
 #pragma unroll
@@ -408,7 +421,7 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
       // publish the mask (release) only now: the softmax has finished tile it - 1 (p_full),
       // so mask_full is never two phases ahead of its reader and slot it & 1 is free
       if (leader) {
-        if (!p.self_prep) bad_mask[it & 1] = bad;
+        if (!self_prep) bad_mask[it & 3] = bad;
         mbar_arrive(mask_full);
       }
       mbar_wait(t_empty, (it & 1) ^ 1);
@@ -443,29 +456,21 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
       }
       __syncwarp();
     }
-  } else {
+  }
+  } else if (warp < 8) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Cfg::REGS_SM));
     // ---- softmax: one thread per row
     const int quad = warp % 4;
     const int row = quad * 32 + lane;
     const uint32_t t_s = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
     const int sl = row / W, rr = row % W;            // the row's slot and row in the slot
     const int lo = sl * W, hi = lo + p.N;            // its sequence's key columns
-    // self_prep: tile it + 1's pre-pass runs right after tile it's P is stored, while the
-    // tensor core does tile it's P V' (the MMA warp waits for it before S'(it + 1))
-    auto prep = [&](int it2, int tile2) {
-      const int st2 = it2 % ST;
-      self_prep_stage<D>(sb + st2 * Cfg::STAGE_BYTES, p, min(p.P, p.BH - tile2 * p.P), c0s + 8 * st2,
-                         vmx, bad_mask + (it2 & 1), in_full + 8 * st2, (it2 / ST) & 1, it2);
-      if (threadIdx.x == 64) mbar_arrive(prep_done);  // (after the prep's last barrier)
-    };
-    const bool self_prep = MODE == kModePasa && p.self_prep;
-    if (self_prep && static_cast<int>(blockIdx.x) < ntiles) prep(0, blockIdx.x);
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int seq0 = tile * p.P, nseq = min(p.P, p.BH - seq0);
       const bool row_ok = sl < nseq && rr < p.N;
       const int st = it % ST;
-      const bool tr0 = threadIdx.x == 64;
+      const bool tr0 = threadIdx.x == 128;
       if (tr0) PK_TR(0, it, 0);
       mbar_wait(s_full, it & 1);
       if (tr0) PK_TR(0, it, 1);
@@ -485,14 +490,13 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
       if (tr0) PK_TR(0, it, 2);
-      if (self_prep && tile + static_cast<int>(gridDim.x) < ntiles) prep(it + 1, tile + gridDim.x);
       if (tr0) PK_TR(0, it, 3);
       // epilogue: O = T 2^c0 / l (global recovering, pasa.cpp:184-194)
       const int c0 = MODE != kModePasa || !row_ok ? 0
-                     : p.self_prep ? c0s[8 * st + sl] : pasa_inflation(p.N, p.vmax[seq0 + sl]);
+                     : self_prep ? c0s[8 * (it & 3) + sl] : pasa_inflation(p.N, p.vmax[seq0 + sl]);
       const float inv_l = __fmul_rn(__frcp_rn(l), ldexpf(1.0f, c0));
       mbar_wait(mask_full, it & 1);
-      const uint32_t bad = bad_mask[it & 1];
+      const uint32_t bad = bad_mask[it & 3];
       // a poisoned tile: this row's own sequence poisoned -> T, else T_clean (warp-uniform
       // column choice per load: rows of a warp may sit in different slots)
       const bool clean = bad != 0 && !((bad >> sl) & 1u);
@@ -529,6 +533,17 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
         }
         if (row_ok) *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(w[0], w[1], w[2], w[3]);
       }
+    }
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::REGS_PREP));
+    // ---- the pre-pass of every tile (self_prep), as soon as its stage has landed: runs
+    // ahead of the softmax, which it never waits for (the MMA warp waits for prep_done)
+    int it = 0;
+    for (int tile = blockIdx.x; self_prep && tile < ntiles; tile += gridDim.x, ++it) {
+      const int st = it % ST;
+      self_prep_stage<D>(sb + st * Cfg::STAGE_BYTES, p, min(p.P, p.BH - tile * p.P), c0s + 8 * (it & 3),
+                         vmx, bad_mask + (it & 3), in_full + 8 * st, (it / ST) & 1, it);
+      if (threadIdx.x == 256) mbar_arrive(prep_done + 8 * st);  // (after the prep's last barrier)
     }
   }
   tc_fence_before();
