@@ -1,11 +1,10 @@
 """Copy one measurement run (gpurun_out/) into profiles/ (tool).
-    python tools/write_profiles.py
-Expects gpurun_out/{bench.json, bench_ref.json, sweep.json, launches.csv, ncu_fwd128.ncu-rep,
-ncu_fwd64.ncu-rep} from: python bench.py; python bench.py --impl reference; tools/sweep.py;
-ncu --metrics gpu__time_duration.sum (bench launch list); ncu --set full on
-tools/ncu_once.py --shape qwen16k / svd.  Writes the round-1 files and
-profiles/roofline_traffic.json (DRAM bytes per launch, read by bench.py)."""
-import csv, json, os, re, shutil, statistics, subprocess
+    python tools/write_profiles.py [TAG]      (TAG: the round, default r02)
+Expects gpurun_out/{bench.json, bench_ref.json, sweep.json, overflow.json, launches.csv,
+ncu_fwd128.ncu-rep, ncu_fwd64.ncu-rep, ncu_packed.ncu-rep} from tools/refresh_profiles.sh.
+Writes profiles/TAG_* and profiles/roofline_traffic.json (DRAM bytes per launch, read by
+bench.py)."""
+import csv, json, os, re, shutil, statistics, subprocess, sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G, P = os.path.join(ROOT, "gpurun_out"), os.path.join(ROOT, "profiles")
@@ -32,6 +31,7 @@ def last_json(path):
 
 
 def main():
+    tag = sys.argv[1] if len(sys.argv) > 1 else "r02"
     out = []
     for r in csv.reader(open(os.path.join(G, "launches.csv"))):
         if r and r[0] == "ID":
@@ -42,7 +42,7 @@ def main():
             if d.get("Metric Name") == "gpu__time_duration.sum":
                 v = float(d["Metric Value"]) * {"ns": 1, "us": 1e3, "ms": 1e6}.get(d["Metric Unit"], 1)
                 out.append((int(d["ID"]), d["Kernel Name"], int(v)))
-    with open(os.path.join(P, "r01_ncu_launches.csv"), "w") as f:
+    with open(os.path.join(P, f"{tag}_ncu_launches.csv"), "w") as f:
         f.write("# ncu --metrics gpu__time_duration.sum --clock-control none -c 60 (cold-cache, serialised): "
                 "PASA_BENCH_NO_SWEEP=1 PASA_BENCH_NO_CPU=1 python bench.py --steps 2 --warmup 3\n")
         w = csv.writer(f)
@@ -51,30 +51,38 @@ def main():
     mean = lambda key: statistics.mean(o[2] for o in out if key in o[1]) / 1e3  # noqa: E731
     k, v, fw = mean("kprep_rank1"), mean("vscale"), mean("pasa_fwd_kernel")
     s128 = ncu_summary(os.path.join(G, "ncu_fwd128.ncu-rep"))
-    open(os.path.join(P, "r01_ncu_pasa_fwd_summary.txt"), "w").write(
-        "# ncu --set full --clock-control none --import-source on -k regex:pasa_fwd -s 2 -c 1 (B200, round 1)\n"
+    open(os.path.join(P, f"{tag}_ncu_pasa_fwd_summary.txt"), "w").write(
+        f"# ncu --set full --clock-control none --import-source on -k regex:pasa_fwd -s 2 -c 1 (B200, {tag})\n"
         "# command: python tools/ncu_once.py --shape qwen16k  (pre-pass, then three forward launches; the third is captured)\n"
-        "# kernel: pasa_fwd_kernel<128, causal, PASA, no-diag> on Qwen2-7B attention (Hq=28, Hkv=4, N=16384), hybrid(0,10) inputs\n"
-        + s128 + f"\n# per-step launch shares (profiles/r01_ncu_launches.csv, device steps of bench.py, cold & serialised): "
+        "# kernel: pasa_fwd_kernel<128, causal, PASA, no-diag> on Qwen2-7B attention (Hq=28, Hkv=4, N=16384), uniform(30, 0.5) inputs\n"
+        + s128 + f"\n# per-step launch shares (profiles/{tag}_ncu_launches.csv, device steps of bench.py, cold & serialised): "
         f"kprep_rank1 {k:.1f} us, vscale {v:.1f} us, pasa_fwd {fw:.0f} us ({100 * fw / (k + v + fw):.1f} %)\n")
     s64 = ncu_summary(os.path.join(G, "ncu_fwd64.ncu-rep"))
-    open(os.path.join(P, "r01_ncu_pasa_fwd_d64_summary.txt"), "w").write(
-        "# ncu --set full --clock-control none --import-source on -k regex:pasa_fwd -s 2 -c 1 (B200, round 1)\n"
-        "# command: python tools/ncu_once.py --shape svd  (B=50, H=5, N=9216, d=64, non-causal; BASELINE configs[2] shape)\n"
+    open(os.path.join(P, f"{tag}_ncu_pasa_fwd_d64_summary.txt"), "w").write(
+        f"# ncu --set full --clock-control none --import-source on -k regex:pasa_fwd -s 2 -c 1 (B200, {tag})\n"
+        "# command: python tools/ncu_once.py --shape svd  (B=50, H=5, N=9216, d=64, non-causal, resonance Q/K; BASELINE configs[2])\n"
         "# kernel: pasa_fwd_kernel<64, non-causal, PASA, no-diag>: S' row sums from the tensor core (pseudo-average GEMM), one MMA issuer per tile\n"
         + s64 + "# xu (MUFU) is the busiest pipe at d = 64: half the MMA work per exponential of d = 128\n")
+    sp = ncu_summary(os.path.join(G, "ncu_packed.ncu-rep"))
+    open(os.path.join(P, f"{tag}_ncu_packed_summary.txt"), "w").write(
+        f"# ncu --set full --clock-control none --import-source on -k regex:packed -s 2 -c 1 (B200, {tag})\n"
+        "# command: python tools/ncu_once.py --shape temporal  (B=9216, H=5, N=25, d=64: the SVD temporal attention)\n"
+        "# kernel: pasa_fwd_packed_kernel<64, PASA> with the pre-pass fused (self_prep): reads Q, K, V, writes O\n"
+        + sp + "# memory-bound: algorithmic bytes 4 x 147.5 MB per launch\n")
     num = lambda key: float(re.search(re.escape(key) + r"\s+\S+\s+([\d.]+)", s128).group(1))  # noqa: E731
     rd, wr = num("dram__bytes_read.sum") * 1e6, num("dram__bytes_write.sum") * 1e6
     json.dump({"kernel": "pasa_fwd_kernel<128,true> (Qwen2-7B attn, N=16384, Hq=28, Hkv=4, causal)",
-               "source": "ncu --set full --clock-control none, round 1 (profiles/r01_ncu_pasa_fwd_summary.txt)",
+               "source": f"ncu --set full --clock-control none, {tag} (profiles/{tag}_ncu_pasa_fwd_summary.txt)",
                "dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
                "algorithmic_bytes_per_launch": 268435456,
                "note": "write < O bytes: the tail of O is still in L2 (write-back) when the kernel ends"},
               open(os.path.join(P, "roofline_traffic.json"), "w"), indent=1)
-    open(os.path.join(P, "r01_bench_16k.json"), "w").write(json.dumps(last_json(os.path.join(G, "bench.json")), indent=1) + "\n")
-    open(os.path.join(P, "r01_bench_reference_arm.json"), "w").write(
+    open(os.path.join(P, f"{tag}_bench_16k.json"), "w").write(json.dumps(last_json(os.path.join(G, "bench.json")), indent=1) + "\n")
+    open(os.path.join(P, f"{tag}_bench_reference_arm.json"), "w").write(
         json.dumps(last_json(os.path.join(G, "bench_ref.json")), indent=1) + "\n")
-    shutil.copy(os.path.join(G, "sweep.json"), os.path.join(P, "r01_sweep.json"))
+    shutil.copy(os.path.join(G, "sweep.json"), os.path.join(P, f"{tag}_sweep.json"))
+    if os.path.exists(os.path.join(G, "overflow.json")):
+        shutil.copy(os.path.join(G, "overflow.json"), os.path.join(P, f"{tag}_overflow_stress.json"))
     print(f"profiles written; pasa_fwd {fw:.0f} us of {k + v + fw:.0f} us per step")
 
 
