@@ -19,10 +19,13 @@
 // the fused kernel does when the sequence is alone: the output is bit-identical to
 // pasa_fwd.cu's, whatever the packing (host pipeline pieces, multi-GPU shards).
 //
-// Persistent CTAs walk the tiles; 6 warps: warp 0 loads (TMA, a two-stage ring, so the next
-// tile's loads overlap this one's compute), warp 1 issues the MMAs, warps 2-5 run the
-// softmax with one thread per row (TMEM lane quadrant = warp % 4).  TMEM: S'/P at +0, T at
-// +128, T_clean at +128 + D (256 columns at d = 64, so two CTAs share an SM; 512 at d = 128).
+// Persistent CTAs walk the tiles; three warpgroups: warp 0 loads (TMA, a two-stage ring, so
+// the next tile's loads overlap this one's compute) and warp 1 issues the MMAs; warps 4-7 run
+// the softmax with one thread per row (TMEM lane quadrant = warp % 4); warps 8-11 (self_prep,
+// the public entry point) run the key pre-pass and the V scale of each staged tile in shared
+// memory -- K' = rank-1 form of K^T M, V' = V 2^-c0 -- so the kernel reads raw K, V from HBM
+// and no workspace round trip is needed.  TMEM: S'/P at +0, T at +128, T_clean at +128 + D
+// (256 columns at d = 64, so two CTAs share an SM; 512 at d = 128).
 //
 // Non-finite V: the tile's P V' also multiplies each row's zero P entries by the other
 // sequences' V' rows, and 0 x Inf = NaN would leak one sequence's Inf/NaN into its
@@ -42,13 +45,20 @@ namespace pasa_b200 {
 using namespace sm100;
 
 // PASA_TRACE builds: CTA 0 records clock64() at fixed points of its first 64 tiles,
-// p.trace[(role * 64 + it) * 8 + event] (role 0 = softmax warp 2 lane 0, 1 = MMA issuer)
+// p.trace[(role * 64 + it) * 16 + event]: role 0 = softmax thread 128 (0 start, 1 S' ready,
+// 2 P stored, 3 O stored, 4 T ready, 5 T read) and the prep (6 stage landed, 7 K' written);
+// role 1 = MMA issuer (0 S' issued, 1 P ready, 2 PV committed), TMA producer (3 Q/K issued,
+// 4 V issued), prep (5 start, 6 done, 8 K/V pass, 9 K' pass, 10 V scale + c0, 11 fenced)
 #ifdef PASA_TRACE
-#define PK_TR(role, it, ev)                                                        \
+#define PK_TRP(tr, role, it, ev)                                                   \
   do {                                                                             \
-    if (p.trace && blockIdx.x == 0 && (it) < 64) p.trace[((role) * 64 + (it)) * 8 + (ev)] = clock64(); \
+    if ((tr) && blockIdx.x == 0 && (it) < 64) (tr)[((role) * 64 + (it)) * 16 + (ev)] = clock64(); \
   } while (0)
+#define PK_TR(role, it, ev) PK_TRP(p.trace, role, it, ev)
 #else
+#define PK_TRP(tr, role, it, ev) \
+  do {                           \
+  } while (0)
 #define PK_TR(role, it, ev) \
   do {                      \
   } while (0)
@@ -64,9 +74,8 @@ struct PackedCfg {
   static constexpr int STAGE_BYTES = 3 * TILE_BYTES;  // Q, K', V' of one tile
   static constexpr int STAGES = 2;
   static constexpr int SMEM_BAR = STAGES * STAGE_BYTES;
-  static constexpr int NUM_BARS = 4 * STAGES + 6;  // in_full/empty, s/p/t_full, t_empty, aux, mask, prep_done, qk_empty
-  // after the barriers: TMEM holder, bad-slot masks [2], per-stage slot exponents c0 [ST][8],
-  // per-slot max|V| bits [8]
+  // qk_full, v_full, in_empty, kprep_done, vprep_done, qk_empty [ST]; s/p/t_full, t_empty, aux, mask
+  static constexpr int NUM_BARS = 6 * STAGES + 6;
   // after the barriers: TMEM holder, bad-slot masks [4], slot exponents c0 [4][8], the
   // prep's per-slot max|V| bits and non-finite slots [9]
   static constexpr int SMEM_BYTES = SMEM_BAR + 8 * NUM_BARS + 4 * (1 + 4 + 32 + 16) + 1024;
@@ -155,8 +164,8 @@ __device__ __noinline__ float row_softmax(uint32_t t_s, int quad, int lo, int hi
                    __fadd_rn(__fadd_rn(acc[4], acc[5]), __fadd_rn(acc[6], acc[7])));
 }
 
-// Self-prepped tile (PackedParams::self_prep, PASA): the 128 softmax threads turn the raw
-// K and V of the stage's nseq sequences into K' and V' in place, with the pre-pass kernels'
+// Self-prepped tile (PackedParams::self_prep, PASA): the prep warpgroup turns the raw K and
+// V of the stage's nseq sequences into K' and V' in place, with the pre-pass kernels'
 // arithmetic (so the output is bit-identical to the prepped path): per sequence and column,
 // colsum = FP32 sum over its N rows ascending, K' = fl16(fl32(fl32(fma(dm, K, fl32(off
 // colsum))) lscale)); max|V| (NaN ignored), c0 = pasa_inflation(N, max|V|), V' = V x
@@ -164,109 +173,168 @@ __device__ __noinline__ float row_softmax(uint32_t t_s, int quad, int lo, int hi
 // mask for the MMA warp) and c0 per slot for the epilogue.  Thread e owns column pair e % (D/2)
 // of slot e / (D/2); the smem tiles are SW128 (row r: 128 bytes per 64-column box, 16-byte
 // chunks XOR-ed with r % 8).
-__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
-  uint32_t v;
-  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
-  asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+//
+// This runs once per tile on one warp per SMSP, so its latency sets the tile rate
+// (tools/prep_probe.cu times it alone), and on a lone warp every branch costs ~20 cycles
+// (predicate set + resolve + reconvergence).  So the slot width WS is a template parameter
+// and the code is straight-line: the WS rows of a slot fully unrolled, rows >= N masked by
+// selects / predicated stores (rows past N are the slot's gap: stale K, zero V), a thread's
+// column pairs unrolled with a predicate, c0 without branches, and the one branch left is the
+// rare V scale.  Shared memory through shared-space pointers (sptr): in an out-of-line
+// function a generic pointer would take the slow generic path.
+template <class T>
+__device__ __forceinline__ T* sptr(uint32_t a) {  // a .shared address as a shared-space pointer
+  extern __shared__ uint8_t smem_raw[];
+  return reinterpret_cast<T*>(smem_raw + (a - smem_u32(smem_raw)));
 }
 
-template <int D>
-__device__ __noinline__ void self_prep_stage(uint32_t stage, const PackedParams& p, int nseq, int* c0,
-                                             unsigned* vmx, volatile uint32_t* bad_out, uint32_t in_full,
-                                             uint32_t parity, int trit) {
-  // (shared-memory addresses as 32-bit .shared offsets: through a generic pointer in this
-  // out-of-line function every access would take the slow generic path)
+// pasa_inflation without branches (same value): 0 unless 1 < need < 3e38, else ceil(log2 need)
+__device__ __forceinline__ int inflation_nb(int S2, float vmax) {
+  const float need = static_cast<float>(S2) * vmax * (1.0f / 16384.0f);
+  const uint32_t b = __float_as_uint(need);
+  const int e = static_cast<int>(b >> 23) - 127 + ((b & 0x7fffffu) != 0u);
+  return (need > 1.0f && need < 3.0e38f) ? e : 0;
+}
+
+// K side of a tile, as soon as its Q and K have landed: column sums and K' in place; clears
+// the max|V| words for the V side (whose atomics follow this function's last barrier).
+template <int D, int WS>
+__device__ __forceinline__ void self_prep_k(uint32_t stage, int N, float dm, float off_s, float lscale, int nseq,
+                                            uint32_t vmx_s, uint32_t qk_full, uint32_t parity, long long* trace,
+                                            int trit) {
+  // (the parameters as register arguments: a PackedParams reference would be read from the
+  // caller's stack -- local memory -- on every call)
   constexpr int BOX = kTile * 128, TILE = (D / 64) * BOX;
+  constexpr int P = 128 / WS, IPT = (P * (D / 2) + 127) / 128;  // column pairs per thread
   const uint32_t kt = stage + TILE;
-  const uint32_t vt = stage + 2 * TILE;
-  // (the parameters as values: through the reference every "memory"-clobbering shared
-  // access below would reload them)
-  const int tid = threadIdx.x - 256, W = p.W, N = p.N;
-  const float dm = p.dm, off_s = p.off, lscale = p.lscale;
-  if (tid < 9) vmx[tid] = 0u;  // [0, 8): slot max|V| bits, [8]: non-finite slots
-  mbar_wait(in_full, parity);
-  if (threadIdx.x == 256) PK_TR(0, trit, 6);
-  named_bar_sync(1, 128);  // vmx reset before any thread's atomicMax
-  // Rows of a slot start at a multiple of 8 (W is), so row r0 + c of a batch of 8 (c0 % 8 == 0)
-  // has swizzle key u = c % 8: within a batch every address is a constant offset from the
-  // batch's base -- no per-element address arithmetic.
-  uint32_t badl = 0;
-  for (int e = tid; e < nseq * (D / 2); e += 128) {
-    const int sl = e / (D / 2), cp = e % (D / 2), r0 = sl * W;
-    const int col = 2 * cp, chunk = (col % 64) / 8;
-    const uint32_t cbase = (col / 64) * BOX + (col % 8) * 2 + r0 * 128;  // + c * 128 + swizzle
-    auto off = [&](int u) { return static_cast<uint32_t>(u * 128 + ((chunk ^ u) << 4)); };
-    // FP32 column sums, rows ascending (the pre-pass's order; add.f32.f16 converts exactly),
-    // max|V| in half2 (HMNMX2 ignores NaN like fmaxf), and 0 x V accumulated in half2: NaN
-    // exactly when some V is Inf or NaN
+  const int tid = threadIdx.x - 256;
+  if (tid < 9) sptr<unsigned>(vmx_s)[tid] = 0u;  // [0, 8): slot max|V| bits, [8]: non-finite slots
+  mbar_wait(qk_full, parity);
+  if (threadIdx.x == 256) PK_TRP(trace, 0, trit, 6);
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int e = tid + 128 * i;
+    const bool live = e < nseq * (D / 2);
+    const int sl = e / (D / 2), cp = e % (D / 2);
+    const int col = 2 * cp, ck = (col % 64) / 8;
+    // row c of the slot: swizzle key c % 8 (slots start at multiples of 8): a constant offset
+    const uint32_t cb = kt + (col / 64) * BOX + (col % 8) * 2 + sl * WS * 128;
+    auto off = [&](int c) { return cb + static_cast<uint32_t>(c * 128 + ((ck ^ (c & 7)) << 4)); };
+    // FP32 column sums, rows ascending (the pre-pass's order; add.f32.f16 converts exactly;
+    // + 0 for the masked rows is exact: the sum starts at +0 and never becomes -0)
     float csx = 0.f, csy = 0.f;
-    __half2 vm2 = __float2half2_rn(0.f), nf2 = __float2half2_rn(0.f);
-    auto absorb = [&](__half2 kh, __half2 vh) {
-      csx = add_lo_f16(csx, h2_as_u32(kh));
-      csy = add_hi_f16(csy, h2_as_u32(kh));
-      vm2 = __hmax2(vm2, __habs2(vh));
-      nf2 = __hfma2(vh, __float2half2_rn(0.f), nf2);
-    };
-    int c0 = 0;
-    for (; c0 + 8 <= N; c0 += 8) {  // full batches: every load in flight before the first use
-      const uint32_t b = cbase + c0 * 128;
-      __half2 kb[8], vb[8];
+#pragma unroll
+    for (int c0 = 0; c0 < WS; c0 += 8) {
+      uint32_t kb[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) kb[u] = *sptr<uint32_t>(off(c0 + u));
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        kb[u] = u32_as_h2(lds_u32(kt + b + off(u)));
-        vb[u] = u32_as_h2(lds_u32(vt + b + off(u)));
+        const uint32_t k = c0 + u < N ? kb[u] : 0u;  // (gap rows hold stale K)
+        csx = add_lo_f16(csx, k);
+        csy = add_hi_f16(csy, k);
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) absorb(kb[u], vb[u]);
     }
-    for (int u = 0; c0 + u < N; ++u)
-      absorb(u32_as_h2(lds_u32(kt + cbase + c0 * 128 + off(u))), u32_as_h2(lds_u32(vt + cbase + c0 * 128 + off(u))));
-    const float vm = fmaxf(__low2float(vm2), __high2float(vm2));
-    atomicMax(vmx + sl, __float_as_uint(vm));  // vm >= 0: bit order = value order
-    if (__hisnan(__low2half(nf2)) || __hisnan(__high2half(nf2))) badl |= 1u << sl;
+    // K' = fl16(fl32(fma(dm, K, fl32(off colsum))) lscale), rows < N
     const float osx = __fmul_rn(off_s, csx), osy = __fmul_rn(off_s, csy);
-    auto kprime = [&](uint32_t a) {
-      const float2 k2 = __half22float2(u32_as_h2(lds_u32(a)));
-      sts_u32(a, h2_as_u32(__floats2half2_rn(__fmul_rn(__fmaf_rn(dm, k2.x, osx), lscale),
-                                             __fmul_rn(__fmaf_rn(dm, k2.y, osy), lscale))));
-    };
-    for (c0 = 0; c0 + 8 <= N; c0 += 8) {
-      const uint32_t b = kt + cbase + c0 * 128;
-      __half2 kb[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) kb[u] = u32_as_h2(lds_u32(b + off(u)));
+    for (int c0 = 0; c0 < WS; c0 += 8) {
+      uint32_t kb[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) kb[u] = *sptr<uint32_t>(off(c0 + u));
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const float2 k2 = __half22float2(kb[u]);
-        sts_u32(b + off(u), h2_as_u32(__floats2half2_rn(__fmul_rn(__fmaf_rn(dm, k2.x, osx), lscale),
-                                                         __fmul_rn(__fmaf_rn(dm, k2.y, osy), lscale))));
+        const float2 k2 = __half22float2(u32_as_h2(kb[u]));
+        const uint32_t kp = h2_as_u32(__floats2half2_rn(__fmul_rn(__fmaf_rn(dm, k2.x, osx), lscale),
+                                                        __fmul_rn(__fmaf_rn(dm, k2.y, osy), lscale)));
+        if (live && c0 + u < N) *sptr<uint32_t>(off(c0 + u)) = kp;
       }
     }
-    for (int u = 0; c0 + u < N; ++u) kprime(kt + cbase + c0 * 128 + off(u));
   }
-  badl = __reduce_or_sync(0xffffffffu, badl);
-  if ((threadIdx.x & 31) == 0 && badl) atomicOr(vmx + 8, badl);
-  named_bar_sync(1, 128);  // every slot's max|V| and the non-finite slots are in
-  if (threadIdx.x == 256) PK_TR(0, trit, 7);
-  for (int e = tid; e < nseq * (D / 2); e += 128) {
-    const int sl = e / (D / 2), cp = e % (D / 2), r0 = sl * W;
-    const int cz = pasa_inflation(N, __uint_as_float(vmx[sl]));
-    if (cz == 0) continue;  // (the usual case: V' = V)
-    const __half2 sc = __half2half2(__float2half_rn(ldexpf(1.0f, -cz)));
-    const int col = 2 * cp;
-    for (int c = 0; c < N; ++c) {
-      const uint32_t a = vt + (col / 64) * BOX + (r0 + c) * 128 + ((((col % 64) / 8) ^ (c & 7)) << 4) +
-                         (col % 8) * 2;
-      sts_u32(a, h2_as_u32(__hmul2(u32_as_h2(lds_u32(a)), sc)));
+  if (threadIdx.x == 256) PK_TRP(trace, 1, trit, 8);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // K' for the tensor core
+  named_bar_sync(1, 128);
+}
+
+// V side, once V has landed: max|V| and the non-finite check per slot, c0, V' in the (rare)
+// tiles that need it, the poisoned-slot mask.  (Tried on the idle warps 2-3 instead, beside
+// the K side: slower -- two warps at 32-40 registers take longer than the P V' can wait.)
+template <int D, int WS>
+__device__ __forceinline__ void self_prep_v(uint32_t stage, int N, int nseq, uint32_t c0_s, uint32_t vmx_s,
+                                            uint32_t bad_s, uint32_t v_full, uint32_t parity, long long* trace,
+                                            int trit) {
+  constexpr int BOX = kTile * 128, TILE = (D / 64) * BOX;
+  constexpr int P = 128 / WS, IPT = (P * (D / 2) + 127) / 128;
+  const uint32_t vt = stage + 2 * TILE;
+  unsigned* vmx = sptr<unsigned>(vmx_s);
+  const int tid = threadIdx.x - 256;
+  mbar_wait(v_full, parity);
+  if (threadIdx.x == 256) PK_TRP(trace, 1, trit, 9);
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int e = tid + 128 * i;
+    const int sl = e / (D / 2), cp = e % (D / 2), col = 2 * cp, ck = (col % 64) / 8;
+    const uint32_t cb = vt + (col / 64) * BOX + (col % 8) * 2 + sl * WS * 128;
+    __half2 vm2 = __float2half2_rn(0.f), nf2 = vm2;
+#pragma unroll
+    for (int c0 = 0; c0 < WS; c0 += 8) {
+      uint32_t vb[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)  // (gap rows of V are zero)
+        vb[u] = *sptr<uint32_t>(cb + static_cast<uint32_t>((c0 + u) * 128 + ((ck ^ u) << 4)));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        vm2 = __hmax2(vm2, __habs2(u32_as_h2(vb[u])));               // NaN ignored, like fmaxf
+        nf2 = __hfma2(u32_as_h2(vb[u]), __float2half2_rn(0.f), nf2);  // NaN iff some V is Inf / NaN
+      }
+    }
+    if (e < nseq * (D / 2)) {
+      atomicMax(vmx + sl, __float_as_uint(fmaxf(__low2float(vm2), __high2float(vm2))));  // >= 0: bits order
+      if (__hisnan(__low2half(nf2)) || __hisnan(__high2half(nf2))) atomicOr(vmx + 8, 1u << sl);
     }
   }
-  if (tid < 8) c0[tid] = tid < nseq ? pasa_inflation(N, __uint_as_float(vmx[tid])) : 0;
-  if (tid == 0) *bad_out = vmx[8];
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // K', V' for the tensor core
+  named_bar_sync(1, 128);  // every slot's max|V| and the non-finite slots are in
+  if (threadIdx.x == 256) PK_TRP(trace, 1, trit, 10);
+  // V' = V fl16(2^-c0): only in the (rare) tiles where some slot needs it
+  int cz[IPT];
+  bool any = false;
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int e = tid + 128 * i;
+    cz[i] = e < nseq * (D / 2) ? inflation_nb(N, __uint_as_float(vmx[e / (D / 2)])) : 0;
+    any |= cz[i] > 0;
+  }
+  if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int e = tid + 128 * i;
+      const int sl = e / (D / 2), cp = e % (D / 2), col = 2 * cp, ck = (col % 64) / 8;
+      const __half2 sc = __half2half2(__float2half_rn(ldexpf(1.0f, -cz[i])));
+      const uint32_t cb = vt + (col / 64) * BOX + (col % 8) * 2 + sl * WS * 128;
+#pragma unroll
+      for (int c = 0; c < WS; ++c) {
+        uint32_t* a = sptr<uint32_t>(cb + static_cast<uint32_t>(c * 128 + ((ck ^ (c & 7)) << 4)));
+        if (cz[i] > 0 && c < N) *a = h2_as_u32(__hmul2(u32_as_h2(*a), sc));
+      }
+    }
+  }
+  if (tid < 8) sptr<int>(c0_s)[tid] = tid < nseq ? inflation_nb(N, __uint_as_float(vmx[tid])) : 0;
+  if (tid == 0) *sptr<uint32_t>(bad_s) = vmx[8];
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // V' for the tensor core
   named_bar_sync(1, 128);
+  if (threadIdx.x == 256) PK_TRP(trace, 1, trit, 11);
+}
+
+// One tile: the K side, kprep_done (the MMA warp may issue S'), then the V side.  (One
+// out-of-line function: two consecutive out-of-line calls here make ptxas 12.9 run for hours.)
+template <int D, int WS>
+__device__ __noinline__ void self_prep_stage(uint32_t stage, int N, float dm, float off_s, float lscale, int nseq,
+                                             uint32_t c0_s, uint32_t vmx_s, uint32_t bad_s, uint32_t qk_full,
+                                             uint32_t v_full, uint32_t kprep_done, uint32_t parity,
+                                             long long* trace, int trit) {
+  self_prep_k<D, WS>(stage, N, dm, off_s, lscale, nseq, vmx_s, qk_full, parity, trace, trit);
+  if (threadIdx.x == 256) mbar_arrive(kprep_done);
+  self_prep_v<D, WS>(stage, N, nseq, c0_s, vmx_s, bad_s, v_full, parity, trace, trit);
 }
 
 }  // namespace
@@ -283,14 +351,16 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sb = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (sb - smem_u32(smem_raw));
-  const uint32_t in_full = sb + Cfg::SMEM_BAR;  // [ST]
-  const uint32_t in_empty = in_full + 8 * ST;   // [ST]: the stage's MMAs are done
+  const uint32_t qk_full = sb + Cfg::SMEM_BAR;  // [ST]: the stage's Q and K (K') have landed
+  const uint32_t v_full = qk_full + 8 * ST;     // [ST]: its V (V') has landed
+  const uint32_t in_empty = v_full + 8 * ST;    // [ST]: the stage's MMAs are done
   const uint32_t s_full = in_empty + 8 * ST, p_full = s_full + 8, t_full = p_full + 8,
                  t_empty = t_full + 8;
   const uint32_t aux = t_empty + 8;       // the first P V' of a poisoned tile is done
   const uint32_t mask_full = aux + 8;     // the tile's poisoned-slot mask is published
-  const uint32_t prep_done = mask_full + 8;     // [ST] self_prep: the stage holds K', V', c0, mask
-  const uint32_t qk_empty = prep_done + 8 * ST;  // [ST]: the stage's S' MMA has read Q and K'
+  const uint32_t kprep_done = mask_full + 8;     // [ST] self_prep: the stage holds K'
+  const uint32_t vprep_done = kprep_done + 8 * ST;  // [ST] self_prep: ... and V', c0, the mask
+  const uint32_t qk_empty = vprep_done + 8 * ST;  // [ST]: the stage's S' MMA has read Q and K'
   // (in_empty: its P V' has read V' -- the Q / K' half of a stage refills a PV earlier)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Cfg::SMEM_BAR + 8 * Cfg::NUM_BARS);
   // [it % 2]: bit s = slot s of tile it holds a non-finite V' row
@@ -305,9 +375,12 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
 
   if (threadIdx.x == 0) {
     for (int st = 0; st < ST; ++st) {
-      mbar_init(in_full + 8 * st, 1);
+      mbar_init(qk_full + 8 * st, 1);
+      mbar_init(v_full + 8 * st, 1);
       mbar_init(in_empty + 8 * st, 1);
       mbar_init(qk_empty + 8 * st, 1);
+      mbar_init(kprep_done + 8 * st, 1);
+      mbar_init(vprep_done + 8 * st, 1);
     }
     mbar_init(s_full, 1);
     mbar_init(p_full, 4);
@@ -315,7 +388,6 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
     mbar_init(t_empty, 4);
     mbar_init(aux, 1);
     mbar_init(mask_full, 1);
-    for (int st = 0; st < ST; ++st) mbar_init(prep_done + 8 * st, 1);
     fence_barrier_init();
   }
   {  // V' rows outside the sequences' N-row slots must read as zero (P = 0 there, and 0 x
@@ -347,22 +419,25 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
         const uint32_t base = sb + st * Cfg::STAGE_BYTES;
         // Q and K' as soon as the stage's S' has run, V' once its P V' has
         mbar_wait(qk_empty + 8 * st, ((it / ST) & 1) ^ 1);
-        mbar_expect_tx(in_full + 8 * st, 3 * Cfg::NBOX * nseq * p.N * 128);
+        mbar_expect_tx(qk_full + 8 * st, 2 * Cfg::NBOX * nseq * p.N * 128);
         for (int sl = 0; sl < nseq; ++sl) {
           const int r = (seq0 + sl) * p.N;  // flat row of the sequence
           for (int bx = 0; bx < Cfg::NBOX; ++bx) {
             const uint32_t off = bx * Cfg::BOX_BYTES + sl * W * 128;
-            tma_load_3d(base + off, &tm_q, in_full + 8 * st, bx * 64, r, 0);
-            tma_load_3d(base + Cfg::TILE_BYTES + off, &tm_kp, in_full + 8 * st, bx * 64, r, 0);
+            tma_load_3d(base + off, &tm_q, qk_full + 8 * st, bx * 64, r, 0);
+            tma_load_3d(base + Cfg::TILE_BYTES + off, &tm_kp, qk_full + 8 * st, bx * 64, r, 0);
           }
         }
+        PK_TR(1, it, 3);
         mbar_wait(in_empty + 8 * st, ((it / ST) & 1) ^ 1);
+        mbar_expect_tx(v_full + 8 * st, Cfg::NBOX * nseq * p.N * 128);
         for (int sl = 0; sl < nseq; ++sl) {
           const int r = (seq0 + sl) * p.N;
           for (int bx = 0; bx < Cfg::NBOX; ++bx)
             tma_load_3d(base + 2 * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES + sl * W * 128, &tm_v,
-                        in_full + 8 * st, bx * 64, r, 0);
+                        v_full + 8 * st, bx * 64, r, 0);
         }
+        PK_TR(1, it, 4);
       }
     }
   } else if (warp == 1) {
@@ -375,10 +450,9 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
       const int st = it % ST, nseq = min(p.P, p.BH - tile * p.P);
       const uint32_t base = sb + st * Cfg::STAGE_BYTES;
       const uint32_t vbase = base + 2 * Cfg::TILE_BYTES;
-      // self_prep: the softmax warps turn K, V into K', V' in place first (and find the
-      // non-finite slots); else the stage holds the pre-pass output as loaded
-      if (self_prep) mbar_wait(prep_done + 8 * st, (it / ST) & 1);
-      else mbar_wait(in_full + 8 * st, (it / ST) & 1);
+      // self_prep: the prep warpgroup turns K into K' in place first (V' and the non-finite
+      // slots follow, before P V'); else the stage holds the pre-pass output as loaded
+      mbar_wait((self_prep ? kprep_done : qk_full) + 8 * st, (it / ST) & 1);
       tc_fence_after();
       // S' = Q K'^T (SS, F16 accumulator) into columns [0, 128); in-order after the
       // previous tile's PV, so its P columns are free
@@ -395,7 +469,8 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
       }
       // while S' runs: which slots' V' rows hold Inf / NaN?  0 x v is NaN exactly for a
       // non-finite v, so one HFMA2 per pair accumulates the verdict.
-      uint32_t bad = self_prep ? bad_mask[it & 3] : 0u;  // (self_prep: from the prep)
+      uint32_t bad = 0u;
+      if (!self_prep) mbar_wait(v_full + 8 * st, (it / ST) & 1);
       for (int r = lane; !self_prep && r < nseq * W; r += 32) {
         if (r % W >= p.N) continue;  // gap rows are zero
         __half2 acc = __float2half2_rn(0.f);
@@ -416,6 +491,11 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
       bad = __reduce_or_sync(0xffffffffu, bad);
       // T = P V' (TS: P packed in columns [0, 64), V' MN-major) into [128, 128 + D), once
       // the softmax has stored P and read the previous tile's T
+      if (self_prep) {  // V' and the mask (from the prep)
+        mbar_wait(vprep_done + 8 * st, (it / ST) & 1);
+        tc_fence_after();
+        bad = bad_mask[it & 3];
+      }
       mbar_wait(p_full, it & 1);
       if (leader) PK_TR(1, it, 1);
       // publish the mask (release) only now: the softmax has finished tile it - 1 (p_full),
@@ -490,12 +570,12 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
       if (tr0) PK_TR(0, it, 2);
-      if (tr0) PK_TR(0, it, 3);
-      // epilogue: O = T 2^c0 / l (global recovering, pasa.cpp:184-194)
+      // epilogue: O = T 2^c0 / l (global recovering, pasa.cpp:184-194); self_prep: c0 from the
+      // prep, published with the mask
+      mbar_wait(mask_full, it & 1);
       const int c0 = MODE != kModePasa || !row_ok ? 0
                      : self_prep ? c0s[8 * (it & 3) + sl] : pasa_inflation(p.N, p.vmax[seq0 + sl]);
       const float inv_l = __fmul_rn(__frcp_rn(l), ldexpf(1.0f, c0));
-      mbar_wait(mask_full, it & 1);
       const uint32_t bad = bad_mask[it & 3];
       // a poisoned tile: this row's own sequence poisoned -> T, else T_clean (warp-uniform
       // column choice per load: rows of a warp may sit in different slots)
@@ -533,17 +613,34 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
         }
         if (row_ok) *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(w[0], w[1], w[2], w[3]);
       }
+      if (tr0) PK_TR(0, it, 3);
     }
   } else {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::REGS_PREP));
     // ---- the pre-pass of every tile (self_prep), as soon as its stage has landed: runs
-    // ahead of the softmax, which it never waits for (the MMA warp waits for prep_done)
+    // ahead of the softmax, which it never waits for (the MMA warp waits for kprep_done before
+    // S' and for vprep_done before P V')
     int it = 0;
     for (int tile = blockIdx.x; self_prep && tile < ntiles; tile += gridDim.x, ++it) {
       const int st = it % ST;
-      self_prep_stage<D>(sb + st * Cfg::STAGE_BYTES, p, min(p.P, p.BH - tile * p.P), c0s + 8 * (it & 3),
-                         vmx, bad_mask + (it & 3), in_full + 8 * st, (it / ST) & 1, it);
-      if (threadIdx.x == 256) mbar_arrive(prep_done + 8 * st);  // (after the prep's last barrier)
+      if (threadIdx.x == 256) PK_TR(1, it, 5);
+      const uint32_t stg = sb + st * Cfg::STAGE_BYTES, c0a = smem_u32(c0s + 8 * (it & 3)), vma = smem_u32(vmx),
+                     bada = smem_u32(const_cast<uint32_t*>(bad_mask) + (it & 3));
+      const int ns = min(p.P, p.BH - tile * p.P);
+      const uint32_t par = (it / ST) & 1;
+      // the slot width as a compile-time row count (straight-line pre-pass)
+#define PK_PREP(WS)                                                                                  \
+  self_prep_stage<D, WS>(stg, p.N, p.dm, p.off, p.lscale, ns, c0a, vma, bada, qk_full + 8 * st, v_full + 8 * st, \
+                         kprep_done + 8 * st, par, p.trace, it)
+      switch (W) {
+        case 16: PK_PREP(16); break;
+        case 32: PK_PREP(32); break;
+        case 48: PK_PREP(48); break;
+        default: PK_PREP(64); break;
+      }
+#undef PK_PREP
+      if (threadIdx.x == 256) mbar_arrive(vprep_done + 8 * st);  // (after the prep's last barrier)
+      if (threadIdx.x == 256) PK_TR(1, it, 6);
     }
   }
   tc_fence_before();
@@ -562,7 +659,10 @@ static cudaError_t launch_packed_t(const CUtensorMap& tq, const CUtensorMap& tk,
   if (e != cudaSuccess) return e;
   const int tiles = (p.BH + p.P - 1) / p.P;  // p.P = 128 / p.W sequences per tile
   const int sms = current_sm_count();  // the launching (current) device
-  const int per_sm = D == 64 ? 2 : 1;  // shared memory: 2 x 98 KB (d = 64), 194 KB (d = 128)
+  int per_sm = D == 64 ? 2 : 1;  // shared memory: 2 x 98 KB (d = 64), 194 KB (d = 128)
+#ifdef PASA_TRACE
+  if (getenv("PASA_PACKED_PER_SM")) per_sm = atoi(getenv("PASA_PACKED_PER_SM"));  // (profiling)
+#endif
   const int grid = tiles < per_sm * sms ? tiles : per_sm * sms;
   pasa_fwd_packed_kernel<D, MODE><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(tq, tk, tv, p);
   return cudaGetLastError();

@@ -1,4 +1,4 @@
-"""Build a variant of libpasa_b200.so with extra -D flags on pasa_fwd.cu (tool).
+"""Build a variant of libpasa_b200.so with extra -D flags on pasa_fwd.cu and pasa_fwd_packed.cu (tool).
     python tools/build_variant.py NAME [--rev GIT_REV] -DPASA_POLY_EVERY=2 ...
 writes paper_2503_01873_b200/_build/NAME.so (for tools/variants.py).  --rev builds
 every CUDA source (and header) of the library as of another commit (e.g. HEAD for an
@@ -33,10 +33,11 @@ for src in B.SOURCES:
     o = os.path.join(B.OUT, src.replace(".cu", ".o"))
     # flags the launcher must see too: the trace hook, the prologue row sum's scratch
     shared = [f for f in flags if f in ("-DPASA_TRACE", "-DPASA_TRACE_CTA") or f.startswith("-DPASA_PRO_SUM")]
-    if rev or src == "pasa_fwd.cu" or (shared and src == "capi.cu"):
+    kern = src in ("pasa_fwd.cu", "pasa_fwd_packed.cu")
+    if rev or (kern and flags) or src == "pasa_fwd.cu" or (shared and src == "capi.cu"):
         o = os.path.join(out, src.replace(".cu", ".o"))
         subprocess.run([B.NVCC, *B.ARCH, *flags_base, f"-I{inc}", f"-I{csrc}",
-                        *(flags if src == "pasa_fwd.cu" else shared),
+                        *(flags if kern else shared),
                         "-c", os.path.join(csrc, src), "-o", o], check=True)
     objs.append(o)
 subprocess.run([B.NVCC, *B.ARCH, "-shared", "-cudart", "static", "-o",

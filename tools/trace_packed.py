@@ -1,9 +1,9 @@
 """Timeline of the packed short-sequence kernel (PASA_TRACE build; profiling tool).
     python -m paper_2503_01873_b200.build --trace && python tools/trace_packed.py [B]
-CTA 0, first tiles: softmax (wait S', exp + P store, next tile's pre-pass, wait T, read T,
-epilogue) and MMA issuer (S' issued, P ready, PV issued) in clock64 cycles."""
-import ctypes as C, math, os, sys
-import numpy as np
+CTA 0, tiles 1..24, in clock64 cycles: the TMA producer (Q/K, V issued), the pre-pass
+warpgroup (stage landed, K' written, done), the MMA issuer (S' issued, P ready, PV committed)
+and the softmax warpgroup (S' ready, P stored, T ready, T read, O stored)."""
+import ctypes as C, os, sys
 import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -20,23 +20,28 @@ def main():
     desc = _lib.Desc(B, 5, 5, 25, 25, 64, 25, 25, 0, 0, 0.984497, 8.0)
     ws = torch.empty(L.pasa_b200_workspace_size(C.byref(desc)), dtype=torch.uint8, device=dev)
     o = torch.empty_like(q)
-    tr = torch.zeros(2 * 64 * 8, dtype=torch.int64, device=dev)
+    tr = torch.zeros(2 * 64 * 16, dtype=torch.int64, device=dev)
     for it in range(3):
         L.pasa_b200_debug_set_trace(tr.data_ptr() if it == 2 else None)
         _lib.check(L.pasa_b200_attention_fwd(C.byref(desc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                              o.data_ptr(), ws.data_ptr(), ws.numel(), None,
                                              torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
-    t = tr.cpu().numpy().reshape(2, 64, 8)
-    base = t[t > 0].min()
-    print(" it | sm: waitS  exp+P  prep  waitT  ldT   epi | mma: S'->Pready  Pready->PVdone | period |"
-          " prep(it+1): in_full wait, K/V pass, V scale + c0")
-    for i in range(1, 20):
-        a, m = t[0, i] - base, t[1, i] - base
-        nxt = t[0, i + 1, 0] - base
-        print(f"{i:3d} | {a[1]-a[0]:6d} {a[2]-a[1]:6d} {a[3]-a[2]:6d} {a[4]-a[3]:6d} {a[5]-a[4]:5d} "
-              f"{nxt - a[5]:5d} | {m[1]-m[0]:8d} {m[2]-m[1]:8d} | {nxt - a[0]:6d} | "
-              f"{t[0, i + 1, 6] - t[0, i, 2]:6d} {t[0, i + 1, 7] - t[0, i + 1, 6]:6d} {t[0, i, 3] - t[0, i + 1, 7]:6d}")
+    t = tr.cpu().numpy().reshape(2, 64, 16)
+    sm, ct = t[0], t[1]
+    base = sm[1, 0]
+    print("absolute cycles from tile 1's softmax start (k = 1000 cycles)")
+    print(" it |   QKiss   Viss | landed  Kdone   prep | S'iss  Prdy  PVcom | S'rdy  Pst  Trdy  Trd  Ost |"
+          " load  prep  S'lat  exp  PV  epi | period")
+    f = lambda x: f"{(x - base) / 1000:6.2f}"
+    for i in range(1, 25):
+        period = sm[i + 1, 1] - sm[i, 1]
+        print(f"{i:3d} | {f(ct[i,3])} {f(ct[i,4])} | {f(sm[i,6])} {f(sm[i,7])} {f(ct[i,6])} | "
+              f"{f(ct[i,0])} {f(ct[i,1])} {f(ct[i,2])} | {f(sm[i,1])} {f(sm[i,2])} {f(sm[i,4])} {f(sm[i,5])} "
+              f"{f(sm[i,3])} | {sm[i,6]-ct[i,4]:5d} {ct[i,6]-sm[i,6]:5d} {sm[i,1]-ct[i,0]:5d} "
+              f"{sm[i,2]-sm[i,1]:5d} {ct[i,2]-ct[i,1]:4d} {sm[i,3]-sm[i,5]:4d} | {period:5d} | "
+              f"prep: K side {ct[i,8]-sm[i,6]:5d} (K landed {sm[i,6]-ct[i,3]:5d} after issue) | V landed "
+              f"{ct[i,9]-ct[i,4]:5d} after issue, V side {ct[i,10]-ct[i,9]:5d} c0 {ct[i,11]-ct[i,10]:5d}")
 
 
 if __name__ == "__main__":
