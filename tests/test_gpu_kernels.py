@@ -817,11 +817,14 @@ def test_two_streams_own_workspaces(dev):
 
 
 @pytest.mark.parametrize("N,D,vamp", [(25, 64, 1.0), (16, 64, 3e3), (32, 128, 1.0), (40, 64, 5e3),
-                                      (64, 128, 2e3), (25, 128, 1e4)])
+                                      (64, 128, 2e3), (25, 128, 1e4), (8, 64, -4e3), (48, 128, -3e3),
+                                      (1, 64, 1.0), (57, 64, -6e3), (13, 128, -1e4)])
 def test_packed_self_prep_matches_prepped(dev, N, D, vamp):
     """Short sequences: pasa_b200_attention_fwd runs the packed kernel with the pre-pass
     fused per tile (raw K, V in shared memory); it must equal, bit for bit, the separate
-    pre-pass (K', V', max|V|) + packed forward -- including V large enough that c0 > 0."""
+    pre-pass (K', V', max|V|) + packed forward -- including V large enough that c0 > 0, in
+    every slot (vamp > 1) or in every third sequence only (vamp < 0: tiles mixing slots that
+    need the V scale with slots that do not), every slot width (N = 1 ... 64)."""
     from paper_2503_01873_b200 import _lib, pasa_attention_fwd
     L = _lib.load()
     g = torch.Generator(device=dev)
@@ -829,7 +832,12 @@ def test_packed_self_prep_matches_prepped(dev, N, D, vamp):
     B, H = 3, 37  # 111 sequences: ragged last tile
     q = torch.randn(B, H, N, D, device=dev, generator=g).half()
     k = (torch.randn(B, H, N, D, device=dev, generator=g) * 4).half()
-    v = (torch.randn(B, H, N, D, device=dev, generator=g) * vamp).half()
+    v = torch.randn(B, H, N, D, device=dev, generator=g)
+    if vamp < 0:  # every third sequence large
+        v.view(B * H, N, D)[::3] *= -vamp
+    else:
+        v *= vamp
+    v = v.half()
     fused = pasa_attention_fwd(q, k, v, BETA_STAR, s1=N, s2=N)
     desc = _lib.Desc(B, H, H, N, N, D, N, N, 0, 0, BETA_STAR, math.sqrt(D))
     kp, vp, o = torch.empty_like(k), torch.empty_like(v), torch.empty_like(q)
