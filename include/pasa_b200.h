@@ -126,6 +126,19 @@ PASA_B200_API int pasa_b200_attention_fwd(const pasa_b200_desc* desc, const void
                             const void* v, void* o, void* workspace, size_t workspace_bytes,
                             pasa_b200_diag* diag, void* stream);
 
+/* Query-row shard of pasa_b200_attention_fwd: computes the rows of query tiles
+ * [tile0, tile0 + ntiles) (128 rows each; the last tile may be ragged) of every (b, h) and
+ * leaves the other rows of o untouched.  The key pre-pass runs over every key, and each tile
+ * is computed exactly as in the whole problem (same S1, S2, causal offset, K', V', c0), so
+ * the union of shards is bit-identical to one pasa_b200_attention_fwd call.  This is what
+ * balances a problem with fewer (b, kv head) units than GPUs (split q-tiles).
+ * Replaces: the (b, h, i) loop of pasa_attention restricted to a range of i
+ * (pasa.cpp:243-287). */
+PASA_B200_API int pasa_b200_attention_fwd_tiles(const pasa_b200_desc* d, const void* q, const void* k,
+                                                const void* v, void* o, void* workspace,
+                                                size_t workspace_bytes, int32_t tile0, int32_t ntiles,
+                                                void* stream);
+
 /* The full pre-pass of the fused kernel, device pointers, stream-ordered:
  * kp = K'^T blocks with lscale = log2(e)/2 (as pasa_b200_preprocess_keys),
  * vmax = max|V| per (b, kv head), and vp = V * 2^-c0 per head with

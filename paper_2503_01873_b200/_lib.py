@@ -66,6 +66,7 @@ def load(path: str = SO) -> C.CDLL:
     L.pasa_b200_workspace_size.argtypes = [dp]
     L.pasa_b200_preprocess_keys.argtypes = [dp, vp, vp, vp, vp, C.c_float, vp]
     L.pasa_b200_attention_fwd.argtypes = [dp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp]
+    L.pasa_b200_attention_fwd_tiles.argtypes = [dp, vp, vp, vp, vp, vp, C.c_size_t, C.c_int32, C.c_int32, vp]
     L.pasa_b200_attention_fwd_prepped.argtypes = [dp, vp, vp, vp, vp, vp, vp]
     L.pasa_b200_preprocess.argtypes = [dp, vp, vp, vp, vp, vp, vp]
     L.pasa_b200_attention_host.argtypes = [dp, vp, vp, vp, vp]

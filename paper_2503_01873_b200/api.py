@@ -301,12 +301,16 @@ def pasa_attention_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, beta: 
                        causal: bool = False, s1: int = 128, s2: int = 128,
                        out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
                        stream: torch.cuda.Stream | None = None,
-                       diag: "RunDiagnostics | None" = None, layout: str = "bhsd") -> torch.Tensor:
+                       diag: "RunDiagnostics | None" = None, layout: str = "bhsd",
+                       q_tiles: tuple[int, int] | None = None) -> torch.Tensor:
     """Device entry point: fp16 CUDA tensors (BHSD, or BSHD with ``layout="bshd"``),
     asynchronous on ``stream`` (default: the current stream; another stream first waits
     for the current one, and everything it reads or writes stays allocated until it is
     done).  ``diag`` (optional) is merged with the device RunDiagnostics of this call (the
-    diagnostic kernel instantiation; synchronises the stream)."""
+    diagnostic kernel instantiation; synchronises the stream).  ``q_tiles=(t0, n)``
+    computes only the query rows of 128-row tiles [t0, t0 + n) of every (b, h)
+    (pasa_b200_attention_fwd_tiles: bit-identical to those rows of the whole call; the
+    other rows of ``out`` are left as they were)."""
     L = _lib.load()
     _check_device_tensors("pasa_attention_fwd", q, k, v, out)
     if workspace is not None and (not workspace.is_cuda or workspace.device != q.device):
@@ -325,11 +329,19 @@ def pasa_attention_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, beta: 
             if diag is not None:
                 dbuf = torch.empty(C.sizeof(_lib.Diag), dtype=torch.uint8, device=q.device)
                 _lib.check(L.pasa_b200_diag_reset(dbuf.data_ptr(), s.cuda_stream))
-            _lib.check(L.pasa_b200_attention_fwd(C.byref(desc), q.data_ptr(), k.data_ptr(),
-                                                 v.data_ptr(), out.data_ptr(), workspace.data_ptr(),
-                                                 workspace.numel() * workspace.element_size(),
-                                                 dbuf.data_ptr() if dbuf is not None else None,
-                                                 s.cuda_stream))
+            if q_tiles is not None:
+                if diag is not None:
+                    raise ValueError("pasa_attention_fwd: diag is not supported with q_tiles")
+                _lib.check(L.pasa_b200_attention_fwd_tiles(
+                    C.byref(desc), q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                    workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+                    int(q_tiles[0]), int(q_tiles[1]), s.cuda_stream))
+            else:
+                _lib.check(L.pasa_b200_attention_fwd(C.byref(desc), q.data_ptr(), k.data_ptr(),
+                                                     v.data_ptr(), out.data_ptr(), workspace.data_ptr(),
+                                                     workspace.numel() * workspace.element_size(),
+                                                     dbuf.data_ptr() if dbuf is not None else None,
+                                                     s.cuda_stream))
         _hold_for(s, cur, q, k, v, out, workspace)
     if dbuf is not None:
         s.synchronize()

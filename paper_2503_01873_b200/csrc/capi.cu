@@ -351,18 +351,24 @@ static bool packed_shape(const pasa_b200_desc* d, const pasa_b200_diag* diag, in
 
 // self_prep (PASA, packed shapes): keys / v are the raw K, V and the packed kernel runs the
 // pre-pass per tile in shared memory (no K', V' round trip through HBM).
+// [tile_lo, tile_hi): the 128-row query tiles computed (of every (b, h)); -1 = all.  Every
+// tile is computed exactly as in the whole problem (same S1, S2, causal offset, K', V', c0),
+// so query-row shards are bit-identical to the unsharded output.
 static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, const void* keys,
                           const void* v, const float* vmax, void* o, void* stream,
-                          pasa_b200_diag* diag = nullptr, int s2_bound = 0, bool self_prep = false) {
+                          pasa_b200_diag* diag = nullptr, int s2_bound = 0, bool self_prep = false,
+                          int tile_lo = 0, int tile_hi = -1) {
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(keys) |
        reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(o)) & 15)
     return fail(PASA_B200_EINVAL, "attention_fwd: tensors must be 16-byte aligned");
+  const int nq_all = (d->seq_q + kTile - 1) / kTile;
+  if (tile_hi < 0) tile_hi = nq_all;
+  if (tile_hi <= tile_lo) return PASA_B200_OK;  // an empty query range
   int rc;
   // The fused kernel's grid has B Hkv kv heads in one dimension (y when non-causal) and the
   // query units in the other; beyond the 65535 limit of y the batch is cut into launches.
   {
-    const long long units = (static_cast<long long>(d->heads_q / d->heads_kv) *
-                                 ((d->seq_q + kTile - 1) / kTile) + 1) / 2;
+    const long long units = (static_cast<long long>(d->heads_q / d->heads_kv) * (tile_hi - tile_lo) + 1) / 2;
     const bool packed = packed_shape(d, diag, 0);
     const long long ydim = d->causal ? units : static_cast<long long>(d->batch) * d->heads_kv;
     if (!packed && ydim > kMaxGridY && d->batch > 1) {
@@ -377,7 +383,8 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
                             static_cast<const uint8_t*>(keys) + kb * b0,
                             static_cast<const uint8_t*>(v) + kb * b0,
                             vmax ? vmax + static_cast<size_t>(b0) * d->heads_kv : nullptr,
-                            static_cast<uint8_t*>(o) + qb * b0, stream, diag, s2_bound);
+                            static_cast<uint8_t*>(o) + qb * b0, stream, diag, s2_bound, false, tile_lo,
+                            tile_hi);
         if (rc) return rc;
       }
       return PASA_B200_OK;
@@ -447,7 +454,8 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
   p.s2 = d->s2;
   p.inv_s2 = static_cast<float>(1.0 / d->s2);
   p.group = d->heads_q / d->heads_kv;
-  p.tiles_per_kv = p.group * p.nq;
+  p.tile_hi = tile_hi;
+  p.tiles_per_kv = p.group * (tile_hi - tile_lo);
   p.inva = static_cast<float>(d->beta / (1.0 - d->beta));  // pasa.cpp:85
   p.qk_scale = static_cast<float>(kLog2e / d->alpha);
   p.vmax = vmax;
@@ -542,6 +550,33 @@ int pasa_b200_attention_fwd(const pasa_b200_desc* d, const void* q, const void* 
   if (rc) return rc;
   if (!diag) return pasa_b200_attention_fwd_prepped(d, q, kp, vp, vmax, o, stream);
   return launch_forward(d, kModePasa, q, kp, vp, vmax, o, stream, diag);
+}
+
+int pasa_b200_attention_fwd_tiles(const pasa_b200_desc* d, const void* q, const void* k, const void* v,
+                                  void* o, void* workspace, size_t workspace_bytes, int32_t tile0,
+                                  int32_t ntiles, void* stream) {
+  g_last_error.clear();
+  int rc = check_desc(d);
+  if (rc) return rc;
+  if (!q || !k || !v || !o || !workspace)
+    return fail(PASA_B200_EINVAL, "attention_fwd_tiles: NULL tensor or workspace");
+  if (workspace_bytes < pasa_b200_workspace_size(d))
+    return fail(PASA_B200_EINVAL, "attention_fwd_tiles: workspace too small");
+  const int nq = (d->seq_q + kTile - 1) / kTile;
+  if (tile0 < 0 || ntiles < 0 || tile0 > nq || ntiles > nq - tile0)
+    return fail(PASA_B200_EINVAL, "attention_fwd_tiles: tile range outside [0, ceil(seq_q / 128))");
+  if (ntiles == 0) return PASA_B200_OK;
+  if (d->beta == 0.0) return launch_forward(d, kModeFa16, q, k, v, nullptr, o, stream, nullptr, 0, false, tile0,
+                                            tile0 + ntiles);
+  if (packed_shape(d, nullptr, 0))  // one query tile per sequence: the range is the whole problem
+    return launch_forward(d, kModePasa, q, k, v, nullptr, o, stream, nullptr, 0, /*self_prep=*/true);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  void* kp = ws;
+  void* vp = ws + align_up(kp_bytes(d), 256);
+  float* vmax = reinterpret_cast<float*>(ws + 2 * align_up(kp_bytes(d), 256));
+  rc = pasa_b200_preprocess(d, k, v, kp, vp, vmax, stream);  // every key: K', V', c0 as unsharded
+  if (rc) return rc;
+  return launch_forward(d, kModePasa, q, kp, vp, vmax, o, stream, nullptr, 0, false, tile0, tile0 + ntiles);
 }
 
 __global__ void diag_reset_kernel(pasa_b200_diag* g) {

@@ -178,7 +178,7 @@ struct TileInfo {
 __device__ __forceinline__ TileInfo tile_info(const FwdParams& p, int hkv, int idx, bool causal) {
   TileInfo ti;
   ti.valid = idx < p.tiles_per_kv;
-  ti.i = p.nq - 1 - idx / p.group;  // longest (causal) tiles first
+  ti.i = p.tile_hi - 1 - idx / p.group;  // longest (causal) tiles first
   ti.hq = hkv * p.group + idx % p.group;
   // causal, bottom-right aligned: query row r sees keys <= r + (S2 - S1); the tile runs the
   // blocks up to the one holding its last valid row's last key (blocks masked for every

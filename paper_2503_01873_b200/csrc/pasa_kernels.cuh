@@ -109,7 +109,9 @@ struct FwdParams {
   float inv_s2;           // fl32(1/s2): the block mean S'bar = sum * inv_s2
   int q_bshd;             // Q and O stored BSHD (TMA coordinates, output address)
   int kv_bshd;            // the K / V operands stored BSHD (FA16 mode's raw K, V)
-  int tiles_per_kv;       // group * nq
+  int tiles_per_kv;       // group * (tile_hi - tile_lo): the query tiles computed per kv head
+  int tile_hi;            // one past the last query tile computed (nq; less for a tile range,
+                          // pasa_b200_attention_fwd_tiles: a query-row shard of the problem)
   float inva;             // beta / (1 - beta)       (pasa.cpp:85)
   float qk_scale;         // FA16 mode only: log2(e) / alpha applied after the FP16 store
   const float* vmax;      // per (b, kv head), from the pre-pass (PASA mode: V is pre-scaled)

@@ -1,8 +1,8 @@
 """Multi-GPU partitioning of the PASA forward: one process per GPU, work split
-by (batch, kv-head) -- the reference's own decomposition (pasa.cpp:243-287
-loops over independent (b, h, i) slices) -- with no collective on the data
-path.  Each rank runs the fused kernel on its shard; an optional all-gather
-of O (outside any timed region) reassembles the full output.
+by (batch, kv-head) and, for balance, by query tiles -- the reference's own
+decomposition (pasa.cpp:243-287 loops over independent (b, h, i) slices) -- with
+no collective on the data path.  Each rank runs the fused kernel on its pieces;
+an optional all-gather of O (outside any timed region) reassembles the output.
 
 Every (b, kv head, query tile) is computed by exactly the same kernel code
 whatever the shard, so the gathered O is bit-identical for any world size.
@@ -53,6 +53,72 @@ def _shard_views(q, k, v, start: int, stop: int):
             v.reshape(B * Hkv, 1, S2, d)[start:stop].reshape(1, n, S2, d))
 
 
+@dataclass(frozen=True)
+class Piece:
+    """Query tiles [tile0, tile0 + ntiles) of every unit in [start, stop) (a unit = one (b, kv
+    head) with its Hq / Hkv query heads; a tile = 128 query rows)."""
+    start: int
+    stop: int
+    tile0: int
+    ntiles: int
+
+
+def tile_costs(seq_q: int, seq_kv: int, causal: bool, s2: int = 128) -> list[int]:
+    """Key blocks each 128-row query tile runs (pasa_fwd.cu tile_info): all of them without a
+    mask; causal (bottom-right aligned, row r sees keys <= r + S2 - S1): up to the block of
+    the tile's last row's last key."""
+    nq, nkv, qoff = (seq_q + 127) // 128, seq_kv // s2, seq_kv - seq_q
+    if not causal:
+        return [nkv] * nq
+    return [min((min(seq_q, 128 * (i + 1)) - 1 + qoff) // s2 + 1, nkv) for i in range(nq)]
+
+
+def partition_work(batch: int, heads_kv: int, seq_q: int, seq_kv: int, causal: bool, world: int,
+                   s2: int = 128) -> list[list[Piece]]:
+    """contiguous (b, kv head) ranges first, then query tiles for balance.  The
+    (unit, tile) work items, unit-major, are cut into `world` contiguous runs of equal key-
+    block cost (each item goes to the run holding its cost midpoint), so a problem with
+    fewer units than GPUs (Qwen2-7B: 4 kv heads on 8 GPUs) or with causal tiles of growing
+    cost still balances to within one tile.  A run is at most three pieces: a unit's tail,
+    whole units, a unit's head -- one launch each (pasa_b200_attention_fwd_tiles)."""
+    if world <= 0:
+        raise ValueError("world size must be positive")
+    cost = tile_costs(seq_q, seq_kv, causal, s2)
+    nq, units = len(cost), batch * heads_kv
+    per_unit = sum(cost)
+    total = per_unit * units
+    prefix = [0]
+    for c in cost:
+        prefix.append(prefix[-1] + c)
+
+    def owner(u, i):  # the run holding item (u, i)'s cost midpoint
+        mid2 = 2 * (u * per_unit + prefix[i]) + cost[i]  # twice the midpoint, in integers
+        return min(world - 1, mid2 * world // (2 * total)) if total else 0
+
+    runs: list[list[tuple[int, int]]] = [[] for _ in range(world)]
+    for u in range(units):
+        lo = 0
+        while lo < nq:  # tiles of unit u by owner (owner is monotone in (u, i))
+            r = owner(u, lo)
+            hi = lo
+            while hi < nq and owner(u, hi) == r:
+                hi += 1
+            runs[r].append((u, lo, hi))
+            lo = hi
+    out: list[list[Piece]] = []
+    for items in runs:
+        pieces: list[Piece] = []
+        for u, lo, hi in items:
+            last = pieces[-1] if pieces else None
+            if (last and lo == 0 and hi == nq and last.tile0 == 0 and last.ntiles == nq
+                    and last.stop == u):
+                pieces[-1] = Piece(last.start, u + 1, 0, nq)  # extend a run of whole units
+            else:
+                pieces.append(Piece(u, u + 1, lo, hi - lo))
+        out.append(pieces)
+    return out
+
+
 def _default_compute(q, k, v, **kw):
     from .api import pasa_attention_fwd
     return pasa_attention_fwd(q, k, v, **kw)
@@ -70,6 +136,24 @@ def shard_forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, shard: Shar
     return [(u, o[:, i * g:(i + 1) * g]) for i, u in enumerate(shard.units())]
 
 
+def pieces_forward(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, pieces: list[Piece],
+                   compute: Callable | None = None, **kw) -> list[tuple[int, int, int, torch.Tensor]]:
+    """Run a rank's pieces (one compute call each; a partial tile range passes q_tiles) and
+    return [(unit, row0, row1, O rows)] with O rows (1, Hq/Hkv, row1 - row0, d)."""
+    compute = compute or _default_compute
+    g, S1 = q.shape[1] // k.shape[1], q.shape[2]
+    out = []
+    for pc in pieces:
+        if pc.stop <= pc.start or pc.ntiles <= 0:
+            continue
+        nq = (S1 + 127) // 128
+        part = {} if (pc.tile0 == 0 and pc.ntiles == nq) else {"q_tiles": (pc.tile0, pc.ntiles)}
+        o = compute(*_shard_views(q, k, v, pc.start, pc.stop), **part, **kw)
+        r0, r1 = 128 * pc.tile0, min(S1, 128 * (pc.tile0 + pc.ntiles))
+        out += [(u, r0, r1, o[:, i * g:(i + 1) * g, r0:r1]) for i, u in enumerate(range(pc.start, pc.stop))]
+    return out
+
+
 def pasa_attention_sharded(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
                            group=None, gather: bool = True, compute: Callable | None = None,
                            **kw) -> torch.Tensor | list[tuple[int, torch.Tensor]]:
@@ -82,20 +166,22 @@ def pasa_attention_sharded(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     B, Hq, S1, d = q.shape
     Hkv = k.shape[1]
-    shards = partition(B, Hkv, world)
-    mine = shard_forward(q, k, v, shards[rank], compute, **kw)
+    work = partition_work(B, Hkv, S1, k.shape[2], bool(kw.get("causal", False)), world, kw.get("s2", 128))
+    mine = pieces_forward(q, k, v, work[rank], compute, **kw)
     if not gather:
         return mine
     g = Hq // Hkv
     out = torch.empty_like(q)
-    for u, o in mine:
-        b, h = divmod(u, Hkv)
-        out[b:b + 1, h * g:(h + 1) * g] = o
+
+    def put(lst, dev):
+        for u, r0, r1, o in lst:
+            b, h = divmod(u, Hkv)
+            out[b:b + 1, h * g:(h + 1) * g, r0:r1] = o.to(dev)
+    put(mine, out.device)
     if world > 1:
-        pieces = [None] * world
-        dist.all_gather_object(pieces, [(u, o.cpu()) for u, o in mine], group=group)
-        for lst in pieces:
-            for u, o in lst:
-                b, h = divmod(u, Hkv)
-                out[b:b + 1, h * g:(h + 1) * g] = o.to(out.device)
+        allp = [None] * world
+        dist.all_gather_object(allp, [(u, r0, r1, o.cpu()) for u, r0, r1, o in mine], group=group)
+        for r, lst in enumerate(allp):
+            if r != rank:
+                put(lst, out.device)
     return out

@@ -151,3 +151,14 @@ def test_no_cpu_fallback_without_a_gpu(lib):
     from paper_2503_01873_b200 import pasa_attention_fwd
     with pytest.raises(ValueError, match="CUDA tensors"):
         pasa_attention_fwd(q, q, q)
+
+
+def test_attention_fwd_tiles_range_errors(lib):
+    """pasa_b200_attention_fwd_tiles validates its query-tile range before any device work."""
+    d = _lib.Desc(1, 2, 2, 1000, 1000, 128, 100, 100, 1, 0, 0.984497, math.sqrt(128.0))
+    ws_bytes = lib.pasa_b200_workspace_size(C.byref(d))
+    buf = C.c_void_p(16)  # never dereferenced: the range check comes first
+    for t0, n in [(-1, 2), (0, 9), (8, 1), (3, -1)]:
+        rc = lib.pasa_b200_attention_fwd_tiles(C.byref(d), buf, buf, buf, buf, buf, ws_bytes, t0, n, None)
+        assert rc == _lib.EINVAL, (t0, n)
+        assert b"tile range" in lib.pasa_b200_last_error()

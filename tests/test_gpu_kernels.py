@@ -292,6 +292,41 @@ def test_sharded_bit_identical(dev, orc, world):
     assert torch.equal(out, full)
 
 
+@pytest.mark.parametrize("world,causal,beta", [(8, True, BETA_STAR), (3, True, BETA_STAR), (8, False, BETA_STAR),
+                                               (5, True, 0.0)])
+def test_sharded_query_tiles_bit_identical(dev, orc, world, causal, beta):
+    """SURVEY.md 8e with fewer (b, kv head) units than GPUs (Qwen-like: 4 kv heads on 8):
+    partition_work splits query tiles, each piece is one pasa_b200_attention_fwd_tiles call
+    (pre-pass over every key), and the reassembled O equals the whole call bit for bit
+    (including a ragged last tile, short KV blocks and the FA16 mode)."""
+    from paper_2503_01873_b200 import pasa_attention_fwd
+    from paper_2503_01873_b200.multi import partition_work, pieces_forward
+    S = 1000  # ragged: 8 tiles, the last one 104 rows
+    q, k, v = orc.generate("hybrid", 0.0, 10.0, 23, 1, 8, S, 128, Hkv=4)
+    qt, kt, vt = (torch.from_numpy(x).half().to(dev) for x in (q, k, v))
+    full = pasa_attention_fwd(qt, kt, vt, beta, causal=causal, s1=100, s2=100)
+    out = torch.full_like(full, float("nan"))
+    for pieces in partition_work(1, 4, S, S, causal, world, s2=100):
+        for u, r0, r1, o in pieces_forward(qt, kt, vt, pieces, beta=beta, causal=causal, s1=100, s2=100):
+            out[:, 2 * u:2 * u + 2, r0:r1] = o
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int16), full.view(torch.int16))
+
+
+def test_attention_fwd_tiles_leaves_other_rows(dev):
+    """pasa_b200_attention_fwd_tiles writes exactly its tiles' rows."""
+    from paper_2503_01873_b200 import pasa_attention_fwd
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    q, k, v = (torch.randn(1, 2, 640, 64, device=dev, generator=g).half() for _ in range(3))
+    full = pasa_attention_fwd(q, k, v, causal=True)
+    out = torch.full_like(q, 7.0)
+    pasa_attention_fwd(q, k, v, causal=True, out=out, q_tiles=(1, 3))
+    torch.cuda.synchronize()
+    assert torch.equal(out[:, :, 128:512], full[:, :, 128:512])
+    assert bool((out[:, :, :128] == 7).all()) and bool((out[:, :, 512:] == 7).all())
+
+
 # ----------------------------------------------------------------- FA16 mode (beta = 0)
 
 @pytest.mark.parametrize("case", [("hybrid", 0.0, 10.0, 1, 1, 2, 2, 512, 128, False),

@@ -12,7 +12,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2503_01873_b200.multi import partition, pasa_attention_sharded
+from paper_2503_01873_b200.multi import partition, partition_work, pasa_attention_sharded, tile_costs
 
 
 def test_partition_balanced_and_complete():
@@ -24,7 +24,32 @@ def test_partition_balanced_and_complete():
         assert max(sizes) - min(sizes) <= 1
 
 
-def _model_compute(q, k, v, causal=False):
+@pytest.mark.parametrize("B,H,S,causal,W", [(1, 4, 16384, True, 8), (1, 4, 4096, False, 8), (2, 4, 1024, True, 3),
+                                             (1, 28, 1024, True, 8), (1, 1, 1000, False, 4), (3, 5, 256, False, 4),
+                                             (1, 2, 384, True, 1), (2, 2, 128, True, 8)])
+def test_partition_work_covers_and_balances(B, H, S, causal, W):
+    """(b, kv head) ranges, then query tiles: every (unit, tile) item exactly
+    once, at most three pieces (launches) per rank, loads within one tile's cost."""
+    work = partition_work(B, H, S, S, causal, W)
+    cost = tile_costs(S, S, causal)
+    nq = len(cost)
+    seen = []
+    loads = []
+    for pieces in work:
+        assert len(pieces) <= 3
+        load = 0
+        for pc in pieces:
+            for u in range(pc.start, pc.stop):
+                for i in range(pc.tile0, pc.tile0 + pc.ntiles):
+                    seen.append((u, i))
+                    load += cost[i]
+        loads.append(load)
+    assert sorted(seen) == [(u, i) for u in range(B * H) for i in range(nq)]
+    if B * H * nq >= W:
+        assert max(loads) - min(loads) <= max(cost)
+
+
+def _model_compute(q, k, v, causal=False, q_tiles=None):  # (a tile range: computed whole, sliced by the caller)
     from oracle.oracle import Oracle, Problem
     orc = Oracle()
     o = orc.model_pasa(Problem(q.double().numpy(), k.double().numpy(), v.double().numpy(),
@@ -51,8 +76,10 @@ def _worker(rank, world, port, q, k, v, out_path):
         dist.destroy_process_group()
 
 
-def test_sharded_equals_single_process(tmp_path, orc):
-    q, k, v = orc.generate("hybrid", 3.0, 10.0, 11, 1, 4, 256, 64, Hkv=2)
+@pytest.mark.parametrize("Hkv", [2, 1])
+def test_sharded_equals_single_process(tmp_path, orc, Hkv):
+    # Hkv = 1: one unit for two ranks -> the query tiles are split
+    q, k, v = orc.generate("hybrid", 3.0, 10.0, 11, 1, 4, 256, 64, Hkv=Hkv)
     q, k, v = (torch.from_numpy(x).half() for x in (q, k, v))
     single = _model_compute(q, k, v, causal=True)
     out = str(tmp_path / "o.pt")
