@@ -66,7 +66,7 @@ using namespace sm100;
 
 namespace {
 
-template <int D>
+template <int D, int WS>
 struct PackedCfg {
   static constexpr int NBOX = D / 64;
   static constexpr int BOX_BYTES = kTile * 128;
@@ -76,17 +76,25 @@ struct PackedCfg {
   static constexpr int SMEM_BAR = STAGES * STAGE_BYTES;
   // qk_full, v_full, in_empty, kprep_done, vprep_done, qk_empty [ST]; s/p/t_full, t_empty, aux, mask
   static constexpr int NUM_BARS = 6 * STAGES + 6;
-  // after the barriers: TMEM holder, bad-slot masks [4], slot exponents c0 [4][8], the
-  // prep's per-slot max|V| bits and non-finite slots [9]
-  static constexpr int SMEM_BYTES = SMEM_BAR + 8 * NUM_BARS + 4 * (1 + 4 + 32 + 16) + 1024;
+  // after the barriers: TMEM holder, bad-slot masks [4], slot exponents c0 [4][8], each prep
+  // warpgroup's per-slot max|V| bits and non-finite slots [2][16]
+  static constexpr int SMEM_BYTES = SMEM_BAR + 8 * NUM_BARS + 4 * (1 + 4 + 32 + 32) + 1024;
+  // softmax pairs per thread (NPR): W = 16, 32 -> 16 (the warp's 32 rows span whole slots);
+  // W = 64 -> 32; W = 48 straddles warps -> all 64
+  static constexpr int NPR = WS <= 32 ? 16 : WS == 64 ? 32 : 64;
+  // prep warpgroups: two, alternating stages (tile it on stage it % 2 -> warpgroup it % 2), so
+  // the per-tile pre-pass -- the latency-bound step -- has two tiles' time; one at d = 64,
+  // W = 48, whose all-column softmax leaves no registers for a second
+  static constexpr int NPREP = (D == 64 && WS == 48) ? 1 : 2;
   // warpgroup 0: warp 0 TMA, warp 1 MMA (2, 3 idle); 1: softmax (warps 4-7 = TMEM lane
-  // quadrants 0-3); 2: the per-tile pre-pass (self_prep)
-  static constexpr int THREADS = 384;
-  // setmaxnreg split of the launch allocation (d = 64: 2 CTAs per SM, 80 x 384 = 30720
-  // registers each; d = 128: 1 CTA, 168 x 384)
-  static constexpr int REGS_CTL = D == 64 ? 32 : 40, REGS_PREP = D == 64 ? 56 : 64,
-                       REGS_SM = D == 64 ? 152 : 232;
-  static_assert(128 * (REGS_CTL + REGS_PREP + REGS_SM) <= (D == 64 ? 80 : 168) * THREADS, "registers");
+  // quadrants 0-3); 2, 3: the per-tile pre-pass (self_prep)
+  static constexpr int THREADS = 256 + 128 * NPREP;
+  static constexpr int CTAS = D == 64 ? 2 : 1;  // per SM (shared memory: 2 x 98 KB / 194 KB)
+  // setmaxnreg split of the launch allocation (65536 / (CTAS x THREADS) registers per thread)
+  static constexpr int REGS_CTL = D == 64 ? 32 : 40, REGS_PREP = D == 64 ? (NPREP == 2 ? 40 : 56) : 64,
+                       REGS_SM = D == 64 ? (NPR == 16 ? 88 : NPR == 32 ? 136 : 152) : 232;
+  static constexpr int REGS_LAUNCH = (65536 / (CTAS * THREADS)) & ~7;
+  static_assert(128 * (REGS_CTL + NPREP * REGS_PREP + REGS_SM) <= REGS_LAUNCH * THREADS, "registers");
   static constexpr uint32_t TMEM_COLS = D == 64 ? 256 : 512;
   static constexpr uint32_t T_CLEAN = 128 + D;  // P V' over zeroed poisoned rows
 };
@@ -201,16 +209,16 @@ __device__ __forceinline__ int inflation_nb(int S2, float vmax) {
 template <int D, int WS>
 __device__ __forceinline__ void self_prep_k(uint32_t stage, int N, float dm, float off_s, float lscale, int nseq,
                                             uint32_t vmx_s, uint32_t qk_full, uint32_t parity, long long* trace,
-                                            int trit) {
+                                            int trit, int g) {
   // (the parameters as register arguments: a PackedParams reference would be read from the
   // caller's stack -- local memory -- on every call)
   constexpr int BOX = kTile * 128, TILE = (D / 64) * BOX;
   constexpr int P = 128 / WS, IPT = (P * (D / 2) + 127) / 128;  // column pairs per thread
   const uint32_t kt = stage + TILE;
-  const int tid = threadIdx.x - 256;
+  const int tid = threadIdx.x - 256 - 128 * g;  // (prep warpgroup g)
   if (tid < 9) sptr<unsigned>(vmx_s)[tid] = 0u;  // [0, 8): slot max|V| bits, [8]: non-finite slots
   mbar_wait(qk_full, parity);
-  if (threadIdx.x == 256) PK_TRP(trace, 0, trit, 6);
+  if (threadIdx.x == 256 + 128 * g) PK_TRP(trace, 0, trit, 6);
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     const int e = tid + 128 * i;
@@ -251,9 +259,9 @@ __device__ __forceinline__ void self_prep_k(uint32_t stage, int N, float dm, flo
       }
     }
   }
-  if (threadIdx.x == 256) PK_TRP(trace, 1, trit, 8);
+  if (threadIdx.x == 256 + 128 * g) PK_TRP(trace, 1, trit, 8);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // K' for the tensor core
-  named_bar_sync(1, 128);
+  named_bar_sync(1 + g, 128);
 }
 
 // V side, once V has landed: max|V| and the non-finite check per slot, c0, V' in the (rare)
@@ -262,14 +270,14 @@ __device__ __forceinline__ void self_prep_k(uint32_t stage, int N, float dm, flo
 template <int D, int WS>
 __device__ __forceinline__ void self_prep_v(uint32_t stage, int N, int nseq, uint32_t c0_s, uint32_t vmx_s,
                                             uint32_t bad_s, uint32_t v_full, uint32_t parity, long long* trace,
-                                            int trit) {
+                                            int trit, int g) {
   constexpr int BOX = kTile * 128, TILE = (D / 64) * BOX;
   constexpr int P = 128 / WS, IPT = (P * (D / 2) + 127) / 128;
   const uint32_t vt = stage + 2 * TILE;
   unsigned* vmx = sptr<unsigned>(vmx_s);
-  const int tid = threadIdx.x - 256;
+  const int tid = threadIdx.x - 256 - 128 * g;  // (prep warpgroup g)
   mbar_wait(v_full, parity);
-  if (threadIdx.x == 256) PK_TRP(trace, 1, trit, 9);
+  if (threadIdx.x == 256 + 128 * g) PK_TRP(trace, 1, trit, 9);
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     const int e = tid + 128 * i;
@@ -293,8 +301,8 @@ __device__ __forceinline__ void self_prep_v(uint32_t stage, int N, int nseq, uin
       if (__hisnan(__low2half(nf2)) || __hisnan(__high2half(nf2))) atomicOr(vmx + 8, 1u << sl);
     }
   }
-  named_bar_sync(1, 128);  // every slot's max|V| and the non-finite slots are in
-  if (threadIdx.x == 256) PK_TRP(trace, 1, trit, 10);
+  named_bar_sync(1 + g, 128);  // every slot's max|V| and the non-finite slots are in
+  if (threadIdx.x == 256 + 128 * g) PK_TRP(trace, 1, trit, 10);
   // V' = V fl16(2^-c0): only in the (rare) tiles where some slot needs it
   int cz[IPT];
   bool any = false;
@@ -321,8 +329,8 @@ __device__ __forceinline__ void self_prep_v(uint32_t stage, int N, int nseq, uin
   if (tid < 8) sptr<int>(c0_s)[tid] = tid < nseq ? inflation_nb(N, __uint_as_float(vmx[tid])) : 0;
   if (tid == 0) *sptr<uint32_t>(bad_s) = vmx[8];
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // V' for the tensor core
-  named_bar_sync(1, 128);
-  if (threadIdx.x == 256) PK_TRP(trace, 1, trit, 11);
+  named_bar_sync(1 + g, 128);
+  if (threadIdx.x == 256 + 128 * g) PK_TRP(trace, 1, trit, 11);
 }
 
 // One tile: the K side, kprep_done (the MMA warp may issue S'), then the V side.  (One
@@ -331,22 +339,22 @@ template <int D, int WS>
 __device__ __noinline__ void self_prep_stage(uint32_t stage, int N, float dm, float off_s, float lscale, int nseq,
                                              uint32_t c0_s, uint32_t vmx_s, uint32_t bad_s, uint32_t qk_full,
                                              uint32_t v_full, uint32_t kprep_done, uint32_t parity,
-                                             long long* trace, int trit) {
-  self_prep_k<D, WS>(stage, N, dm, off_s, lscale, nseq, vmx_s, qk_full, parity, trace, trit);
-  if (threadIdx.x == 256) mbar_arrive(kprep_done);
-  self_prep_v<D, WS>(stage, N, nseq, c0_s, vmx_s, bad_s, v_full, parity, trace, trit);
+                                             long long* trace, int trit, int g) {
+  self_prep_k<D, WS>(stage, N, dm, off_s, lscale, nseq, vmx_s, qk_full, parity, trace, trit, g);
+  if (threadIdx.x == 256 + 128 * g) mbar_arrive(kprep_done);
+  self_prep_v<D, WS>(stage, N, nseq, c0_s, vmx_s, bad_s, v_full, parity, trace, trit, g);
 }
 
 }  // namespace
 
 // Persistent: CTA b processes tiles b, b + gridDim.x, ...; the loads of the next tile run
 // in the second stage while the current one is computed.
-template <int D, int MODE>
-__global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
+template <int D, int MODE, int WS>
+__global__ void __launch_bounds__(PackedCfg<D, WS>::THREADS, PackedCfg<D, WS>::CTAS)
     pasa_fwd_packed_kernel(const __grid_constant__ CUtensorMap tm_q,
                            const __grid_constant__ CUtensorMap tm_kp,
                            const __grid_constant__ CUtensorMap tm_v, const PackedParams p) {
-  using Cfg = PackedCfg<D>;
+  using Cfg = PackedCfg<D, WS>;
   constexpr int ST = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sb = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -367,10 +375,10 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
   // per tile it, slot it & 3: written up to two tiles ahead of the epilogue that reads it
   volatile uint32_t* bad_mask = tmem_holder + 1;                 // [4]
   int* c0s = reinterpret_cast<int*>(tmem_holder + 5);            // [4][8]
-  unsigned* vmx = reinterpret_cast<unsigned*>(c0s + 32);         // [9] (prep scratch)
+  unsigned* vmx = reinterpret_cast<unsigned*>(c0s + 32);         // [NPREP][16] (prep scratch)
   const int warp = static_cast<int>(warp_id());
   const int lane = threadIdx.x & 31;
-  const int W = p.W;                                // slot stride (rows / keys)
+  constexpr int W = WS;                             // slot stride (rows / keys) = p.W
   const int ntiles = (p.BH + p.P - 1) / p.P;
 
   if (threadIdx.x == 0) {
@@ -562,9 +570,7 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
       // The pair index keeps its tile position (chain i & 3, mask range_keep(i, lo, hi)),
       // so the row's sums are the same FP32 chains as over all 128 columns.
       // (W = 16, 32: 32 columns; W = 64: 64; W = 48 straddles -- all 128)
-      const float l = W <= 32  ? row_softmax<16, MODE>(t_s, quad, lo, hi, p.qk_scale)
-                      : W == 64 ? row_softmax<32, MODE>(t_s, quad, lo, hi, p.qk_scale)
-                                : row_softmax<64, MODE>(t_s, quad, lo, hi, p.qk_scale);
+      const float l = row_softmax<Cfg::NPR, MODE>(t_s, quad, lo, hi, p.qk_scale);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -619,28 +625,21 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::REGS_PREP));
     // ---- the pre-pass of every tile (self_prep), as soon as its stage has landed: runs
     // ahead of the softmax, which it never waits for (the MMA warp waits for kprep_done before
-    // S' and for vprep_done before P V')
-    int it = 0;
-    for (int tile = blockIdx.x; self_prep && tile < ntiles; tile += gridDim.x, ++it) {
+    // S' and for vprep_done before P V').  Prep warpgroup g takes the tiles it with
+    // it % NPREP == g (with two: always stage g).
+    const int g = (warp - 8) / 4;
+    const uint32_t lead = 256 + 128 * g;  // the warpgroup's first thread
+    int it = g;
+    for (int tile = blockIdx.x + g * gridDim.x; self_prep && tile < ntiles;
+         tile += Cfg::NPREP * gridDim.x, it += Cfg::NPREP) {
       const int st = it % ST;
-      if (threadIdx.x == 256) PK_TR(1, it, 5);
-      const uint32_t stg = sb + st * Cfg::STAGE_BYTES, c0a = smem_u32(c0s + 8 * (it & 3)), vma = smem_u32(vmx),
-                     bada = smem_u32(const_cast<uint32_t*>(bad_mask) + (it & 3));
-      const int ns = min(p.P, p.BH - tile * p.P);
-      const uint32_t par = (it / ST) & 1;
-      // the slot width as a compile-time row count (straight-line pre-pass)
-#define PK_PREP(WS)                                                                                  \
-  self_prep_stage<D, WS>(stg, p.N, p.dm, p.off, p.lscale, ns, c0a, vma, bada, qk_full + 8 * st, v_full + 8 * st, \
-                         kprep_done + 8 * st, par, p.trace, it)
-      switch (W) {
-        case 16: PK_PREP(16); break;
-        case 32: PK_PREP(32); break;
-        case 48: PK_PREP(48); break;
-        default: PK_PREP(64); break;
-      }
-#undef PK_PREP
-      if (threadIdx.x == 256) mbar_arrive(vprep_done + 8 * st);  // (after the prep's last barrier)
-      if (threadIdx.x == 256) PK_TR(1, it, 6);
+      if (threadIdx.x == lead) PK_TR(1, it, 5);
+      self_prep_stage<D, WS>(sb + st * Cfg::STAGE_BYTES, p.N, p.dm, p.off, p.lscale, min(p.P, p.BH - tile * p.P),
+                             smem_u32(c0s + 8 * (it & 3)), smem_u32(vmx + 16 * g),
+                             smem_u32(const_cast<uint32_t*>(bad_mask) + (it & 3)), qk_full + 8 * st, v_full + 8 * st,
+                             kprep_done + 8 * st, (it / ST) & 1, p.trace, it, g);
+      if (threadIdx.x == lead) mbar_arrive(vprep_done + 8 * st);  // (after the prep's last barrier)
+      if (threadIdx.x == lead) PK_TR(1, it, 6);
     }
   }
   tc_fence_before();
@@ -649,31 +648,43 @@ __global__ void __launch_bounds__(PackedCfg<D>::THREADS, D == 64 ? 2 : 1)
   if (warp == 0) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
 }
 
-template <int D, int MODE>
+template <int D, int MODE, int WS>
 static cudaError_t launch_packed_t(const CUtensorMap& tq, const CUtensorMap& tk,
                                    const CUtensorMap& tv, const PackedParams& p,
                                    cudaStream_t stream) {
-  using Cfg = PackedCfg<D>;
-  cudaError_t e = cudaFuncSetAttribute(pasa_fwd_packed_kernel<D, MODE>,
+  using Cfg = PackedCfg<D, WS>;
+  cudaError_t e = cudaFuncSetAttribute(pasa_fwd_packed_kernel<D, MODE, WS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int tiles = (p.BH + p.P - 1) / p.P;  // p.P = 128 / p.W sequences per tile
   const int sms = current_sm_count();  // the launching (current) device
-  int per_sm = D == 64 ? 2 : 1;  // shared memory: 2 x 98 KB (d = 64), 194 KB (d = 128)
+  int per_sm = Cfg::CTAS;
 #ifdef PASA_TRACE
   if (getenv("PASA_PACKED_PER_SM")) per_sm = atoi(getenv("PASA_PACKED_PER_SM"));  // (profiling)
 #endif
   const int grid = tiles < per_sm * sms ? tiles : per_sm * sms;
-  pasa_fwd_packed_kernel<D, MODE><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(tq, tk, tv, p);
+  pasa_fwd_packed_kernel<D, MODE, WS><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(tq, tk, tv, p);
   return cudaGetLastError();
+}
+
+template <int D, int MODE>
+static cudaError_t launch_packed_w(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                                   const PackedParams& p, cudaStream_t stream) {
+  switch (p.W) {  // the slot width as a compile-time row count
+    case 16: return launch_packed_t<D, MODE, 16>(tq, tk, tv, p, stream);
+    case 32: return launch_packed_t<D, MODE, 32>(tq, tk, tv, p, stream);
+    case 48: return launch_packed_t<D, MODE, 48>(tq, tk, tv, p, stream);
+    case 64: return launch_packed_t<D, MODE, 64>(tq, tk, tv, p, stream);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_fwd_packed(int D, int mode, const CUtensorMap& tq, const CUtensorMap& tk,
                               const CUtensorMap& tv, const PackedParams& p, cudaStream_t stream) {
-  if (D == 64) return mode == kModePasa ? launch_packed_t<64, kModePasa>(tq, tk, tv, p, stream)
-                                        : launch_packed_t<64, kModeFa16>(tq, tk, tv, p, stream);
-  if (D == 128) return mode == kModePasa ? launch_packed_t<128, kModePasa>(tq, tk, tv, p, stream)
-                                         : launch_packed_t<128, kModeFa16>(tq, tk, tv, p, stream);
+  if (D == 64) return mode == kModePasa ? launch_packed_w<64, kModePasa>(tq, tk, tv, p, stream)
+                                        : launch_packed_w<64, kModeFa16>(tq, tk, tv, p, stream);
+  if (D == 128) return mode == kModePasa ? launch_packed_w<128, kModePasa>(tq, tk, tv, p, stream)
+                                         : launch_packed_w<128, kModeFa16>(tq, tk, tv, p, stream);
   return cudaErrorInvalidValue;
 }
 

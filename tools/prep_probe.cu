@@ -14,7 +14,7 @@ using namespace pasa_b200;
 
 template <int D>
 __global__ void __launch_bounds__(384, 1) prep_probe(PackedParams p, int iters) {
-  using Cfg = PackedCfg<D>;
+  using Cfg = PackedCfg<D, 32>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sb = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem = smem_raw + (sb - smem_u32(smem_raw));
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(384, 1) prep_probe(PackedParams p, int iters) 
         PK_TR(1, it, 5);
       }
       self_prep_stage<D, 32>(sb, p.N, p.dm, p.off, p.lscale, nseq, smem_u32(c0s), smem_u32(vmx),
-                             smem_u32(const_cast<uint32_t*>(bad)), in_full, in_full, kdone, it & 1, p.trace, it);
+                             smem_u32(const_cast<uint32_t*>(bad)), in_full, in_full, kdone, it & 1, p.trace, it, 0);
       if (threadIdx.x == 256) PK_TR(1, it, 6);
     }
   }
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(384, 1) prep_probe(PackedParams p, int iters) 
 int main(int argc, char** argv) {
   const int ctas = argc > 1 ? atoi(argv[1]) : 1;
   constexpr int D = 64;
-  using Cfg = PackedCfg<D>;
+  using Cfg = PackedCfg<D, 32>;
   PackedParams p{};
   p.N = 25;
   p.W = 32;
