@@ -26,7 +26,8 @@ cudaError_t launch_kprep(const KprepParams& p, int B, int Hkv, cudaStream_t stre
 cudaError_t launch_vscale(const VscaleParams& p, cudaStream_t stream);
 cudaError_t launch_ksum(const void* kp, void* ks, int BH, int S2, int s2, int D, cudaStream_t stream);
 cudaError_t launch_fwd_packed(int D, int mode, const CUtensorMap& tq, const CUtensorMap& tk,
-                              const CUtensorMap& tv, const PackedParams& p, cudaStream_t stream);
+                              const CUtensorMap& tv, const CUtensorMap& to, const PackedParams& p,
+                              cudaStream_t stream);
 cudaError_t launch_fwd(int D, bool causal, int mode, const CUtensorMap& tq, const CUtensorMap& tk,
                        const CUtensorMap& tv, const CUtensorMap& tks, const CUtensorMap& to,
                        const FwdParams& p, cudaStream_t stream);
@@ -399,6 +400,8 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
     if ((rc = make_tmap(&tq, q, d->head_dim, rows, 1, n))) return rc;
     if ((rc = make_tmap(&tk, keys, d->head_dim, rows, 1, n))) return rc;
     if ((rc = make_tmap(&tv, v, d->head_dim, rows, 1, n))) return rc;
+    CUtensorMap tom;  // O: stored by TMA from the staged tile, one box of N rows per sequence
+    if ((rc = make_tmap(&tom, o, d->head_dim, rows, 1, n))) return rc;
     PackedParams pp{};
     pp.BH = bh;
     pp.N = n;
@@ -416,7 +419,7 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
       pp.off = __half2float(of);
       pp.lscale = static_cast<float>(0.5 * kLog2e);  // the fused path's K' carries log2(e)/2
     }
-    cudaError_t e = launch_fwd_packed(d->head_dim, mode, tq, tk, tv, pp, static_cast<cudaStream_t>(stream));
+    cudaError_t e = launch_fwd_packed(d->head_dim, mode, tq, tk, tv, tom, pp, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "pasa_fwd_packed launch");
     return PASA_B200_OK;
   }

@@ -74,8 +74,9 @@ struct PackedCfg {
   static constexpr int STAGE_BYTES = 3 * TILE_BYTES;  // Q, K', V' of one tile
   static constexpr int STAGES = 2;
   static constexpr int SMEM_BAR = STAGES * STAGE_BYTES;
-  // qk_full, v_full, in_empty, kprep_done, vprep_done, qk_empty [ST]; s/p/t_full, t_empty, aux, mask
-  static constexpr int NUM_BARS = 6 * STAGES + 6;
+  // qk_full, v_full, in_empty, kprep_done, vprep_done, qk_empty, o_free [ST]; s/p/t_full,
+  // t_empty, aux, mask
+  static constexpr int NUM_BARS = 7 * STAGES + 6;
   // after the barriers: TMEM holder, bad-slot masks [4], slot exponents c0 [4][8], each prep
   // warpgroup's per-slot max|V| bits and non-finite slots [2][16]
   static constexpr int SMEM_BYTES = SMEM_BAR + 8 * NUM_BARS + 4 * (1 + 4 + 32 + 32) + 1024;
@@ -353,7 +354,8 @@ template <int D, int MODE, int WS>
 __global__ void __launch_bounds__(PackedCfg<D, WS>::THREADS, PackedCfg<D, WS>::CTAS)
     pasa_fwd_packed_kernel(const __grid_constant__ CUtensorMap tm_q,
                            const __grid_constant__ CUtensorMap tm_kp,
-                           const __grid_constant__ CUtensorMap tm_v, const PackedParams p) {
+                           const __grid_constant__ CUtensorMap tm_v,
+                           const __grid_constant__ CUtensorMap tm_o, const PackedParams p) {
   using Cfg = PackedCfg<D, WS>;
   constexpr int ST = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -370,6 +372,7 @@ __global__ void __launch_bounds__(PackedCfg<D, WS>::THREADS, PackedCfg<D, WS>::C
   const uint32_t vprep_done = kprep_done + 8 * ST;  // [ST] self_prep: ... and V', c0, the mask
   const uint32_t qk_empty = vprep_done + 8 * ST;  // [ST]: the stage's S' MMA has read Q and K'
   // (in_empty: its P V' has read V' -- the Q / K' half of a stage refills a PV earlier)
+  const uint32_t o_free = qk_empty + 8 * ST;  // [ST]: the O tile staged in its V' buffer is stored
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + Cfg::SMEM_BAR + 8 * Cfg::NUM_BARS);
   // [it % 2]: bit s = slot s of tile it holds a non-finite V' row
   // per tile it, slot it & 3: written up to two tiles ahead of the epilogue that reads it
@@ -389,6 +392,7 @@ __global__ void __launch_bounds__(PackedCfg<D, WS>::THREADS, PackedCfg<D, WS>::C
       mbar_init(qk_empty + 8 * st, 1);
       mbar_init(kprep_done + 8 * st, 1);
       mbar_init(vprep_done + 8 * st, 1);
+      mbar_init(o_free + 8 * st, 1);
     }
     mbar_init(s_full, 1);
     mbar_init(p_full, 4);
@@ -438,6 +442,7 @@ __global__ void __launch_bounds__(PackedCfg<D, WS>::THREADS, PackedCfg<D, WS>::C
         }
         PK_TR(1, it, 3);
         mbar_wait(in_empty + 8 * st, ((it / ST) & 1) ^ 1);
+        mbar_wait(o_free + 8 * st, ((it / ST) & 1) ^ 1);  // the V buffer also stages O
         mbar_expect_tx(v_full + 8 * st, Cfg::NBOX * nseq * p.N * 128);
         for (int sl = 0; sl < nseq; ++sl) {
           const int r = (seq0 + sl) * p.N;
@@ -511,6 +516,17 @@ __global__ void __launch_bounds__(PackedCfg<D, WS>::THREADS, PackedCfg<D, WS>::C
       if (leader) {
         if (!self_prep) bad_mask[it & 3] = bad;
         mbar_arrive(mask_full);
+      }
+      if (nseq < p.P) {
+        // a ragged tile: its unused slots hold an earlier tile's staged O (possibly non-finite),
+        // and P = 0 there multiplies them -- zero those V' rows first
+        for (int e = lane; e < (p.P - nseq) * W * Cfg::NBOX * 8; e += 32) {
+          const int r = nseq * W + e / (Cfg::NBOX * 8), bx = (e / 8) % Cfg::NBOX, c = e % 8;
+          *reinterpret_cast<uint4*>(smem + (vbase - sb) + bx * Cfg::BOX_BYTES + r * 128 + c * 16) =
+              make_uint4(0, 0, 0, 0);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
       }
       mbar_wait(t_empty, (it & 1) ^ 1);
       tc_fence_after();
@@ -607,7 +623,11 @@ __global__ void __launch_bounds__(PackedCfg<D, WS>::THREADS, PackedCfg<D, WS>::C
       __syncwarp();
       if (lane == 0) mbar_arrive(t_empty);
       if (tr0) PK_TR(0, it, 5);
-      uint16_t* dst = p.out + (static_cast<long long>(seq0 + sl) * p.N + rr) * D;
+      // O rows staged in the stage's V' buffer (P V' has read it: t_full), SW128 like the loads
+      // (slot rows start at multiples of 8, so the 16-byte chunk of row r sits at c ^ r % 8),
+      // then one TMA store of N rows per sequence and 64-column box.  Gap rows and unused
+      // slots are not written (the MMA warp zeroes a ragged tile's unused slots before P V').
+      const uint32_t vst = sb + st * Cfg::STAGE_BYTES + 2 * Cfg::TILE_BYTES;
 #pragma unroll
       for (int i = 0; i < D / 2; i += 4) {
         uint32_t w[4];
@@ -617,7 +637,20 @@ __global__ void __launch_bounds__(PackedCfg<D, WS>::THREADS, PackedCfg<D, WS>::C
           const __half c = __float2half_rn(__fmul_rn(hi_f(tv[i + k]), inv_l));
           w[k] = h2_as_u32(__halves2half2(a, c));
         }
-        if (row_ok) *reinterpret_cast<uint4*>(dst + 2 * i) = make_uint4(w[0], w[1], w[2], w[3]);
+        const int col = 2 * i, chunk = (col % 64) / 8;
+        const uint32_t a = vst + (col / 64) * Cfg::BOX_BYTES + row * 128 + ((chunk ^ (row & 7)) << 4);
+        if (row_ok)
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+                       "r"(w[3]) : "memory");
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // O for the TMA engine
+      named_bar_sync(3, 128);
+      if (tr0) {
+        for (int s2 = 0; s2 < nseq; ++s2)
+          for (int bx = 0; bx < Cfg::NBOX; ++bx)
+            tma_store_3d(&tm_o, vst + bx * Cfg::BOX_BYTES + s2 * W * 128, bx * 64, (seq0 + s2) * p.N, 0);
+        tma_store_commit_wait_read();
+        mbar_arrive(o_free + 8 * st);
       }
       if (tr0) PK_TR(0, it, 3);
     }
@@ -650,7 +683,7 @@ __global__ void __launch_bounds__(PackedCfg<D, WS>::THREADS, PackedCfg<D, WS>::C
 
 template <int D, int MODE, int WS>
 static cudaError_t launch_packed_t(const CUtensorMap& tq, const CUtensorMap& tk,
-                                   const CUtensorMap& tv, const PackedParams& p,
+                                   const CUtensorMap& tv, const CUtensorMap& to, const PackedParams& p,
                                    cudaStream_t stream) {
   using Cfg = PackedCfg<D, WS>;
   cudaError_t e = cudaFuncSetAttribute(pasa_fwd_packed_kernel<D, MODE, WS>,
@@ -663,28 +696,29 @@ static cudaError_t launch_packed_t(const CUtensorMap& tq, const CUtensorMap& tk,
   if (getenv("PASA_PACKED_PER_SM")) per_sm = atoi(getenv("PASA_PACKED_PER_SM"));  // (profiling)
 #endif
   const int grid = tiles < per_sm * sms ? tiles : per_sm * sms;
-  pasa_fwd_packed_kernel<D, MODE, WS><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(tq, tk, tv, p);
+  pasa_fwd_packed_kernel<D, MODE, WS><<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, stream>>>(tq, tk, tv, to, p);
   return cudaGetLastError();
 }
 
 template <int D, int MODE>
 static cudaError_t launch_packed_w(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                                   const PackedParams& p, cudaStream_t stream) {
+                                   const CUtensorMap& to, const PackedParams& p, cudaStream_t stream) {
   switch (p.W) {  // the slot width as a compile-time row count
-    case 16: return launch_packed_t<D, MODE, 16>(tq, tk, tv, p, stream);
-    case 32: return launch_packed_t<D, MODE, 32>(tq, tk, tv, p, stream);
-    case 48: return launch_packed_t<D, MODE, 48>(tq, tk, tv, p, stream);
-    case 64: return launch_packed_t<D, MODE, 64>(tq, tk, tv, p, stream);
+    case 16: return launch_packed_t<D, MODE, 16>(tq, tk, tv, to, p, stream);
+    case 32: return launch_packed_t<D, MODE, 32>(tq, tk, tv, to, p, stream);
+    case 48: return launch_packed_t<D, MODE, 48>(tq, tk, tv, to, p, stream);
+    case 64: return launch_packed_t<D, MODE, 64>(tq, tk, tv, to, p, stream);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_fwd_packed(int D, int mode, const CUtensorMap& tq, const CUtensorMap& tk,
-                              const CUtensorMap& tv, const PackedParams& p, cudaStream_t stream) {
-  if (D == 64) return mode == kModePasa ? launch_packed_w<64, kModePasa>(tq, tk, tv, p, stream)
-                                        : launch_packed_w<64, kModeFa16>(tq, tk, tv, p, stream);
-  if (D == 128) return mode == kModePasa ? launch_packed_w<128, kModePasa>(tq, tk, tv, p, stream)
-                                         : launch_packed_w<128, kModeFa16>(tq, tk, tv, p, stream);
+                              const CUtensorMap& tv, const CUtensorMap& to, const PackedParams& p,
+                              cudaStream_t stream) {
+  if (D == 64) return mode == kModePasa ? launch_packed_w<64, kModePasa>(tq, tk, tv, to, p, stream)
+                                        : launch_packed_w<64, kModeFa16>(tq, tk, tv, to, p, stream);
+  if (D == 128) return mode == kModePasa ? launch_packed_w<128, kModePasa>(tq, tk, tv, to, p, stream)
+                                         : launch_packed_w<128, kModeFa16>(tq, tk, tv, to, p, stream);
   return cudaErrorInvalidValue;
 }
 
