@@ -409,7 +409,6 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
     pp.P = kTile / pp.W;
     pp.qk_scale = static_cast<float>(kLog2e / d->alpha);
     pp.vmax = vmax;
-    pp.out = static_cast<uint16_t*>(o);
     pp.trace = g_trace;
     if (self_prep && mode == kModePasa) {
       __half dg, of;
@@ -462,7 +461,6 @@ static int launch_forward(const pasa_b200_desc* d, int mode, const void* q, cons
   p.inva = static_cast<float>(d->beta / (1.0 - d->beta));  // pasa.cpp:85
   p.qk_scale = static_cast<float>(kLog2e / d->alpha);
   p.vmax = vmax;
-  p.out = static_cast<uint16_t*>(o);
   p.trace = g_trace;
   p.diag = diag;
   p.diag_scale = mode == kModePasa ? static_cast<float>(2.0 / kLog2e) : 1.0f;

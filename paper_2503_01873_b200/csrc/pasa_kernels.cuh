@@ -115,7 +115,7 @@ struct FwdParams {
   float inva;             // beta / (1 - beta)       (pasa.cpp:85)
   float qk_scale;         // FA16 mode only: log2(e) / alpha applied after the FP16 store
   const float* vmax;      // per (b, kv head), from the pre-pass (PASA mode: V is pre-scaled)
-  uint16_t* out;          // (B, Hq, S1, D) fp16
+  // (O: stored by TMA through the kernel's tm_o map, Q's shape and layout)
   void* diag;             // optional device pasa_b200_diag (RunDiagnostics); nullptr = off
   float diag_scale;       // stored score -> reference units (PASA: 2/log2(e); FA16: 1)
   long long* trace;       // PASA_TRACE builds only: clock64 timeline (see pasa_fwd.cu)
@@ -142,7 +142,7 @@ struct PackedParams {
   int BH, N, W, P;
   float qk_scale;         // FA16 mode: log2(e) / alpha
   const float* vmax;      // PASA, prepped inputs: per sequence, from the pre-pass (V' = V 2^-c0)
-  uint16_t* out;
+  // (O: stored by TMA through the kernel's tm_o map)
   // PASA, self_prep = 1: the kernel reads raw K and V and runs the pre-pass per tile in shared
   // memory -- K' = fl16(fl32(fma(dm, K, fl32(off colsum))) lscale) (pasa_kprep_rank1_small
   // _kernel's arithmetic), max|V| and V' = V 2^-c0 per sequence (pasa_vscale_kernel's)
