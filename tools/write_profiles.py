@@ -67,7 +67,7 @@ def main():
     open(os.path.join(P, f"{tag}_ncu_packed_summary.txt"), "w").write(
         f"# ncu --set full --clock-control none --import-source on -k regex:packed -s 2 -c 1 (B200, {tag})\n"
         "# command: python tools/ncu_once.py --shape temporal  (B=9216, H=5, N=25, d=64: the SVD temporal attention)\n"
-        "# kernel: pasa_fwd_packed_kernel<64, PASA> with the pre-pass fused (self_prep): reads Q, K, V, writes O\n"
+        "# kernel: pasa_fwd_packed_kernel<64, PASA, W = 32> with the pre-pass fused (self_prep): reads Q, K, V, writes O\n"
         + sp + "# memory-bound: algorithmic bytes 4 x 147.5 MB per launch\n")
     num = lambda key: float(re.search(re.escape(key) + r"\s+\S+\s+([\d.]+)", s128).group(1))  # noqa: E731
     rd, wr = num("dram__bytes_read.sum") * 1e6, num("dram__bytes_write.sum") * 1e6
