@@ -224,7 +224,9 @@ __device__ __forceinline__ void self_prep_k(uint32_t stage, int N, float dm, flo
   for (int i = 0; i < IPT; ++i) {
     const int e = tid + 128 * i;
     const bool live = e < nseq * (D / 2);
-    const int sl = e / (D / 2), cp = e % (D / 2);
+    // (items past the live ones still load -- straight-line code -- so their slot is clamped
+    // into the tile: with P = 2 slots, threads 64-127 would otherwise read past the stage)
+    const int sl = min(e / (D / 2), P - 1), cp = e % (D / 2);
     const int col = 2 * cp, ck = (col % 64) / 8;
     // row c of the slot: swizzle key c % 8 (slots start at multiples of 8): a constant offset
     const uint32_t cb = kt + (col / 64) * BOX + (col % 8) * 2 + sl * WS * 128;
@@ -282,7 +284,7 @@ __device__ __forceinline__ void self_prep_v(uint32_t stage, int N, int nseq, uin
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     const int e = tid + 128 * i;
-    const int sl = e / (D / 2), cp = e % (D / 2), col = 2 * cp, ck = (col % 64) / 8;
+    const int sl = min(e / (D / 2), P - 1), cp = e % (D / 2), col = 2 * cp, ck = (col % 64) / 8;
     const uint32_t cb = vt + (col / 64) * BOX + (col % 8) * 2 + sl * WS * 128;
     __half2 vm2 = __float2half2_rn(0.f), nf2 = vm2;
 #pragma unroll
@@ -317,7 +319,7 @@ __device__ __forceinline__ void self_prep_v(uint32_t stage, int N, int nseq, uin
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
       const int e = tid + 128 * i;
-      const int sl = e / (D / 2), cp = e % (D / 2), col = 2 * cp, ck = (col % 64) / 8;
+      const int sl = min(e / (D / 2), P - 1), cp = e % (D / 2), col = 2 * cp, ck = (col % 64) / 8;
       const __half2 sc = __half2half2(__float2half_rn(ldexpf(1.0f, -cz[i])));
       const uint32_t cb = vt + (col / 64) * BOX + (col % 8) * 2 + sl * WS * 128;
 #pragma unroll

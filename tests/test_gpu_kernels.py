@@ -885,3 +885,25 @@ def test_packed_self_prep_matches_prepped(dev, N, D, vamp):
     torch.cuda.synchronize()
     assert bool(torch.isfinite(fused).all())
     assert torch.equal(fused.view(torch.int16), o.view(torch.int16))
+
+
+@pytest.mark.parametrize("N,D", [(25, 64), (16, 128), (40, 64), (64, 64)])
+def test_packed_repeatable(dev, N, D):
+    """Race canary for the packed kernel's warp-specialised pipeline (two prep warpgroups,
+    O staged in the consumed V' buffer, ragged last tile): 12 launches on the same inputs,
+    including a non-finite V, must give identical bits every time."""
+    from paper_2503_01873_b200 import pasa_attention_fwd
+    g = torch.Generator(device=dev)
+    g.manual_seed(N + D)
+    B, H = 301, 5  # 1505 sequences: many tiles per CTA, ragged last tile
+    q, k, v = (torch.randn(B, H, N, D, device=dev, generator=g).half() for _ in range(3))
+    v[17, 3, N // 2, 5] = float("nan")
+    first = pasa_attention_fwd(q, k, v, BETA_STAR, s1=N, s2=N)
+    for _ in range(11):
+        again = pasa_attention_fwd(q, k, v, BETA_STAR, s1=N, s2=N)
+        assert torch.equal(again.view(torch.int16), first.view(torch.int16))
+    torch.cuda.synchronize()
+    bad = torch.zeros(B * H, dtype=torch.bool, device=dev)
+    bad[17 * H + 3] = True
+    fin = torch.isfinite(first.view(B * H, -1)).all(dim=1)
+    assert bool(fin[~bad].all())  # the NaN stays in its own sequence
