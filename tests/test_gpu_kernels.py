@@ -864,7 +864,7 @@ def test_packed_self_prep_matches_prepped(dev, N, D, vamp):
     L = _lib.load()
     g = torch.Generator(device=dev)
     g.manual_seed(N * D)
-    B, H = 3, 37  # 111 sequences: ragged last tile
+    B, H = 3, 401  # 1203 sequences: ragged last tile, several tiles per CTA at every slot width
     q = torch.randn(B, H, N, D, device=dev, generator=g).half()
     k = (torch.randn(B, H, N, D, device=dev, generator=g) * 4).half()
     v = torch.randn(B, H, N, D, device=dev, generator=g)
@@ -887,7 +887,7 @@ def test_packed_self_prep_matches_prepped(dev, N, D, vamp):
     assert torch.equal(fused.view(torch.int16), o.view(torch.int16))
 
 
-@pytest.mark.parametrize("N,D", [(25, 64), (16, 128), (40, 64), (64, 64)])
+@pytest.mark.parametrize("N,D", [(25, 64), (16, 128), (40, 64), (64, 64), (48, 128), (9, 64)])
 def test_packed_repeatable(dev, N, D):
     """Race canary for the packed kernel's warp-specialised pipeline (two prep warpgroups,
     O staged in the consumed V' buffer, ragged last tile): 12 launches on the same inputs,
