@@ -907,3 +907,35 @@ def test_packed_repeatable(dev, N, D):
     bad[17 * H + 3] = True
     fin = torch.isfinite(first.view(B * H, -1)).all(dim=1)
     assert bool(fin[~bad].all())  # the NaN stays in its own sequence
+
+
+@pytest.mark.parametrize("shape", [
+    # B, Hq, Hkv, S1, S2, d, s1, s2, causal
+    (1, 4, 2, 1, 1, 128, 1, 1, False),        # one query row, one key
+    (2, 3, 3, 1, 300, 64, 1, 100, True),      # decode-like: one row after 300 cached keys
+    (1, 8, 1, 129, 129, 128, 129, 129, False),  # s2 = 129 > 128: rejected cleanly
+    (1, 8, 1, 129, 129, 128, 129, 43, False),  # S = 129: a 128-row tile + a 1-row tail
+    (3, 2, 2, 127, 254, 64, 127, 127, True),  # ragged tile, bottom-right causal, s2 = 127
+    (1, 2, 2, 4096, 4096, 128, 128, 128, True),
+    (70000, 1, 1, 16, 16, 64, 16, 16, False),  # many one-block sequences (packed)
+    (4, 16, 16, 640, 640, 64, 128, 64, True),
+])
+def test_fused_shape_canary(dev, shape):
+    """Crash / race canary over unusual shapes: either a clean validation error, or a finite
+    output that is bit-identical across two launches."""
+    from paper_2503_01873_b200 import pasa_attention_fwd
+    from paper_2503_01873_b200._lib import PasaError
+    B, Hq, Hkv, S1, S2, d, s1, s2, causal = shape
+    g = torch.Generator(device=dev)
+    g.manual_seed(S1 * 7 + S2)
+    q = torch.randn(B, Hq, S1, d, device=dev, generator=g).half()
+    k = torch.randn(B, Hkv, S2, d, device=dev, generator=g).half()
+    v = torch.randn(B, Hkv, S2, d, device=dev, generator=g).half()
+    try:
+        a = pasa_attention_fwd(q, k, v, BETA_STAR, causal=causal, s1=s1, s2=s2)
+    except (ValueError, PasaError):
+        return  # rejected by validation (s2 > 128 is PASA_B200_EUNSUPPORTED)
+    b = pasa_attention_fwd(q, k, v, BETA_STAR, causal=causal, s1=s1, s2=s2)
+    torch.cuda.synchronize()
+    assert bool(torch.isfinite(a).all())
+    assert torch.equal(a.view(torch.int16), b.view(torch.int16))
