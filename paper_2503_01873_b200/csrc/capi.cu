@@ -8,6 +8,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -639,6 +640,91 @@ struct HostCache {
 };
 static thread_local HostCache g_host_cache;
 
+// One piece of a query-tile split (more devices than (b, kv head) units): units [u0, u1),
+// query tiles [t0, t0 + nt) of each, on the current device.  Q rows of those tiles and the
+// units' K, V go in, pasa_b200_attention_fwd_tiles computes them exactly as the whole problem
+// does, the O rows come back.  Not pipelined: a split piece is a small share.
+struct TilePiece {
+  int u0, u1, t0, nt;
+};
+
+static int host_tile_piece(const pasa_b200_desc* d, const uint16_t* q, const uint16_t* k, const uint16_t* v,
+                           uint16_t* o, const TilePiece& pc) {
+  const int group = d->heads_q / d->heads_kv, nu = pc.u1 - pc.u0;
+  pasa_b200_desc sd = *d;  // the piece's units as one batch of nu kv heads (BHSD)
+  sd.batch = 1;
+  sd.heads_kv = nu;
+  sd.heads_q = nu * group;
+  const size_t head = static_cast<size_t>(d->seq_q) * d->head_dim * 2;  // bytes per q head
+  const size_t kunit = static_cast<size_t>(d->seq_kv) * d->head_dim * 2;
+  const int r0 = pc.t0 * kTile, r1 = std::min(d->seq_q, (pc.t0 + pc.nt) * kTile);
+  const size_t rows_b = static_cast<size_t>(r1 - r0) * d->head_dim * 2, off_b = static_cast<size_t>(r0) * d->head_dim * 2;
+  const size_t qb = head * nu * group, kb = kunit * nu, wsb = pasa_b200_workspace_size(&sd);
+  cudaStream_t st = nullptr;
+  void *dq = nullptr, *dk = nullptr, *dv = nullptr, *dout = nullptr, *ws = nullptr;
+  int rc = PASA_B200_OK;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&dq, qb);
+  if (e == cudaSuccess) e = cudaMalloc(&dout, qb);
+  if (e == cudaSuccess) e = cudaMalloc(&dk, kb);
+  if (e == cudaSuccess) e = cudaMalloc(&dv, kb);
+  if (e == cudaSuccess) e = cudaMalloc(&ws, wsb);
+  const uint8_t* qh = reinterpret_cast<const uint8_t*>(q) + head * group * pc.u0;
+  uint8_t* oh = reinterpret_cast<uint8_t*>(o) + head * group * pc.u0;
+  if (e == cudaSuccess)  // the tiles' rows of every q head of the piece (pitch: one head)
+    e = cudaMemcpy2DAsync(static_cast<uint8_t*>(dq) + off_b, head, qh + off_b, head, rows_b, nu * group,
+                          cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(dk, reinterpret_cast<const uint8_t*>(k) + kunit * pc.u0, kb, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(dv, reinterpret_cast<const uint8_t*>(v) + kunit * pc.u0, kb, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) rc = cuda_fail(e, "attention_host_multi: piece setup");
+  if (rc == PASA_B200_OK) rc = pasa_b200_attention_fwd_tiles(&sd, dq, dk, dv, dout, ws, wsb, pc.t0, pc.nt, st);
+  if (rc == PASA_B200_OK) {
+    e = cudaMemcpy2DAsync(oh + off_b, head, static_cast<uint8_t*>(dout) + off_b, head, rows_b, nu * group,
+                          cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "attention_host_multi: piece copy-out");
+  }
+  if (st) cudaStreamSynchronize(st);
+  for (void* b : {dq, dk, dv, dout, ws})
+    if (b) cudaFree(b);
+  if (st) cudaStreamDestroy(st);
+  return rc;
+}
+
+// partition_work of multi.py: the unit-major (unit, tile) items cut into n runs of equal
+// key-block cost (an item goes to the run holding its cost midpoint); a run is at most three
+// pieces (a unit's tail, whole units, a unit's head).
+static std::vector<std::vector<TilePiece>> tile_partition(const pasa_b200_desc* d, int n) {
+  const int nq = (d->seq_q + kTile - 1) / kTile, nkv = d->seq_kv / d->s2, qoff = d->seq_kv - d->seq_q;
+  const int units = d->batch * d->heads_kv;
+  std::vector<long long> cost(nq), prefix(nq + 1, 0);
+  for (int i = 0; i < nq; ++i) {
+    cost[i] = d->causal ? std::min((std::min(d->seq_q, kTile * (i + 1)) - 1 + qoff) / d->s2 + 1, nkv) : nkv;
+    prefix[i + 1] = prefix[i] + cost[i];
+  }
+  const long long per_unit = prefix[nq], total = per_unit * units;
+  auto owner = [&](int u, int i) {
+    const long long mid2 = 2 * (u * per_unit + prefix[i]) + cost[i];
+    return total ? static_cast<int>(std::min<long long>(n - 1, mid2 * n / (2 * total))) : 0;
+  };
+  std::vector<std::vector<TilePiece>> runs(n);
+  for (int u = 0; u < units; ++u)
+    for (int lo = 0; lo < nq;) {
+      const int r = owner(u, lo);
+      int hi = lo;
+      while (hi < nq && owner(u, hi) == r) ++hi;
+      auto& pcs = runs[r];
+      if (!pcs.empty() && lo == 0 && hi == nq && pcs.back().t0 == 0 && pcs.back().nt == nq && pcs.back().u1 == u)
+        pcs.back().u1 = u + 1;
+      else
+        pcs.push_back({u, u + 1, lo, hi - lo});
+      lo = hi;
+    }
+  return runs;
+}
+
 int pasa_b200_attention_host_multi(const pasa_b200_desc* d, const uint16_t* q, const uint16_t* k,
                                    const uint16_t* v, uint16_t* o, const int32_t* devices,
                                    int32_t n_devices) {
@@ -651,8 +737,37 @@ int pasa_b200_attention_host_multi(const pasa_b200_desc* d, const uint16_t* q, c
     return fail(PASA_B200_EUNSUPPORTED, "attention_host_multi: BHSD only (units must be contiguous)");
   // The (batch, kv head) units, contiguous in BHSD, are split evenly across the devices
   // (no exchange -- each device computes its units' whole output); one host
-  // thread per device runs the pipelined host entry point on its share.
+  // thread per device runs the pipelined host entry point on its share.  With more devices
+  // than units, query tiles are split too (tile_partition; bit-identical, like multi.py).
   const int units = d->batch * d->heads_kv, group = d->heads_q / d->heads_kv;
+  if (n_devices > units && !packed_shape(d, nullptr, 0) && (d->seq_q + kTile - 1) / kTile > 1) {
+    const auto runs = tile_partition(d, n_devices);
+    std::vector<int> rcs(n_devices, PASA_B200_OK);
+    std::vector<std::string> errs(n_devices);
+    std::vector<std::thread> pool;
+    for (int r = 0; r < n_devices; ++r) {
+      if (runs[r].empty()) continue;
+      pool.emplace_back([&, r] {
+        if (cudaSetDevice(devices[r]) != cudaSuccess) {
+          rcs[r] = PASA_B200_ENODEV;
+          errs[r] = "attention_host_multi: cudaSetDevice failed";
+          return;
+        }
+        for (const TilePiece& pc : runs[r])
+          if ((rcs[r] = host_tile_piece(d, q, k, v, o, pc)) != PASA_B200_OK) {
+            errs[r] = g_last_error;
+            break;
+          }
+      });
+    }
+    for (auto& th : pool) th.join();
+    for (int r = 0; r < n_devices; ++r)
+      if (rcs[r]) {
+        g_last_error = errs[r];
+        return rcs[r];
+      }
+    return PASA_B200_OK;
+  }
   const int n = n_devices < units ? n_devices : units;
   const size_t q_unit = static_cast<size_t>(group) * d->seq_q * d->head_dim;  // halves
   const size_t k_unit = static_cast<size_t>(d->seq_kv) * d->head_dim;

@@ -512,6 +512,28 @@ def test_host_multi_device_bit_identical(dev):
     assert torch.isfinite(o1.float()).all() and torch.equal(o1, o3)
 
 
+@pytest.mark.parametrize("causal,S,ndev", [(True, 1000, 5), (False, 384, 4), (True, 2048, 8)])
+def test_host_multi_query_tile_split(dev, causal, S, ndev):
+    """pasa_b200_attention_host_multi with more devices than (b, kv head) units (here device 0
+    repeated): query tiles are split across the list and the output is
+    bit-identical to the single-device host call (ragged last tile included)."""
+    from paper_2503_01873_b200 import _lib
+    B, Hq, Hkv, D = 1, 4, 2, 128
+    g = torch.Generator().manual_seed(S)
+    q = (torch.randn(B, Hq, S, D, generator=g) * 2).half().pin_memory()
+    k = (torch.randn(B, Hkv, S, D, generator=g) * 2).half().pin_memory()
+    v = torch.randn(B, Hkv, S, D, generator=g).half().pin_memory()
+    L = _lib.load()
+    desc = _lib.Desc(B, Hq, Hkv, S, S, D, 8 if S == 1000 else 128, 8 if S == 1000 else 128, int(causal), 0,
+                     BETA_STAR, math.sqrt(D))
+    o1, on = torch.empty_like(q).pin_memory(), torch.full_like(q, float("nan")).pin_memory()
+    _lib.check(L.pasa_b200_attention_host(C.byref(desc), q.data_ptr(), k.data_ptr(), v.data_ptr(), o1.data_ptr()))
+    devs = (C.c_int32 * ndev)(*([0] * ndev))
+    _lib.check(L.pasa_b200_attention_host_multi(C.byref(desc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                                on.data_ptr(), devs, ndev))
+    assert torch.isfinite(o1.float()).all() and torch.equal(o1, on)
+
+
 def test_fa16_ragged(dev, orc):
     from paper_2503_01873_b200 import flash_fp16_fwd
     q, k, v = orc.generate("hybrid", 0.0, 10.0, 14, 1, 2, 160, 64)
