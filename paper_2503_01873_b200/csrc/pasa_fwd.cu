@@ -51,12 +51,12 @@ constexpr bool kPingPong = (D == 64 ? PASA_PINGPONG_D64 : PASA_PINGPONG) != 0;
 #define PASA_DYN_ORDER 1
 #endif
 // One exp pair in kPolyEvery on the FMA-pipe polynomial (0: MUFU only).  d = 128
-// balances MUFU against issue slots at 6 (5-7 within noise, +2-3 % over 4 once P is
-// released in parts and the tiles' exp passes overlap); at d = 64 the FMA pipe and the
+// balances MUFU against issue slots at 8 (round 2, with the TMA-stored epilogue: +1-2 % over
+// 6 at Qwen 16K, 10 and MUFU-only lose 2-4 %; round 1: +2-3 % over 4); at d = 64 the FMA pipe and the
 // issue slots are shared with twice the softmax work per FLOP and MUFU-only wins
 // (measured: tools/variants.py, +6 % at d = 64 over 1/4; 1/8 and 1/16 lose 9-10 %).
 #ifndef PASA_POLY_EVERY
-#define PASA_POLY_EVERY 6
+#define PASA_POLY_EVERY 8
 #endif
 #ifndef PASA_POLY_EVERY_D64
 #define PASA_POLY_EVERY_D64 0

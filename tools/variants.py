@@ -10,6 +10,8 @@ from paper_2503_01873_b200 import _lib  # noqa: E402
 dev = torch.device("cuda:0")
 CFGS = [("qwen16k-causal", 1, 28, 4, 16384, 128, True), ("H32-16k", 1, 32, 32, 16384, 128, False),
         ("d64-8k", 8, 8, 8, 8192, 64, False)]
+MORE = {"qwen32k-causal": ("qwen32k-causal", 1, 28, 4, 32768, 128, True),
+        "qwen8k-causal": ("qwen8k-causal", 1, 28, 4, 8192, 128, True)}
 
 
 def setup(L, B, Hq, Hkv, S, D, causal):
@@ -50,9 +52,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rounds", type=int, default=5)
     ap.add_argument("--fa16", action="store_true")
+    ap.add_argument("--cfg", nargs="*", default=None, help=f"workloads (default the first three; more: {list(MORE)})")
     ap.add_argument("libs", nargs="+")
     a = ap.parse_args()
     global FA16
+    cfgs = CFGS if not a.cfg else [MORE[c] if c in MORE else next(x for x in CFGS if x[0] == c) for c in a.cfg]
     FA16 = a.fa16
     libs = []
     for so in a.libs:
@@ -62,7 +66,7 @@ def main():
         L.pasa_b200_flash_fp16_fwd.argtypes = [C.POINTER(_lib.Desc)] + [C.c_void_p] * 5
         libs.append(L)
     res = {so: [] for so in a.libs}
-    for name, B, Hq, Hkv, S, D, causal in CFGS:
+    for name, B, Hq, Hkv, S, D, causal in cfgs:
         fl = 4.0 * B * Hq * S * S * D * (0.5 if causal else 1.0)
         args = [setup(L, B, Hq, Hkv, S, D, causal) for L in libs]
         ts = {so: [] for so in a.libs}
