@@ -19,22 +19,25 @@
 // the fused kernel does when the sequence is alone: the output is bit-identical to
 // pasa_fwd.cu's, whatever the packing (host pipeline pieces, multi-GPU shards).
 //
-// Persistent CTAs walk the tiles; three warpgroups: warp 0 loads (TMA, a two-stage ring, so
-// the next tile's loads overlap this one's compute) and warp 1 issues the MMAs; warps 4-7 run
-// the softmax with one thread per row (TMEM lane quadrant = warp % 4); warps 8-11 (self_prep,
-// the public entry point) run the key pre-pass and the V scale of each staged tile in shared
-// memory -- K' = rank-1 form of K^T M, V' = V 2^-c0 -- so the kernel reads raw K, V from HBM
-// and no workspace round trip is needed.  TMEM: S'/P at +0, T at +128, T_clean at +128 + D
-// (256 columns at d = 64, so two CTAs share an SM; 512 at d = 128).
+// Persistent CTAs walk the tiles with a two-stage TMA ring (Q / K and V of a stage arrive on
+// separate barriers, so S' can run before V has landed); the kernel is instantiated per slot
+// width WS.  Warpgroups: warp 0 loads, warp 1 issues the MMAs; warps 4-7 run the softmax with
+// one thread per row (TMEM lane quadrant = warp % 4) and the epilogue, whose O tile is staged
+// in the stage's consumed V' buffer and leaves by TMA; warps 8-11 and 12-15 (self_prep, the
+// public entry point) run the key pre-pass and the V scale of the staged tiles in shared
+// memory -- K' = rank-1 form of K^T M, V' = V 2^-c0 -- warpgroup g taking stage g, so the
+// kernel reads raw K, V from HBM and no workspace round trip is needed.  TMEM: S'/P at +0,
+// T at +128, T_clean at +128 + D (256 columns at d = 64, so two CTAs share an SM; 512 at
+// d = 128).
 //
 // Non-finite V: the tile's P V' also multiplies each row's zero P entries by the other
 // sequences' V' rows, and 0 x Inf = NaN would leak one sequence's Inf/NaN into its
-// neighbours (the unpacked kernel keeps heads apart).  So the MMA warp scans the tile's V'
-// rows while S' runs; for a tile with a non-finite V' row it issues P V' twice -- into T
-// (the poisoned sequences read it: exactly what they get alone) and, after zeroing the
-// poisoned sequences' V' rows in shared memory, into T_clean (everyone else reads it).
-// The zeroed rows stay zero until TMA refills them, so the stale slots of a ragged last
-// tile are clean too.  Clean tiles pay only the scan.
+// neighbours (the unpacked kernel keeps heads apart).  So the pre-pass (or, on prepped
+// inputs, the MMA warp while S' runs) finds the slots with a non-finite V' row; for such a
+// tile the MMA warp issues P V' twice -- into T (the poisoned sequences read it: exactly what
+// they get alone) and, after zeroing the poisoned sequences' V' rows in shared memory, into
+// T_clean (everyone else reads it).  A ragged last tile first zeroes its unused slots (they
+// hold an earlier tile's staged O).  Clean tiles pay nothing extra.
 #include <cuda.h>
 #include <cuda_fp16.h>
 
@@ -46,9 +49,9 @@ using namespace sm100;
 
 // PASA_TRACE builds: CTA 0 records clock64() at fixed points of its first 64 tiles,
 // p.trace[(role * 64 + it) * 16 + event]: role 0 = softmax thread 128 (0 start, 1 S' ready,
-// 2 P stored, 3 O stored, 4 T ready, 5 T read) and the prep (6 stage landed, 7 K' written);
-// role 1 = MMA issuer (0 S' issued, 1 P ready, 2 PV committed), TMA producer (3 Q/K issued,
-// 4 V issued), prep (5 start, 6 done, 8 K/V pass, 9 K' pass, 10 V scale + c0, 11 fenced)
+// 2 P stored, 3 O stored, 4 T ready, 5 T read) and the prep (6 Q/K landed); role 1 = MMA
+// issuer (0 S' issued, 1 P ready, 2 PV committed), TMA producer (3 Q/K issued, 4 V issued),
+// prep (5 start, 6 done, 8 K' written, 9 V landed, 10 max|V| in, 11 c0 and mask written)
 #ifdef PASA_TRACE
 #define PK_TRP(tr, role, it, ev)                                                   \
   do {                                                                             \
