@@ -36,7 +36,7 @@ def main():
     f = lambda x: f"{(x - base) / 1000:6.2f}"
     for i in range(1, 25):
         period = sm[i + 1, 1] - sm[i, 1]
-        print(f"{i:3d} | {f(ct[i,3])} {f(ct[i,4])} | {f(sm[i,6])} {f(sm[i,7])} {f(ct[i,6])} | "
+        print(f"{i:3d} | {f(ct[i,3])} {f(ct[i,4])} | {f(sm[i,6])} {f(ct[i,8])} {f(ct[i,6])} | "
               f"{f(ct[i,0])} {f(ct[i,1])} {f(ct[i,2])} | {f(sm[i,1])} {f(sm[i,2])} {f(sm[i,4])} {f(sm[i,5])} "
               f"{f(sm[i,3])} | {sm[i,6]-ct[i,4]:5d} {ct[i,6]-sm[i,6]:5d} {sm[i,1]-ct[i,0]:5d} "
               f"{sm[i,2]-sm[i,1]:5d} {ct[i,2]-ct[i,1]:4d} {sm[i,3]-sm[i,5]:4d} | {period:5d} | "
