@@ -26,6 +26,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 import math
+from collections import OrderedDict
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -254,7 +255,8 @@ def _check_device_tensors(fn: str, q: torch.Tensor, k: torch.Tensor, v: torch.Te
         raise ValueError(f"{fn}: out must be a contiguous tensor of q's shape {tuple(q.shape)}")
 
 
-_WS: dict[tuple[int, int], torch.Tensor] = {}
+_WS: "OrderedDict[tuple[int, int], torch.Tensor]" = OrderedDict()
+_WS_MAX = 8  # cached workspaces (least recently used dropped first)
 
 
 def workspace_for(desc: _lib.Desc, device: torch.device,
@@ -264,7 +266,9 @@ def workspace_for(desc: _lib.Desc, device: torch.device,
     Each stream gets its own buffer, allocated while that stream is current, so torch's
     caching allocator only hands its memory out again in that stream's order: two calls on
     different streams never share a workspace, and a buffer replaced by a larger one cannot
-    be reused while a kernel on its stream may still read it."""
+    be reused while a kernel on its stream may still read it.  At most _WS_MAX buffers are
+    kept (a dropped one is freed in its stream's order, like any tensor the launches
+    recorded on that stream); release_workspaces() drops them all."""
     n = _lib.load().pasa_b200_workspace_size(C.byref(desc))
     idx = device.index if device.index is not None else torch.cuda.current_device()
     s = stream if stream is not None else torch.cuda.current_stream(idx)
@@ -274,7 +278,15 @@ def workspace_for(desc: _lib.Desc, device: torch.device,
         with torch.cuda.device(idx), torch.cuda.stream(s):
             ws = torch.empty(n, dtype=torch.uint8, device=device)
         _WS[key] = ws
+    _WS.move_to_end(key)
+    while len(_WS) > _WS_MAX:
+        _WS.popitem(last=False)
     return ws[:n]
+
+
+def release_workspaces() -> None:
+    """Drop every cached K'/V' workspace (freed in the order of the streams that used them)."""
+    _WS.clear()
 
 
 def _launch_stream(dev: torch.device, stream: "torch.cuda.Stream | None"):

@@ -961,3 +961,21 @@ def test_fused_shape_canary(dev, shape):
     torch.cuda.synchronize()
     assert bool(torch.isfinite(a).all())
     assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+
+
+def test_workspace_cache_bounded(dev):
+    """The per-(device, stream) K'/V' workspace cache keeps at most _WS_MAX buffers (LRU), and
+    calls on many streams still agree bit for bit."""
+    from paper_2503_01873_b200 import api, pasa_attention_fwd
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    q, k, v = (torch.randn(1, 2, 256, 64, device=dev, generator=g).half() for _ in range(3))
+    want = pasa_attention_fwd(q, k, v, causal=True)
+    streams = [torch.cuda.Stream(dev) for _ in range(api._WS_MAX + 3)]
+    outs = [pasa_attention_fwd(q, k, v, causal=True, stream=s) for s in streams]
+    torch.cuda.synchronize()
+    assert len(api._WS) <= api._WS_MAX
+    for o in outs:
+        assert torch.equal(o.view(torch.int16), want.view(torch.int16))
+    api.release_workspaces()
+    assert len(api._WS) == 0
