@@ -1,5 +1,5 @@
 """Warp-state samples of an ncu --set full report by opcode and top instructions (tool).
-    python tools/ncu_stalls.py gpurun_out/ncu_fwd128.ncu-rep > profiles/r01_ncu_pasa_fwd_stalls.txt"""
+    python tools/ncu_stalls.py gpurun_out/ncu_fwd128.ncu-rep > profiles/r02_ncu_pasa_fwd_stalls.txt"""
 import csv, subprocess, sys
 from collections import defaultdict
 
