@@ -192,6 +192,29 @@ def test_fwd_tier1_vs_reference(dev, orc, cell):
         assert orc.nan_pct(orc.flash_ref(pb)) == 100.0
 
 
+def test_fwd_k_only_bias_config1(dev, orc):
+    """SURVEY.md 8d config 1, K-only-bias variant: Q, V ~ U(0.5, 1.5), K ~ U(0.5, 1.5) + 600 at
+    (1, 2, 1024, 128) -- the reference's naive partial-FP16 FA overflows everywhere (100 % NaN),
+    PASA stays finite; Tier-1 parity against the reference's PASA on the same FP16 inputs."""
+    rng = np.random.default_rng(0)
+    sh = (1, 2, 1024, 128)
+    q = rng.uniform(0.5, 1.5, sh).astype(np.float16).astype(np.float64)
+    k = (rng.uniform(0.5, 1.5, sh) + 600.0).astype(np.float16).astype(np.float64)
+    v = rng.uniform(0.5, 1.5, sh).astype(np.float16).astype(np.float64)
+    pb = Problem(q, k, v)
+    o, _ = run_fwd(dev, q, k, v)
+    on = o.double().cpu().numpy()
+    gold = orc.golden(pb)
+    refo = orc.pasa_ref(pb)
+    assert orc.nan_pct(on) == 0.0 and orc.nan_pct(refo) == 0.0
+    assert orc.nan_pct(orc.flash_ref(pb)) == 100.0
+    r_ref = orc.rmse(refo, gold)
+    assert orc.rmse(on, gold) <= 1.25 * r_ref + 1e-3
+    assert orc.rmse(on, refo) <= 2.0 * r_ref + 1e-3
+    o16 = run_fwd(dev, q, k, v, beta=0.0)[0]  # the same pipeline's naive FP16 FA (beta = 0)
+    assert not bool(torch.isfinite(o16).any())
+
+
 def test_fwd_resonance_no_overflow(dev, orc):
     q, k, v = orc.generate_resonance(0, 1, 2, 1024, 64)
     pb = Problem(q, k, v)
