@@ -2,8 +2,10 @@
 //
 // Compiled against the REFERENCE's own headers (include/pasa/pasa.hpp), it
 // defines the symbols other reference objects bind to -- build_shifting_matrix,
-// PasaParams::make, preprocess_keys and pasa_attention (pasa.hpp:27-99) -- on
-// top of libpasa_b200.so's C-ABI.  Linking the reference's bench.o (whose
+// shifting_matrix_inverse, PasaParams::make, preprocess_keys and pasa_attention
+// (pasa.hpp:27-99) -- on top of libpasa_b200.so's C-ABI.  The per-block CPU primitives
+// (recover_global_mean, correction_terms, OnlineState) are not provided: the B200 build
+// runs that recursion on the device inside pasa_attention.  Linking the reference's bench.o (whose
 // `sweep` calls PasaParams::make, pasa_attention and preprocess_keys,
 // bench.cpp:136, :196, :224) against this file instead of pasa.o runs the
 // reference's own harness on the B200 kernel.  INTEGRATION.md shows the recipe.
@@ -55,6 +57,20 @@ bool is_pasa_fp16(const pasa::PrecisionPolicy& p) {
 }  // namespace
 
 namespace pasa {
+
+// Theorem 2.1's closed-form inverse of (I - lambda J): I + lambda / (1 - lambda s) J, FP64
+// (pasa.cpp:37-51); singular exactly when lambda s == 1 (beta == 1).
+Matrix2D shifting_matrix_inverse(size_t s, double lambda) {
+  const double denom = 1.0 - lambda * static_cast<double>(s);
+  if (denom == 0.0) throw SingularMatrixError("shifting matrix is singular: lambda * s == 1 (beta == 1)");
+  const double off = lambda / denom;
+  Matrix2D m(s, s, Prec::FP64);
+  for (size_t r = 0; r < s; ++r) {
+    double* row = m.row(r);
+    for (size_t c = 0; c < s; ++c) row[c] = r == c ? 1.0 + off : off;
+  }
+  return m;
+}
 
 Matrix2D build_shifting_matrix(size_t s2, double beta, double alpha, Prec prec) {
   if (s2 == 0) throw std::invalid_argument("shifting matrix: s2 must be >= 1");

@@ -7,13 +7,13 @@ The compute lives in ``libpasa_b200.so`` (CUDA, sm_100a, C-ABI in
 reference's operator API.
 """
 from .api import (BETA_STAR, AttentionProblem, AttnOptions, M0Mode, PasaParams, PolicyId, Prec,
-                  PrecisionPolicy, RunDiagnostics, build_shifting_matrix, flash_attention,
-                  flash_fp16_fwd, make_problem, pasa_attention, pasa_attention_fwd, policy_for,
-                  preprocess_keys, shift_entries)
+                  PrecisionPolicy, RunDiagnostics, SingularMatrixError, build_shifting_matrix,
+                  flash_attention, flash_fp16_fwd, make_problem, pasa_attention, pasa_attention_fwd,
+                  policy_for, preprocess_keys, shift_entries, shifting_matrix_inverse)
 
 __all__ = [
     "BETA_STAR", "AttentionProblem", "AttnOptions", "M0Mode", "PasaParams", "PolicyId", "Prec",
-    "PrecisionPolicy", "RunDiagnostics", "build_shifting_matrix", "flash_attention",
+    "PrecisionPolicy", "RunDiagnostics", "SingularMatrixError", "build_shifting_matrix", "flash_attention",
     "flash_fp16_fwd", "make_problem", "pasa_attention",
-    "pasa_attention_fwd", "policy_for", "preprocess_keys", "shift_entries",
+    "pasa_attention_fwd", "policy_for", "preprocess_keys", "shift_entries", "shifting_matrix_inverse",
 ]

@@ -131,6 +131,21 @@ def shift_entries(s2: int, beta: float, alpha: float) -> tuple[float, float]:
     return _f16_bits_to_float(d.value), _f16_bits_to_float(o.value)
 
 
+class SingularMatrixError(ValueError):
+    """pasa.hpp:19-21 (a std::domain_error there)."""
+
+
+def shifting_matrix_inverse(s: int, lam: float) -> np.ndarray:
+    """Theorem 2.1's closed-form inverse of (I - lam J): I + lam / (1 - lam s) J, FP64
+    (pasa.cpp:37-51); SingularMatrixError exactly when lam s == 1 (beta == 1)."""
+    denom = 1.0 - lam * float(s)
+    if denom == 0.0:
+        raise SingularMatrixError("shifting matrix is singular: lambda * s == 1 (beta == 1)")
+    m = np.full((s, s), lam / denom)
+    m[np.diag_indices(s)] += 1.0
+    return m
+
+
 def build_shifting_matrix(s2: int, beta: float, alpha: float, prec: Prec = Prec.FP16) -> np.ndarray:
     """M = I/alpha - beta*J/(alpha*s2), each entry rounded once (pasa.cpp:16-35)."""
     if prec != Prec.FP16:
