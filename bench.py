@@ -177,11 +177,13 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def time_reference_step(ref, q, k, v):
+def time_reference_step(ref, q, k, v, threads):
+    """The thread count goes to the reference explicitly (AttnOptions::threads,
+    parallel.hpp:20-32): under torchrun OMP_NUM_THREADS=1 would otherwise pin it to one."""
     from oracle.oracle import PASA_FP16, Problem
     pb = Problem(q, k, v)
     t0 = time.perf_counter()
-    o = ref.pasa(pb, BETA, PASA_FP16)
+    o = ref.pasa(pb, BETA, PASA_FP16, threads=threads)
     dt = time.perf_counter() - t0
     return dt, o
 
@@ -201,8 +203,8 @@ def run_reference_arm(args):
     q, k, v, nb = reference_sample(cores, SEQ)
     flops = 4.0 * nb * 128 * SEQ * D  # non-causal rows: the work the reference performs
     for _ in range(args.warmup):
-        time_reference_step(ref, q, k, v)
-    times = [time_reference_step(ref, q, k, v)[0] for _ in range(args.steps)]
+        time_reference_step(ref, q, k, v, cores)
+    times = [time_reference_step(ref, q, k, v, cores)[0] for _ in range(args.steps)]
     tot = sum(times)
     val = flops * len(times) / tot / 1e12
     sample = (f"pasa::pasa_attention PASA_FP16 (oracle/_ref), 1 head x {nb} query blocks "
@@ -423,7 +425,7 @@ def run_b200(args):
         if ref_available():
             cores = cpu_cores()
             qs, ks, vs, nb = reference_sample(8 * cores, SEQ)  # ~10 s of reference work
-            dt, o_ref = time_reference_step(RefLib(), qs, ks, vs)
+            dt, o_ref = time_reference_step(RefLib(), qs, ks, vs, cores)
             cpu_base = {"value": 4.0 * nb * 128 * SEQ * D / dt / 1e12, "unit": UNIT,
                         "cores": cores, "kind": "reference",
                         "sample": f"pasa::pasa_attention (oracle/_ref) 1 head x {nb} query blocks "
