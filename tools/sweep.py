@@ -28,6 +28,7 @@ sys.path.insert(0, ROOT)
 
 from paper_2503_01873_b200 import _lib  # noqa: E402
 from paper_2503_01873_b200 import bench_api as ba  # noqa: E402
+from bench import ClockSampler  # noqa: E402
 
 BETA = 0.984497
 
@@ -91,10 +92,12 @@ def run(L, name, kind, B, Hq, Hkv, S, d, causal, iters, dev, full_rmse=True):
     for _ in range(3):
         launch()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(iters)]
-    for e in evs:
-        flush.zero_()
-        launch(e)
     torch.cuda.synchronize()
+    with ClockSampler(dev.index or 0) as cs:  # nvidia-smi during the timed launches
+        for e in evs:
+            flush.zero_()
+            launch(e)
+        torch.cuda.synchronize()
     step = sum(e[0].elapsed_time(e[2]) for e in evs) / iters
     fwd = sum(e[1].elapsed_time(e[2]) for e in evs) / iters
     flops = 4.0 * B * Hq * S * S * d * (0.5 if causal else 1.0)
@@ -116,7 +119,7 @@ def run(L, name, kind, B, Hq, Hkv, S, d, causal, iters, dev, full_rmse=True):
            "fwd_tflops": flops / fwd / 1e9, "step_tflops": flops / step / 1e9,
            "fwd_frac_of_measured_peak": flops / fwd / 1e9 / peak(),
            "rmse_vs_fp32_full": full, "rmse_vs_fp64_sampled": math.sqrt(err / nrm),
-           "nonfinite": int((~torch.isfinite(o)).sum().item())}
+           "nonfinite": int((~torch.isfinite(o)).sum().item()), "clocks": cs.summary()}
     print(json.dumps(res), flush=True)
     del q, k, v, kp, vp, o, flush, ws
     torch.cuda.empty_cache()
@@ -127,16 +130,19 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.json"))
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--only", default="", help="comma list of row groups: qwen,svd,long (default all)")
     a = ap.parse_args()
     L = _lib.load()
     dev = torch.device("cuda:0")
     it = 5 if a.quick else 10
     rows = []
-    for S in (8192, 16384, 32768):
+    only = set(a.only.split(",")) if a.only else {"qwen", "svd", "long"}
+    for S in ((8192, 16384, 32768) if "qwen" in only else ()):
         rows.append(run(L, "qwen2-7b (configs[1])", "uniform30", 1, 28, 4, S, 128, True, it, dev))
-    rows.append(run(L, "svd-spatial d=64 (configs[2])", "resonance", 50, 5, 5, 9216, 64, False, it, dev))
-    rows.append(run(L, "svd-temporal d=64 (configs[2])", "resonance", 9216, 5, 5, 25, 64, False, it, dev))
-    for S in (4096, 8192, 16384, 32768, 65536, 131072):
+    if "svd" in only:
+        rows.append(run(L, "svd-spatial d=64 (configs[2])", "resonance", 50, 5, 5, 9216, 64, False, it, dev))
+        rows.append(run(L, "svd-temporal d=64 (configs[2])", "resonance", 9216, 5, 5, 25, 64, False, it, dev))
+    for S in ((4096, 8192, 16384, 32768, 65536, 131072) if "long" in only else ()):
         if a.quick and S > 32768:
             break
         rows.append(run(L, "long sweep H=32 d=128 (configs[3])", "hybrid", 1, 32, 32, S, 128, False,
