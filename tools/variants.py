@@ -10,7 +10,8 @@ from paper_2503_01873_b200 import _lib  # noqa: E402
 dev = torch.device("cuda:0")
 CFGS = [("qwen16k-causal", 1, 28, 4, 16384, 128, True), ("H32-16k", 1, 32, 32, 16384, 128, False),
         ("d64-8k", 8, 8, 8, 8192, 64, False)]
-MORE = {"qwen32k-causal": ("qwen32k-causal", 1, 28, 4, 32768, 128, True),
+MORE = {"svd-spatial": ("svd-spatial", 50, 5, 5, 9216, 64, False),
+        "qwen32k-causal": ("qwen32k-causal", 1, 28, 4, 32768, 128, True),
         "qwen8k-causal": ("qwen8k-causal", 1, 28, 4, 8192, 128, True)}
 
 
