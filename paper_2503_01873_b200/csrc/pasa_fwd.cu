@@ -436,15 +436,22 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       tma_prefetch(&tm_kp);
       tma_prefetch(&tm_v);
       if (kTcSum || kProSum) tma_prefetch(&tm_ks);
-      for (int t = 0; t < NT; ++t) {
-        if (!tl[t].valid) continue;
+      auto load_q = [&](int t) {
+        if (!tl[t].valid) return;
         mbar_expect_tx(q_full + 8 * (t), Cfg::TILE_BYTES);
         for (int bx = 0; bx < Cfg::NBOX; ++bx)
           // BHSD (c, s, b Hq + h); BSHD (h D + c, s, b) on the {Hq D, S1, B} map
           tma_load_3d(sb + Cfg::SMEM_Q + t * Cfg::TILE_BYTES + bx * Cfg::BOX_BYTES, &tm_q,
                       q_full + 8 * (t), (p.q_bshd ? tl[t].hq * D : 0) + bx * 64, tl[t].i * kTile,
                       p.q_bshd ? b : b * p.Hq + tl[t].hq);
-      }
+      };
+      // Start-up order Q_0, K'(0), Q_1, V'(0): the CTA's first S' waits for the loads
+      // ahead of it (per-SM load bandwidth sets the start-up time), so tile 0's S'(0)
+      // issues once 2/3 of the first S' operands have landed.  The prologue GEMM
+      // (kProSum) reads every Q tile first.
+      const bool q_early = kProSum || nmax == 0;
+      for (int t = 0; t < NT; ++t)
+        if (t == 0 || q_early) load_q(t);
       // Prologue (kProSum): the head's K' block sums, 128 blocks at a time, into the V'
       // stages (free until the first V' load): box (hl, bx) = the hi (hl = 0) or lo rows,
       // columns [64 bx, 64 bx + 64), 128 blocks x 128 B (SW128, K-major like K').
@@ -468,6 +475,8 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
             tma_load_3d(sb + Cfg::SMEM_KS + (ks * Cfg::NBOX + bx) * Cfg::KS_BOX, &tm_ks,
                         k_full + 8 * (ks), bx * 64, 2 * j, b * p.Hkv + hkv);
         }
+        if (j == 0 && !q_early)
+          for (int t = 1; t < NT; ++t) load_q(t);
         if (kProSum && j == 0 && nch > 0) mbar_wait(ks_empty, (nch - 1) & 1);  // V area free
         mbar_wait(v_empty + 8 * (vs), ((j / VS) & 1) ^ 1);
         mbar_expect_tx(v_full + 8 * (vs), Cfg::NBOX * 128 * p.s2);
@@ -614,8 +623,9 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
                   kIdPV, part > 0 || k > 0);
         }
       };
-      for (int t = 0; t < NT; ++t)
-        if (tl[t].valid) mbar_wait(q_full + 8 * (t), 0);
+      if (kProSum)
+        for (int t = 0; t < NT; ++t)
+          if (tl[t].valid) mbar_wait(q_full + 8 * (t), 0);
       // Prologue (kProSum): G_t = [Q_t | Q_t] [hi | lo]^T (K = 2 D) for 128 blocks at a
       // time into tile t's T columns [256 t + 128, 256 t + 128 + nb) (FP32), read out by the
       // softmax warps (g_free); S'(0) is issued after the last chunk's GEMMs, into the S'
@@ -643,9 +653,10 @@ __global__ void __launch_bounds__(FwdCfg<D>::THREADS, 1)
       }
       if (nmax > 0) {
         mbar_wait(k_full + 8 * (0), 0);
-        tc_fence_after();
         for (int t = 0; t < NT; ++t) {
           if (tl[t].nblk == 0) continue;
+          mbar_wait(q_full + 8 * (t), 0);  // Q_1 lands after K'(0)
+          tc_fence_after();
           issue_s(t, 0);
           tc_commit(s_full + 8 * (t));
         }
