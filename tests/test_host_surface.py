@@ -202,3 +202,24 @@ def test_recovery_relation():
         lhs = (s @ m).mean(axis=1) / (1.0 - beta)
         rhs = s.mean(axis=1) / alpha
         assert np.abs(lhs - rhs).max() <= 1e-12 * np.abs(rhs).max() * s2
+
+
+def test_bench_reference_arm_passes_thread_count(monkeypatch):
+    """The reference arm hands its thread count to pasa_attention explicitly
+    (AttnOptions::threads, parallel.hpp:20-32): under torchrun OMP_NUM_THREADS=1 would
+    otherwise pin the reference to one thread while the line reports every core."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+
+    seen = {}
+
+    class FakeRef:
+        def pasa(self, pb, beta, policy, threads=0):
+            seen["threads"] = threads
+            return np.zeros(pb.q.shape)
+
+    q = np.zeros((1, 1, 128, 128))
+    monkeypatch.setenv("OMP_NUM_THREADS", "1")
+    dt, _ = bench.time_reference_step(FakeRef(), q, q, q, 7)
+    assert seen["threads"] == 7 and dt >= 0.0
